@@ -1,0 +1,121 @@
+// ref_probe.cpp — thin extern "C" probe over the reference library's C++
+// internals, linked into oracle/_ref/libhetplan_probe.so together with the
+// reference objects compiled from /root/reference/proj/src (see Makefile).
+//
+// TEST INFRASTRUCTURE ONLY: used by tests/ to pin the C restatement
+// (hetplan_oracle.c) to the reference itself, function by function.
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "hetplan/grouping.hpp"
+#include "hetplan/partition.hpp"
+#include "hetplan/profile.hpp"
+
+using namespace hetplan;
+
+extern "C" {
+
+// solve_grouping_topk (P/src/grouping.cpp:269-335) with one device per unit
+// (tp_dim = 1): device i lives on node node_id[i] with local rank = its index
+// among that node's devices, type "T<type_id>".
+// Returns 0 ok, 3 InfeasibleError, 6 InvalidArgumentError, 5 other.
+int ref_solve_grouping(int n, const double* power, const double* memory, const int* type_id,
+                       const int* node_id, int n_microbatches, double min_mem,
+                       int exact_threshold, long long node_budget, int top_k, int* out_count,
+                       int* out_rgs, double* out_obj, double* out_z, int* out_optimal,
+                       long long* out_visited) {
+  try {
+    GroupingProblem pb;
+    std::vector<int> next_rank(1024, 0);
+    for (int i = 0; i < n; ++i) {
+      const int node = node_id[i];
+      pb.devices.push_back({DeviceId{node, next_rank[node]++},
+                            "T" + std::to_string(type_id[i]), power[i], memory[i]});
+    }
+    pb.tp_dim = 1;
+    pb.n_microbatches = n_microbatches;
+    pb.min_mem = min_mem;
+    pb.big_l = 0;
+    pb.exact_threshold = exact_threshold;
+    pb.node_budget = node_budget;
+    pb.top_k = top_k;
+    auto sols = solve_grouping_topk(pb);
+    *out_count = static_cast<int>(sols.size());
+    for (size_t k = 0; k < sols.size(); ++k) {
+      // Unit order in the solver is the DeviceId order; map back to input order.
+      std::vector<int> order(n);
+      for (int i = 0; i < n; ++i) order[i] = i;
+      std::sort(order.begin(), order.end(), [&](int a, int b) {
+        return pb.devices[a].id < pb.devices[b].id;
+      });
+      for (int i = 0; i < n; ++i) {
+        out_rgs[k * n + i] = sols[k].assignment.at(pb.devices[i].id);
+      }
+      out_obj[k] = sols[k].objective;
+      out_z[k] = sols[k].z;
+      *out_optimal = sols[k].optimal ? 1 : 0;
+      *out_visited = sols[k].nodes_visited;
+    }
+    return 0;
+  } catch (const InfeasibleError&) {
+    return 3;
+  } catch (const InvalidArgumentError&) {
+    return 6;
+  } catch (...) {
+    return 5;
+  }
+}
+
+// balance_workload (P/src/partition.cpp:51-110) with a profile table built
+// from prof[s*n_bits + b] (<= 0: entry absent), one GPU type per stage.
+int ref_balance_workload(int n_layers, int P, int n_bits, const double* prof,
+                         const double* mem_capacity, const int* stage_index, int tp, double ppb,
+                         double pab, double opt_mult, int k_total, int k_group,
+                         int allow_zero, int* out_layers, double* out_times,
+                         double* out_bottleneck) {
+  try {
+    ProfileTable table;
+    for (int s = 0; s < P; ++s) {
+      for (int b = 0; b < n_bits; ++b) {
+        if (prof[s * n_bits + b] > 0) {
+          table.add("S" + std::to_string(s), tp, 1 << b, prof[s * n_bits + b]);
+        }
+      }
+    }
+    ModelConfig cfg;
+    cfg.n_layers = n_layers;
+    cfg.per_layer_param_bytes = ppb;
+    cfg.per_layer_activation_bytes = pab;
+    cfg.optimizer_multiplier = opt_mult;
+    cfg.n_microbatches = k_total;
+    MemoryModel mem = MemoryModel::from_config(cfg);
+    PartitionProblem pp;
+    pp.n_layers = n_layers;
+    pp.n_microbatches = k_group;
+    pp.tp_dim = tp;
+    pp.profile = &table;
+    pp.memmodel = &mem;
+    pp.config = &cfg;
+    pp.allow_zero_layers = allow_zero != 0;
+    for (int s = 0; s < P; ++s) {
+      pp.stages.push_back({"S" + std::to_string(s), 1.0, mem_capacity[s], stage_index[s]});
+    }
+    Partition part = balance_workload(pp);
+    for (int s = 0; s < P; ++s) {
+      out_layers[s] = part.layers[s];
+      out_times[s] = part.stage_times[s];
+    }
+    *out_bottleneck = part.bottleneck;
+    return 0;
+  } catch (const InfeasibleError&) {
+    return 3;
+  } catch (const InvalidArgumentError&) {
+    return 6;
+  } catch (...) {
+    return 5;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,217 @@
+"""ctypes binding of the reference C ABI (P/include/hetplan/c_api.h).
+
+The same binding drives both the product library (``libhetplan_b200.so``, the
+drop-in) and the reference library compiled from its own sources
+(``oracle/_ref/libhetplan.so``, test/baseline only) — they export the identical
+ABI, which is the point of the drop-in boundary. Function names and error
+behaviour follow the reference: every call returns an ``hp_status``
+(c_api.h:41-48) and failures raise :class:`HetplanError` carrying the status and
+``hp_last_error()`` text.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+HP_OK = 0
+HP_PARSE_ERROR = 2
+HP_INFEASIBLE = 3
+HP_UNRECOVERABLE = 4
+HP_INTERNAL_ERROR = 5
+HP_INVALID_ARGUMENT = 6
+
+STATUS_NAMES = {
+    HP_OK: "HP_OK",
+    HP_PARSE_ERROR: "HP_PARSE_ERROR",
+    HP_INFEASIBLE: "HP_INFEASIBLE",
+    HP_UNRECOVERABLE: "HP_UNRECOVERABLE",
+    HP_INTERNAL_ERROR: "HP_INTERNAL_ERROR",
+    HP_INVALID_ARGUMENT: "HP_INVALID_ARGUMENT",
+}
+
+
+class HetplanError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {message}")
+        self.status = status
+        self.message = message
+
+
+class hp_plan_options(C.Structure):
+    """c_api.h:76-87, field for field."""
+
+    _fields_ = [
+        ("tp_dims", C.POINTER(C.c_int)),
+        ("n_tp_dims", C.c_int),
+        ("min_mem_override", C.c_double),
+        ("exact_threshold", C.c_int),
+        ("node_budget", C.c_longlong),
+        ("top_k", C.c_int),
+        ("sync_overlap_max", C.c_int),
+        ("validate_with_sim", C.c_int),
+        ("derive_power", C.c_int),
+        ("power_reference", C.c_char_p),
+    ]
+
+
+@dataclass
+class PlanOptions:
+    tp_dims: Optional[Sequence[int]] = None
+    min_mem_override: float = 0.0
+    exact_threshold: int = 8
+    node_budget: int = 5_000_000
+    top_k: int = 1
+    sync_overlap_max: bool = False
+    validate_with_sim: bool = False
+    derive_power: bool = False
+    power_reference: Optional[str] = None
+
+
+_VP = C.c_void_p
+
+
+class HetplanLib:
+    """One loaded C-ABI library (product or reference)."""
+
+    def __init__(self, path: str):
+        if not os.path.exists(path):
+            raise FileNotFoundError(path)
+        # RTLD_LOCAL (the ctypes default): product and reference export the same
+        # symbols and must not interpose on each other.
+        self.path = path
+        self.lib = C.CDLL(path, mode=getattr(os, "RTLD_LOCAL", 0) | getattr(os, "RTLD_NOW", 2))
+        L = self.lib
+        L.hp_version.restype = C.c_char_p
+        L.hp_last_error.restype = C.c_char_p
+        L.hp_string_free.argtypes = [C.c_void_p]
+        for name in ("hp_cluster_parse", "hp_model_parse", "hp_profile_parse",
+                     "hp_cluster_load_file", "hp_model_load_file", "hp_profile_load_file",
+                     "hp_plan_load_file"):
+            getattr(L, name).argtypes = [C.c_char_p, C.POINTER(_VP)]
+            getattr(L, name).restype = C.c_int
+        L.hp_profile_synth.argtypes = [_VP, C.c_double, C.c_int, C.POINTER(_VP)]
+        L.hp_profile_synth.restype = C.c_int
+        L.hp_cluster_device_count.argtypes = [_VP]
+        L.hp_cluster_device_count.restype = C.c_int
+        L.hp_plan_options_init.argtypes = [C.POINTER(hp_plan_options)]
+        L.hp_plan_compute.argtypes = [_VP, _VP, _VP, C.POINTER(hp_plan_options), C.POINTER(_VP)]
+        L.hp_plan_compute.restype = C.c_int
+        for name in ("hp_plan_to_json", "hp_plan_explain"):
+            getattr(L, name).argtypes = [_VP, C.POINTER(C.c_void_p)]
+            getattr(L, name).restype = C.c_int
+        L.hp_estimate_to_json.argtypes = [_VP, _VP, _VP, _VP, C.POINTER(C.c_void_p)]
+        L.hp_estimate_to_json.restype = C.c_int
+        L.hp_profile_write_file.argtypes = [_VP, C.c_char_p]
+        L.hp_profile_write_file.restype = C.c_int
+        L.hp_plan_write_file.argtypes = [_VP, C.c_char_p]
+        L.hp_plan_write_file.restype = C.c_int
+        for name in ("hp_cluster_free", "hp_model_free", "hp_profile_free", "hp_plan_free"):
+            getattr(L, name).argtypes = [_VP]
+            getattr(L, name).restype = None
+
+    # -- helpers ---------------------------------------------------------
+    def _check(self, status: int) -> None:
+        if status != HP_OK:
+            raise HetplanError(status, self.lib.hp_last_error().decode())
+
+    def _take_string(self, ptr: C.c_void_p) -> str:
+        s = C.cast(ptr, C.c_char_p).value.decode()
+        self.lib.hp_string_free(ptr)
+        return s
+
+    def version(self) -> str:
+        return self.lib.hp_version().decode()
+
+    # -- handles ---------------------------------------------------------
+    def cluster_parse(self, text: str) -> "Handle":
+        h = _VP()
+        self._check(self.lib.hp_cluster_parse(text.encode(), C.byref(h)))
+        return Handle(self, h, "hp_cluster_free")
+
+    def model_parse(self, text: str) -> "Handle":
+        h = _VP()
+        self._check(self.lib.hp_model_parse(text.encode(), C.byref(h)))
+        return Handle(self, h, "hp_model_free")
+
+    def profile_parse(self, text: str) -> "Handle":
+        h = _VP()
+        self._check(self.lib.hp_profile_parse(text.encode(), C.byref(h)))
+        return Handle(self, h, "hp_profile_free")
+
+    def profile_synth(self, cluster: "Handle", base_seconds: float, max_layers: int) -> "Handle":
+        h = _VP()
+        self._check(self.lib.hp_profile_synth(cluster.ptr, base_seconds, max_layers, C.byref(h)))
+        return Handle(self, h, "hp_profile_free")
+
+    def plan_compute(self, cluster: "Handle", model: "Handle", profile: "Handle",
+                     options: Optional[PlanOptions] = None) -> "Handle":
+        o = hp_plan_options()
+        self.lib.hp_plan_options_init(C.byref(o))
+        keep = []
+        if options is not None:
+            if options.tp_dims is not None:
+                arr = (C.c_int * len(options.tp_dims))(*options.tp_dims)
+                keep.append(arr)
+                o.tp_dims = C.cast(arr, C.POINTER(C.c_int))
+                o.n_tp_dims = len(options.tp_dims)
+            o.min_mem_override = options.min_mem_override
+            o.exact_threshold = options.exact_threshold
+            o.node_budget = options.node_budget
+            o.top_k = options.top_k
+            o.sync_overlap_max = int(options.sync_overlap_max)
+            o.validate_with_sim = int(options.validate_with_sim)
+            o.derive_power = int(options.derive_power)
+            if options.power_reference is not None:
+                b = options.power_reference.encode()
+                keep.append(b)
+                o.power_reference = b
+        h = _VP()
+        self._check(self.lib.hp_plan_compute(cluster.ptr, model.ptr, profile.ptr, C.byref(o),
+                                             C.byref(h)))
+        return Handle(self, h, "hp_plan_free")
+
+    def plan_to_json(self, plan: "Handle") -> str:
+        p = C.c_void_p()
+        self._check(self.lib.hp_plan_to_json(plan.ptr, C.byref(p)))
+        return self._take_string(p)
+
+    def plan_explain(self, plan: "Handle") -> str:
+        p = C.c_void_p()
+        self._check(self.lib.hp_plan_explain(plan.ptr, C.byref(p)))
+        return self._take_string(p)
+
+    def estimate_to_json(self, plan, cluster, model, profile) -> str:
+        p = C.c_void_p()
+        self._check(self.lib.hp_estimate_to_json(plan.ptr, cluster.ptr, model.ptr, profile.ptr,
+                                                 C.byref(p)))
+        return self._take_string(p)
+
+    def plan_json(self, cluster_text: str, model_text: str, max_layers: int,
+                  options: Optional[PlanOptions] = None, base_seconds: float = 0.05) -> str:
+        """Convenience: parse, synthesize the profile, plan, serialize."""
+        cl = self.cluster_parse(cluster_text)
+        md = self.model_parse(model_text)
+        pr = self.profile_synth(cl, base_seconds, max_layers)
+        return self.plan_to_json(self.plan_compute(cl, md, pr, options))
+
+
+class Handle:
+    """Owns one opaque hp_* handle; freed with the matching hp_*_free."""
+
+    def __init__(self, lib: HetplanLib, ptr: C.c_void_p, free_name: str):
+        self.lib = lib
+        self.ptr = ptr
+        self._free = getattr(lib.lib, free_name)
+
+    def close(self) -> None:
+        if self.ptr:
+            self._free(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,1828 @@
+// hpk_grouping.cu — B200 grouping search (the hot loop of the reference
+// planner: dfs() in P/src/grouping.cpp:135-202 under solve_grouping_topk
+// :269-335; P = /root/reference/proj).
+//
+// Two engines, both on the GPU, both exact (bit-identical winner, visits and
+// optimal flag):
+//
+//  * Wave engine (hpk_wave_kernel): one persistent cooperative kernel searches
+//    a batch of problems. The lexicographic (preorder) DFS is cut into an
+//    ordered list of segments (subtrees). Each wave every warp runs one segment
+//    (a warp-cooperative DFS: lane g owns DP group g) with the front's exact
+//    cutoff and a visit cap; unfinished segments are split speculatively into a
+//    prefix record plus the remainder's subtrees; a per-problem scheduler CTA
+//    then commits the longest prefix of the list whose runs are exact (cutoff
+//    at their position unchanged), applying the budget cut exactly where the
+//    serial DFS would abort. A prefix record whose cutoff turned out stale is
+//    re-run with an end marker; the ancestor it now prunes deletes the pieces
+//    beneath it. Exactness argument and data layout: DESIGN.md.
+//
+//  * Serial replica (hpk_serial_kernel): one thread per problem replays the
+//    reference DFS statement by statement (including the += / -= group sums
+//    and top_k bookkeeping). Used when a problem is outside the wave engine's
+//    contract (n > 64 units, top_k > 1, or unit powers / memories whose sums
+//    are not exact in fp64 so the reference's sums are path dependent).
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "hetplan_b200.h"
+#include "hpk_common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace hpk {
+
+constexpr int MAXN = HPK_MAX_UNITS;  // 64 units -> lanes own groups g and g+32
+constexpr int WARPS_PER_BLOCK = 8;
+constexpr int BLOCK_THREADS = WARPS_PER_BLOCK * 32;
+constexpr uint8_t KIND_FULL = 0;
+constexpr uint8_t KIND_PREFIX = 1;
+
+// ------------------------------------------------------------------ layout
+
+struct GProb {
+  int n, K, exact_mem, pad0;
+  long long budget;  // < 0: unlimited (exhaustive mode)
+  double min_mem;
+  double p[MAXN], m[MAXN];
+  int tkey[MAXN], nkey[MAXN];
+  double f[MAXN + 2];   // f[d] = 1 - (d-1)/(K+d-1): Eq. (2) factor (grouping.cpp:103-108)
+  double R[MAXN + 1];   // exact suffix sums of unit powers (contract: exact)
+  double RM[MAXN + 1];  // remaining_mem from d, serial as grouping.cpp:156-160
+};
+
+struct __align__(16) Entry {
+  uint8_t u[MAXN];         // segment root (entered by this segment's run)
+  uint8_t end[MAXN];       // PREFIX: end marker (first node NOT in the segment)
+  uint8_t stop[MAXN];      // run output: next node to enter when the cap hit
+  uint8_t best_rgs[MAXN];  // run output: best leaf
+  double cutoff_used;
+  double m;                // max feasible leaf objective (-1: none)
+  double best_obj;
+  long long visits;
+  int best_G;
+  int a_star;              // PREFIX re-run: depth of the pruned ancestor of `end`
+  uint8_t du, dend, dstop, kind;
+  uint8_t ran, finished, has_best, ran_now;
+  uint8_t capped, pad[7];
+};
+
+struct GState {
+  double C;          // exact cutoff at the commit front
+  long long V;       // committed visits
+  double best_obj;
+  int best_G, has_best;
+  int cur, head, len;
+  int done, aborted, rerun_pending, pad;
+  long long rerun_cap;
+  double seed_obj, seed_z;
+  int seed_ix, waves;
+  long long runs, run_visits;
+  int max_list, error;
+  uint8_t best_rgs[MAXN];
+  uint8_t seed_rgs[MAXN];
+};
+
+struct RunItem {
+  int problem, index;
+  long long cap;
+};
+
+struct RunQueue {
+  int len, head;
+  int pad[2];
+};
+
+struct KParams {
+  GProb* probs;
+  GState* states;
+  Entry* lists;       // [P][2][lcap]
+  int* scratch;       // [P][lcap + 1]
+  RunQueue* queues;   // [2]
+  RunItem* items;     // [2][qcap]
+  int* active;        // problems still running
+  int* err;           // watchdog flags
+  int n_problems;
+  int lcap, qcap, qmax;
+  long long seg_cap;
+  int max_waves;
+};
+
+__device__ __forceinline__ Entry* list_ptr(const KParams& kp, int p, int buf) {
+  return kp.lists + ((size_t)p * 2 + buf) * kp.lcap;
+}
+
+// --------------------------------------------------------------- warp DFS
+
+struct WarpSmem {
+  double S[MAXN + 1];    // approx sum of Eq.(2) effective powers at each level
+  double DEF[MAXN + 1];  // approx memory deficit at each level
+  uint8_t path[MAXN];
+  uint8_t nxt[MAXN + 1];
+  uint8_t Gat[MAXN + 1];
+  uint8_t endp[MAXN];
+  uint8_t best[MAXN];
+};
+
+enum : int { DEC_PASS = 0, DEC_PRUNE = 1, DEC_EXACT = 2 };
+
+constexpr double kEps52 = 2.220446049250313e-16;  // 2^-52
+
+// Per-lane group registers: lane owns groups lane and lane+32.
+struct Groups {
+  double gp[2], gm[2];
+  int gc[2];
+};
+
+__device__ __forceinline__ void add_unit(Groups& g, int lane, int grp, double up, double um) {
+  if ((grp & 31) == lane) {
+    const int s = grp >> 5;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      if (k == s) {
+        if (g.gc[k] == 0) {  // new group: push_back (grouping.cpp:180-182)
+          g.gp[k] = up;
+          g.gm[k] = um;
+          g.gc[k] = 1;
+        } else {             // += (grouping.cpp:184-186)
+          g.gp[k] += up;
+          g.gm[k] += um;
+          g.gc[k] += 1;
+        }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void remove_unit(Groups& g, int lane, int grp, double up, double um) {
+  if ((grp & 31) == lane) {
+    const int s = grp >> 5;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      if (k == s) {
+        if (g.gc[k] == 1) {  // pop_back (grouping.cpp:192-194)
+          g.gp[k] = 0;
+          g.gm[k] = 0;
+          g.gc[k] = 0;
+        } else {             // -= (grouping.cpp:196-198); exact under the contract
+          g.gp[k] -= up;
+          g.gm[k] -= um;
+          g.gc[k] -= 1;
+        }
+      }
+    }
+  }
+}
+
+// eff of this lane's slot k (0 if the group does not exist)
+__device__ __forceinline__ double slot_eff(const GProb& P, const Groups& g, int k) {
+  return g.gc[k] > 0 ? g.gp[k] * P.f[g.gc[k]] : 0.0;
+}
+__device__ __forceinline__ double slot_def(const GProb& P, const Groups& g, int k) {
+  if (g.gc[k] == 0) return 0.0;
+  const double d = P.min_mem - g.gm[k];
+  return d > 0.0 ? d : 0.0;  // std::max(0.0, d)
+}
+
+// Exact node check in the reference's serial order (grouping.cpp:154-169) for
+// the node whose units 0..next-1 are applied. Warp-uniform result.
+__device__ bool exact_passes(const GProb& P, const Groups& g, int G, int next, double cut) {
+  double bound = 0;
+  for (int gi = 0; gi < G; ++gi) {
+    const int k = gi >> 5;
+    const double e = shfl(k == 0 ? slot_eff(P, g, 0) : slot_eff(P, g, 1), gi & 31);
+    bound += e;
+  }
+  for (int i = next; i < P.n; ++i) bound += P.p[i];
+  if (cut >= 0 && bound < cut) return false;
+  double deficit = 0;
+  for (int gi = 0; gi < G; ++gi) {
+    const int k = gi >> 5;
+    const double dv = shfl(k == 0 ? slot_def(P, g, 0) : slot_def(P, g, 1), gi & 31);
+    deficit += dv;
+  }
+  return !(deficit > P.RM[next]);
+}
+
+// Filter decision for a node given approximate sums; margins bound the gap
+// between the approximations and the reference's serial fp64 sums.
+__device__ __forceinline__ int decide(const GProb& P, double A, double Tabs, double D,
+                                      double Dabs, int Gn, int next, double cut) {
+  int db = DEC_PASS;
+  if (cut >= 0) {
+    const double mb = (double)(Gn + (P.n - next) + 16) * kEps52 * Tabs;
+    if (A + mb < cut) db = DEC_PRUNE;
+    else if (A - mb >= cut) db = DEC_PASS;
+    else db = DEC_EXACT;
+  }
+  const double rem = P.RM[next];
+  int dd;
+  if (P.exact_mem) {
+    dd = D > rem ? DEC_PRUNE : DEC_PASS;
+  } else {
+    const double md = (double)(Gn + 8) * kEps52 * (Dabs + rem);
+    if (D - md > rem) dd = DEC_PRUNE;
+    else if (D + md <= rem) dd = DEC_PASS;
+    else dd = DEC_EXACT;
+  }
+  if (db == DEC_PRUNE || dd == DEC_PRUNE) return DEC_PRUNE;
+  if (db == DEC_PASS && dd == DEC_PASS) return DEC_PASS;
+  return DEC_EXACT;
+}
+
+struct RunOut {
+  long long visits;
+  double m;
+  bool finished, has_best;
+  double best_obj;
+  int best_G, a_star, dstop;
+};
+
+// DFS of subtree(E.u) in preorder (PREFIX: stopping before E.end), cap visits.
+__device__ RunOut run_segment(const GProb& P, const Entry* E, Entry* Eout, double C,
+                              long long cap, WarpSmem* sm, int lane, int* err) {
+  const int n = P.n;
+  const int du = E->du;
+  const bool prefix = E->kind == KIND_PREFIX;
+  if (cap <= 0) {  // budget already exhausted: the reference aborts before entering u
+    RunOut z;
+    z.visits = 0;
+    z.m = -1.0;
+    z.finished = false;
+    z.has_best = false;
+    z.best_obj = 0;
+    z.best_G = 0;
+    z.a_star = -1;
+    z.dstop = 0;
+    return z;
+  }
+  const int dend = prefix ? E->dend : 0;
+  for (int i = lane; i < du; i += 32) sm->path[i] = E->u[i];
+  if (prefix)
+    for (int i = lane; i < dend; i += 32) sm->endp[i] = E->end[i];
+  __syncwarp();
+
+  Groups g;
+  g.gp[0] = g.gp[1] = 0;
+  g.gm[0] = g.gm[1] = 0;
+  g.gc[0] = g.gc[1] = 0;
+  int G = 0;
+  if (lane == 0) sm->Gat[0] = 0;
+  for (int i = 0; i + 1 < du; ++i) {
+    const int grp = sm->path[i];
+    add_unit(g, lane, grp, P.p[i], P.m[i]);
+    if (grp == G) ++G;
+    if (lane == 0) sm->Gat[i + 1] = (uint8_t)G;
+  }
+  RunOut o;
+  o.visits = 0;
+  o.m = -1.0;
+  o.finished = false;
+  o.has_best = false;
+  o.best_obj = 0;
+  o.best_G = 0;
+  o.a_star = -1;
+  o.dstop = 0;
+  double cut = C;
+  int match = prefix ? du : -1;
+  long long iters = 0;
+  const long long max_iters = 4 * cap + 4 * MAXN + 64;  // watchdog (never hit when correct)
+
+  // Enter the segment root u.
+  {
+    const int i = du - 1;
+    const int grp = sm->path[i];
+    add_unit(g, lane, grp, P.p[i], P.m[i]);
+    if (grp == G) ++G;
+    if (lane == 0) sm->Gat[du] = (uint8_t)G;
+    o.visits = 1;
+  }
+  int d = du;
+  if (d == n) {  // the root is a leaf (grouping.cpp:138-149)
+    bool infeas = false;
+    double z = INFINITY;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      if (g.gc[k] > 0) {
+        if (g.gm[k] < P.min_mem) infeas = true;
+        const double e = slot_eff(P, g, k);
+        z = e < z ? e : z;
+      }
+    }
+    const bool any_infeas = __any_sync(HPK_FULL_MASK, infeas);
+    z = warp_min(z);
+    if (!any_infeas) {
+      const double obj = (double)G * z;
+      o.has_best = true;
+      o.best_obj = obj;
+      o.best_G = G;
+      o.m = obj;
+      for (int i = lane; i < n; i += 32) sm->best[i] = sm->path[i];
+    }
+    o.finished = true;
+    goto done;
+  }
+  {  // node check of u itself
+    double le = slot_eff(P, g, 0) + slot_eff(P, g, 1);
+    double ld = slot_def(P, g, 0) + slot_def(P, g, 1);
+    const double S = warp_sum_approx(le);
+    const double DEF = warp_sum_approx(ld);
+    const double A = S + P.R[d];
+    int dec = decide(P, A, A, DEF, DEF, G, d, cut);
+    if (dec == DEC_EXACT) dec = exact_passes(P, g, G, d, cut) ? DEC_PASS : DEC_PRUNE;
+    if (dec == DEC_PRUNE) {
+      if (prefix) o.a_star = du;
+      o.finished = true;
+      goto done;
+    }
+    if (lane == 0) {
+      sm->S[d] = S;
+      sm->DEF[d] = DEF;
+      sm->nxt[d] = 0;
+    }
+    __syncwarp();
+  }
+
+  while (true) {
+    if (++iters > max_iters) {
+      if (lane == 0) atomicOr(err, 1);
+      o.finished = true;
+      break;
+    }
+    if (d == n - 1) {
+      // ---- leaf batch: children c = c0..G are leaves (unit n-1) ----
+      const int c0 = sm->nxt[d];
+      int count = G + 1 - c0;
+      bool end_hit = false;
+      if (prefix && match == d) {
+        const int ec = sm->endp[d];  // dend == n here
+        if (ec - c0 < count) {
+          count = ec - c0 > 0 ? ec - c0 : 0;
+          end_hit = true;
+        }
+      }
+      bool cap_hit = false;
+      if ((long long)count > cap - o.visits) {
+        count = (int)(cap - o.visits);
+        cap_hit = true;
+        end_hit = false;
+      }
+      if (count > 0) {
+        const double up = P.p[n - 1], um = P.m[n - 1];
+        bool inf_k[2];
+        double eff_k[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const bool valid = g.gc[k] > 0;
+          inf_k[k] = valid && g.gm[k] < P.min_mem;
+          eff_k[k] = valid ? slot_eff(P, g, k) : INFINITY;
+        }
+        const int n_inf = __popc(__ballot_sync(HPK_FULL_MASK, inf_k[0])) +
+                          __popc(__ballot_sync(HPK_FULL_MASK, inf_k[1]));
+        // min1 / idx1 / min2 over existing groups
+        double m1, m2;
+        int i1;
+        if (eff_k[0] <= eff_k[1]) {
+          m1 = eff_k[0];
+          i1 = lane;
+          m2 = eff_k[1];
+        } else {
+          m1 = eff_k[1];
+          i1 = lane + 32;
+          m2 = eff_k[0];
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          const double om1 = __shfl_xor_sync(HPK_FULL_MASK, m1, off);
+          const int oi1 = __shfl_xor_sync(HPK_FULL_MASK, i1, off);
+          const double om2 = __shfl_xor_sync(HPK_FULL_MASK, m2, off);
+          if (om1 < m1 || (om1 == m1 && oi1 < i1)) {
+            m2 = m1 < om2 ? m1 : om2;
+            m1 = om1;
+            i1 = oi1;
+          } else {
+            m2 = om1 < m2 ? om1 : m2;
+          }
+        }
+        // each lane evaluates the children it owns (c = lane, lane+32)
+        double best_o = -1.0;
+        int best_Gc = 0, best_c = 1 << 30;
+        double mx = -1.0;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int c = lane + 32 * k;
+          if (c >= c0 && c < c0 + count) {
+            double eff_new, mem_new, other_min;
+            int others_inf, Gc;
+            if (c < G) {
+              eff_new = (g.gp[k] + up) * P.f[g.gc[k] + 1];
+              mem_new = g.gm[k] + um;
+              others_inf = n_inf - (inf_k[k] ? 1 : 0);
+              other_min = (c == i1) ? m2 : m1;
+              Gc = G;
+            } else {  // c == G: new singleton group
+              eff_new = up * P.f[1];
+              mem_new = um;
+              others_inf = n_inf;
+              other_min = m1;
+              Gc = G + 1;
+            }
+            if (others_inf == 0 && !(mem_new < P.min_mem)) {
+              const double z = eff_new < other_min ? eff_new : other_min;
+              const double obj = (double)Gc * z;
+              mx = obj > mx ? obj : mx;
+              if (best_o < 0 || key_better(obj, Gc, c, best_o, best_Gc, best_c)) {
+                best_o = obj;
+                best_Gc = Gc;
+                best_c = c;
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          const double oo = __shfl_xor_sync(HPK_FULL_MASK, best_o, off);
+          const int og = __shfl_xor_sync(HPK_FULL_MASK, best_Gc, off);
+          const int oc = __shfl_xor_sync(HPK_FULL_MASK, best_c, off);
+          if (oo >= 0 && (best_o < 0 || key_better(oo, og, oc, best_o, best_Gc, best_c))) {
+            best_o = oo;
+            best_Gc = og;
+            best_c = oc;
+          }
+          const double om = __shfl_xor_sync(HPK_FULL_MASK, mx, off);
+          mx = om > mx ? om : mx;
+        }
+        o.visits += count;
+        if (best_o >= 0) {
+          if (!o.has_best || best_o > o.best_obj ||
+              (best_o == o.best_obj && best_Gc < o.best_G)) {
+            o.has_best = true;
+            o.best_obj = best_o;
+            o.best_G = best_Gc;
+            for (int i = lane; i < n - 1; i += 32) sm->best[i] = sm->path[i];
+            if (lane == 0) sm->best[n - 1] = (uint8_t)best_c;
+          }
+          o.m = mx > o.m ? mx : o.m;
+          cut = mx > cut ? mx : cut;
+        }
+      }
+      if (cap_hit) {
+        for (int i = lane; i < d; i += 32) Eout->stop[i] = sm->path[i];
+        if (lane == 0) Eout->stop[d] = (uint8_t)(c0 + count);
+        o.dstop = d + 1;
+        o.finished = false;
+        break;
+      }
+      if (end_hit) {
+        o.finished = true;
+        break;
+      }
+      if (lane == 0) sm->nxt[d] = (uint8_t)(G + 1);
+      __syncwarp();
+    }
+    const int c = sm->nxt[d];
+    if (c > G) {  // node exhausted: pop unit d-1
+      if (d == du) {
+        o.finished = true;
+        break;
+      }
+      const int grp = sm->path[d - 1];
+      remove_unit(g, lane, grp, P.p[d - 1], P.m[d - 1]);
+      G = sm->Gat[d - 1];
+      --d;
+      if (match > d) match = d;
+      continue;
+    }
+    if (prefix && match == d) {
+      const int ec = sm->endp[d];
+      if (c > ec || (c == ec && d + 1 == dend)) {
+        o.finished = true;
+        break;
+      }
+    }
+    if (o.visits >= cap) {
+      for (int i = lane; i < d; i += 32) Eout->stop[i] = sm->path[i];
+      if (lane == 0) Eout->stop[d] = (uint8_t)c;
+      o.dstop = d + 1;
+      o.finished = false;
+      break;
+    }
+    o.visits += 1;
+    if (lane == 0) sm->nxt[d] = (uint8_t)(c + 1);
+    // ---- check child c (internal node at depth d+1) on its owner lane ----
+    int dec;
+    {
+      const int owner = c & 31, k = c >> 5;
+      int ldec = 0;
+      if (lane == owner) {
+        const double up = P.p[d], um = P.m[d];
+        double eff_old, eff_new, def_old, def_new;
+        int Gc;
+        const int gck = k == 0 ? g.gc[0] : g.gc[1];
+        const double gpk = k == 0 ? g.gp[0] : g.gp[1];
+        const double gmk = k == 0 ? g.gm[0] : g.gm[1];
+        if (c < G) {
+          eff_old = gpk * P.f[gck];
+          eff_new = (gpk + up) * P.f[gck + 1];
+          const double d0 = P.min_mem - gmk;
+          def_old = d0 > 0.0 ? d0 : 0.0;
+          const double d1 = P.min_mem - (gmk + um);
+          def_new = d1 > 0.0 ? d1 : 0.0;
+          Gc = G;
+        } else {
+          eff_old = 0;
+          eff_new = up * P.f[1];
+          def_old = 0;
+          const double d1 = P.min_mem - um;
+          def_new = d1 > 0.0 ? d1 : 0.0;
+          Gc = G + 1;
+        }
+        const double Sd = sm->S[d], Dd = sm->DEF[d];
+        const double R = P.R[d + 1];
+        const double A = ((Sd - eff_old) + eff_new) + R;
+        const double Tabs = Sd + eff_new + R;
+        const double Dn = (Dd - def_old) + def_new;
+        ldec = decide(P, A, Tabs, Dn, Dd + def_new, Gc, d + 1, cut);
+      }
+      dec = shfl(ldec, owner);
+    }
+    if (dec == DEC_EXACT) {
+      add_unit(g, lane, c, P.p[d], P.m[d]);
+      const int Gc = c == G ? G + 1 : G;
+      dec = exact_passes(P, g, Gc, d + 1, cut) ? DEC_PASS : DEC_PRUNE;
+      remove_unit(g, lane, c, P.p[d], P.m[d]);
+    }
+    if (dec == DEC_PRUNE) {
+      if (prefix && match == d && c == sm->endp[d] && o.a_star < 0) o.a_star = d + 1;
+      continue;
+    }
+    // ---- descend into child c ----
+    if (lane == 0) sm->path[d] = (uint8_t)c;
+    add_unit(g, lane, c, P.p[d], P.m[d]);
+    if (c == G) ++G;
+    if (prefix && match == d && c == sm->endp[d]) match = d + 1;
+    ++d;
+    {
+      const double le = slot_eff(P, g, 0) + slot_eff(P, g, 1);
+      const double ld = slot_def(P, g, 0) + slot_def(P, g, 1);
+      const double S = warp_sum_approx(le);
+      const double DEF = warp_sum_approx(ld);
+      if (lane == 0) {
+        sm->Gat[d] = (uint8_t)G;
+        sm->S[d] = S;
+        sm->DEF[d] = DEF;
+        sm->nxt[d] = 0;
+      }
+      __syncwarp();
+    }
+  }
+done:
+  __syncwarp();
+  if (o.has_best)
+    for (int i = lane; i < n; i += 32) Eout->best_rgs[i] = sm->best[i];
+  __syncwarp();
+  return o;
+}
+
+// --------------------------------------------------------------- scheduler
+
+__device__ __forceinline__ bool is_prefix_of(const uint8_t* a, int la, const uint8_t* b, int lb) {
+  if (la > lb) return false;
+  for (int i = 0; i < la; ++i)
+    if (a[i] != b[i]) return false;
+  return true;
+}
+
+// number of remainder pieces of subtree(u) after stop point q
+__device__ int n_pieces(const Entry& e) {
+  int pm[MAXN + 1];  // pm[d] = #groups of q[0..d)
+  pm[0] = 0;
+  for (int i = 0; i < e.dstop; ++i) pm[i + 1] = max(pm[i], (int)e.stop[i] + 1);
+  int cnt = 1;
+  for (int d = e.dstop - 1; d >= (int)e.du; --d) cnt += pm[d] - e.stop[d];
+  return cnt;
+}
+
+// piece k (0-based) of the remainder: writes its path into out, returns depth
+__device__ int piece_path(const Entry& e, int k, uint8_t* out) {
+  const int dq = e.dstop;
+  if (k == 0) {
+    for (int i = 0; i < dq; ++i) out[i] = e.stop[i];
+    return dq;
+  }
+  int pm[MAXN + 1];
+  pm[0] = 0;
+  for (int i = 0; i < dq; ++i) pm[i + 1] = max(pm[i], (int)e.stop[i] + 1);
+  int idx = k - 1;
+  for (int d = dq - 1; d >= (int)e.du; --d) {
+    const int cnt = pm[d] - e.stop[d];
+    if (idx < cnt) {
+      for (int i = 0; i < d; ++i) out[i] = e.stop[i];
+      out[d] = (uint8_t)(e.stop[d] + 1 + idx);
+      return d + 1;
+    }
+    idx -= cnt;
+  }
+  return -1;  // unreachable
+}
+
+// Block-wide exclusive scan of a[0..len) in place; returns the total.
+__device__ int block_scan_excl(int* a, int len, int* smem_tmp) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int per = (len + nt - 1) / nt;
+  const int lo = min(len, tid * per), hi = min(len, lo + per);
+  int s = 0;
+  for (int i = lo; i < hi; ++i) s += a[i];
+  smem_tmp[tid] = s;
+  __syncthreads();
+  if (tid == 0) {
+    int run = 0;
+    for (int t = 0; t < nt; ++t) {
+      const int v = smem_tmp[t];
+      smem_tmp[t] = run;
+      run += v;
+    }
+    smem_tmp[nt] = run;
+  }
+  __syncthreads();
+  int run = smem_tmp[tid];
+  for (int i = lo; i < hi; ++i) {
+    const int v = a[i];
+    a[i] = run;
+    run += v;
+  }
+  const int total = smem_tmp[nt];
+  __syncthreads();
+  return total;
+}
+
+__device__ void push_items(const KParams& kp, int queue, int p, const Entry* L, int head, int len,
+                           double C, int lane) {
+  // first qmax entries (list order) that need a run at cutoff C
+  RunQueue* q = kp.queues + queue;
+  RunItem* items = kp.items + (size_t)queue * kp.qcap;
+  int pushed = 0;
+  for (int base = 0; base < len && pushed < kp.qmax; base += 32) {
+    const int i = base + lane;
+    bool need = false;
+    if (i < len) {
+      const Entry& e = L[head + i];
+      need = !(e.ran && e.cutoff_used == C) && !e.capped;
+    }
+    const unsigned bal = __ballot_sync(HPK_FULL_MASK, need);
+    int cnt = __popc(bal);
+    if (pushed + cnt > kp.qmax) cnt = kp.qmax - pushed;
+    int slot0 = 0;
+    if (lane == 0 && cnt > 0) slot0 = atomicAdd(&q->len, cnt);
+    slot0 = shfl(slot0, 0);
+    const int rank = __popc(bal & ((1u << lane) - 1));
+    if (need && rank < cnt && slot0 + rank < kp.qcap) {
+      items[slot0 + rank].problem = p;
+      items[slot0 + rank].index = head + i;
+      items[slot0 + rank].cap = kp.seg_cap;
+    }
+    pushed += cnt;
+  }
+}
+
+__device__ void finish_problem(const KParams& kp, GState& S) {
+  S.done = 1;
+  atomicSub(kp.active, 1);
+}
+
+// Per-problem scheduler: split, ordered commit, queue the next wave.
+__device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* smem_tmp) {
+  GState& S = kp.states[p];
+  const GProb& P = kp.probs[p];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (S.done) return;
+  Entry* Lin = list_ptr(kp, p, S.cur);
+  Entry* Lout = list_ptr(kp, p, S.cur ^ 1);
+  const int head = S.head, len = S.len;
+
+  if (S.rerun_pending) {
+    // the capped re-run of the overflow segment (at the head) is back
+    if (tid == 0) {
+      const Entry& e = Lin[head];
+      if (e.has_best && (!S.has_best || e.best_obj > S.best_obj ||
+                         (e.best_obj == S.best_obj && e.best_G < S.best_G))) {
+        S.has_best = 1;
+        S.best_obj = e.best_obj;
+        S.best_G = e.best_G;
+        for (int i = 0; i < P.n; ++i) S.best_rgs[i] = e.best_rgs[i];
+      }
+      S.V = P.budget;
+      S.aborted = 1;
+      S.rerun_pending = 0;
+      finish_problem(kp, S);
+    }
+    __syncthreads();
+    return;
+  }
+
+  // ---- A. split: unfinished FULL runs -> PREFIX record + remainder pieces
+  int* cnt = kp.scratch + (size_t)p * (kp.lcap + 1);
+  for (int i = tid; i < len; i += blockDim.x) {
+    const Entry& e = Lin[head + i];
+    int c = 1;
+    if (e.ran_now && e.kind == KIND_FULL && !e.finished && !e.capped) c += n_pieces(e);
+    cnt[i] = c;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    // capacity: keep splits in list order while they fit; the first split
+    // always proceeds (progress guarantee). Dropped splits are re-run later.
+    long long total = 0;
+    for (int i = 0; i < len; ++i) total += cnt[i];
+    if (total > kp.lcap) {
+      long long run = 0;
+      bool first = true;
+      for (int i = 0; i < len; ++i) {
+        if (cnt[i] > 1) {
+          if (first || run + cnt[i] + (len - i - 1) <= kp.lcap) {
+            first = false;
+          } else {
+            cnt[i] = 1;
+            Lin[head + i].ran = 0;  // discard the partial run
+            Lin[head + i].ran_now = 0;
+          }
+        }
+        run += cnt[i];
+      }
+    }
+  }
+  __syncthreads();
+  const int total = block_scan_excl(cnt, len, smem_tmp);
+  if (tid == 0) cnt[len] = total;
+  __syncthreads();
+  // write the new list: one output slot per thread iteration
+  for (int o = tid; o < total; o += blockDim.x) {
+    int lo = 0, hi = len;  // largest i with cnt[i] <= o
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (cnt[mid] <= o) lo = mid;
+      else hi = mid;
+    }
+    const int i = lo;
+    const int k = o - cnt[i];
+    const Entry& e = Lin[head + i];
+    const bool split = (cnt[i + 1] - cnt[i]) > 1;
+    Entry& out = Lout[o];
+    if (k == 0) {
+      out = e;
+      out.ran_now = 0;
+      if (split) {
+        out.kind = KIND_PREFIX;
+        for (int j = 0; j < e.dstop; ++j) out.end[j] = e.stop[j];
+        out.dend = e.dstop;
+        out.finished = 1;
+      }
+    } else {
+      const int du = piece_path(e, k - 1, out.u);
+      out.du = (uint8_t)du;
+      out.kind = KIND_FULL;
+      out.ran = 0;
+      out.ran_now = 0;
+      out.finished = 0;
+      out.capped = 0;
+      out.has_best = 0;
+      out.a_star = -1;
+    }
+  }
+  __syncthreads();
+
+  // ---- B. ordered commit walk (warp 0)
+  if (warp == 0) {
+    double C = S.C;
+    long long V = S.V;
+    const long long B = P.budget;
+    int i = 0;
+    int new_head = 0;
+    int done = 0, aborted = 0, rerun = 0;
+    long long rerun_cap = 0;
+    while (i < total) {
+      const int j = i + lane;
+      bool ok = false;
+      long long v = 0;
+      double m = -1, bo = 0;
+      int bg = 0, hb = 0, ast = -1, kind = 0;
+      if (j < total) {
+        const Entry& e = Lout[j];
+        ok = e.ran && e.cutoff_used == C && e.finished && !e.capped;
+        v = e.visits;
+        m = e.m;
+        hb = e.has_best;
+        bo = e.best_obj;
+        bg = e.best_G;
+        ast = e.a_star;
+        kind = e.kind;
+      }
+      const unsigned bad = __ballot_sync(HPK_FULL_MASK, !ok);
+      const int first_bad = bad ? __ffs(bad) - 1 : 32;
+      // inclusive scan of visits
+      long long cum = v;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const long long t = __shfl_up_sync(HPK_FULL_MASK, cum, off);
+        if (lane >= off) cum += t;
+      }
+      const bool imp = ok && m > C;
+      const bool del = ok && kind == KIND_PREFIX && ast >= 0;
+      const bool over = ok && B >= 0 && V + cum >= B;
+      const unsigned special = __ballot_sync(HPK_FULL_MASK, (imp || del || over) && lane < first_bad);
+      const int first_sp = special ? __ffs(special) - 1 : 32;
+      int kc = first_bad;  // lanes [0, kc) are processed this chunk
+      if (first_sp < kc) kc = first_sp + 1;
+      const bool special_last = kc > 0 && first_sp == kc - 1;
+      // budget overflow inside the special lane: do not commit it, re-run capped
+      bool overflow = false;
+      if (special_last) {
+        const long long cum_l = shfl(cum, kc - 1);
+        const int over_l = shfl((int)over, kc - 1);
+        if (over_l && V + cum_l > B) overflow = true;
+      }
+      const int kcommit = overflow ? kc - 1 : kc;
+      // merge bests of [0, kcommit): (obj desc, G asc, index asc)
+      double ko = -1;
+      int kg = 0, ki = 1 << 30;
+      if (lane < kcommit && hb) {
+        ko = bo;
+        kg = bg;
+        ki = lane;
+      }
+      double mm = (lane < kcommit) ? m : -1.0;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const double oo = __shfl_xor_sync(HPK_FULL_MASK, ko, off);
+        const int og = __shfl_xor_sync(HPK_FULL_MASK, kg, off);
+        const int oi = __shfl_xor_sync(HPK_FULL_MASK, ki, off);
+        if (oo >= 0 && (ko < 0 || key_better(oo, og, oi, ko, kg, ki))) {
+          ko = oo;
+          kg = og;
+          ki = oi;
+        }
+        const double om = __shfl_xor_sync(HPK_FULL_MASK, mm, off);
+        mm = om > mm ? om : mm;
+      }
+      const int gh = *((volatile int*)&S.has_best);
+      const double gbo = *((volatile double*)&S.best_obj);
+      const int gbg = *((volatile int*)&S.best_G);
+      if (ko >= 0 && (!gh || ko > gbo || (ko == gbo && kg < gbg))) {
+        const Entry& w = Lout[i + ki];
+        for (int t = lane; t < P.n; t += 32) S.best_rgs[t] = w.best_rgs[t];
+        if (lane == 0) {
+          S.has_best = 1;
+          S.best_obj = ko;
+          S.best_G = kg;
+        }
+      }
+      __syncwarp();
+      if (kcommit > 0) V += shfl(cum, kcommit - 1);
+      C = mm > C ? mm : C;
+      i += kcommit;
+      if (overflow) {
+        rerun = 1;
+        rerun_cap = B - V;
+        break;
+      }
+      if (special_last) {
+        const int jl = i - 1;  // the special entry, now committed
+        const int del_l = shfl((int)del, kc - 1);
+        if (del_l) {
+          const Entry& e = Lout[jl];
+          const int la = e.a_star;
+          int ndel = 0;
+          for (int base = jl + 1; base < total; base += 32) {
+            const int t = base + lane;
+            bool inside = false;
+            if (t < total) inside = is_prefix_of(e.end, la, Lout[t].u, Lout[t].du);
+            const unsigned bin = __ballot_sync(HPK_FULL_MASK, inside);
+            const int firstout = (~bin) ? __ffs(~bin) - 1 : 32;
+            ndel += firstout;
+            if (firstout < 32) break;
+          }
+          i += ndel;
+        }
+        if (B >= 0 && V == B) {
+          done = 1;
+          aborted = i < total ? 1 : 0;
+        }
+        break;  // entries after a special one ran under a different state
+      }
+      if (kc < 32) break;  // reached an entry that still needs a run
+    }
+    new_head = i;
+    if (lane == 0) {
+      S.C = C;
+      S.V = V;
+      S.cur ^= 1;
+      S.head = new_head;
+      S.len = total - new_head;
+      S.waves += 1;
+      S.max_list = max(S.max_list, total);
+      if (rerun) {
+        S.rerun_pending = 1;
+        S.rerun_cap = rerun_cap;
+        Lout[new_head].capped = 1;
+      }
+      if (done) {
+        S.aborted = aborted;
+        finish_problem(kp, S);
+      } else if (!rerun && S.len == 0) {
+        S.aborted = 0;
+        finish_problem(kp, S);
+      }
+    }
+    __syncwarp();
+    const int flag = shfl(lane == 0 ? ((S.done ? 0 : 1) | (rerun ? 2 : 0)) : 0, 0);
+    if (flag & 2) {
+      if (lane == 0) {
+        RunQueue* q = kp.queues + next_queue;
+        const int slot = atomicAdd(&q->len, 1);
+        RunItem* items = kp.items + (size_t)next_queue * kp.qcap;
+        items[slot].problem = p;
+        items[slot].index = new_head;
+        items[slot].cap = rerun_cap;
+      }
+    } else if (flag & 1) {
+      push_items(kp, next_queue, p, Lout, new_head, total - new_head, C, lane);
+    }
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- init
+
+__device__ void first_occurrence(const int* key, int n, uint8_t* out) {
+  int seen[MAXN];
+  int ns = 0;
+  for (int i = 0; i < n; ++i) {
+    int ix = -1;
+    for (int j = 0; j < ns; ++j)
+      if (seen[j] == key[i]) {
+        ix = j;
+        break;
+      }
+    if (ix < 0) {
+      seen[ns] = key[i];
+      ix = ns++;
+    }
+    out[i] = (uint8_t)ix;
+  }
+}
+
+// evaluate_partition (grouping.cpp:227-247): fresh sums in unit order
+__device__ double evaluate_partition(const GProb& P, const uint8_t* rgs, double* z_out) {
+  int m = 0;
+  for (int i = 0; i < P.n; ++i) m = max(m, (int)rgs[i] + 1);
+  double pw[MAXN], me[MAXN];
+  int cnt[MAXN];
+  for (int g = 0; g < m; ++g) {
+    pw[g] = 0;
+    me[g] = 0;
+    cnt[g] = 0;
+  }
+  for (int i = 0; i < P.n; ++i) {
+    pw[rgs[i]] += P.p[i];
+    me[rgs[i]] += P.m[i];
+    cnt[rgs[i]] += 1;
+  }
+  double z = 0;
+  for (int gi = 0; gi < m; ++gi) {
+    if (cnt[gi] == 0 || me[gi] < P.min_mem) return -1;
+    const double rho = (double)(cnt[gi] - 1) / (double)(P.K + cnt[gi] - 1);
+    const double gv = pw[gi] * (1.0 - rho);
+    z = gi == 0 ? gv : (gv < z ? gv : z);
+  }
+  *z_out = z;
+  return (double)m * z;
+}
+
+__device__ void init_problem(const KParams& kp, int p) {
+  GProb& P = kp.probs[p];
+  GState& S = kp.states[p];
+  const int tid = threadIdx.x;
+  const int n = P.n;
+  for (int d = tid; d <= n + 1; d += blockDim.x) {
+    if (d >= 1) P.f[d] = 1.0 - (double)(d - 1) / (double)(P.K + d - 1);
+    else P.f[0] = 0.0;
+  }
+  for (int d = tid; d <= n; d += blockDim.x) {
+    double rm = 0;
+    for (int i = d; i < n; ++i) rm += P.m[i];
+    P.RM[d] = rm;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double r = 0;
+    P.R[n] = 0;
+    for (int d = n - 1; d >= 0; --d) {
+      r += P.p[d];
+      P.R[d] = r;
+    }
+    // seeds: one group, singletons, by type, by node (grouping.cpp:206-225)
+    uint8_t seeds[4][MAXN];
+    for (int i = 0; i < n; ++i) {
+      seeds[0][i] = 0;
+      seeds[1][i] = (uint8_t)i;
+    }
+    first_occurrence(P.tkey, n, seeds[2]);
+    first_occurrence(P.nkey, n, seeds[3]);
+    double seed_obj = -1, seed_z = 0;
+    int seed_ix = -1;
+    for (int k = 0; k < 4; ++k) {
+      double z = 0;
+      const double obj = evaluate_partition(P, seeds[k], &z);
+      if (obj > seed_obj) {  // strict: the first seed wins ties (:304)
+        seed_obj = obj;
+        seed_z = z;
+        seed_ix = k;
+      }
+    }
+    S.seed_obj = seed_obj;
+    S.seed_z = seed_z;
+    S.seed_ix = seed_ix;
+    if (seed_ix >= 0)
+      for (int i = 0; i < n; ++i) S.seed_rgs[i] = seeds[seed_ix][i];
+    S.C = seed_obj;  // prune_floor (:312)
+    S.V = 0;
+    S.has_best = 0;
+    S.best_obj = 0;
+    S.best_G = 0;
+    S.cur = 0;
+    S.head = 0;
+    S.done = 0;
+    S.aborted = 0;
+    S.rerun_pending = 0;
+    S.waves = 0;
+    S.runs = 0;
+    S.run_visits = 0;
+    S.max_list = 1;
+    S.error = 0;
+    // root node (not a visit): bound = sum of all powers, serially (:154-160)
+    double bound = 0;
+    for (int i = 0; i < n; ++i) bound += P.p[i];
+    const bool pruned = (S.C >= 0 && bound < S.C) || (0.0 > P.RM[0]);
+    if (pruned) {
+      S.len = 0;
+      S.done = 1;
+      atomicSub(kp.active, 1);
+    } else {
+      Entry& e = list_ptr(kp, p, 0)[0];
+      e.u[0] = 0;  // root has no groups: its only child is [0]
+      e.du = 1;
+      e.kind = KIND_FULL;
+      e.ran = 0;
+      e.ran_now = 0;
+      e.finished = 0;
+      e.capped = 0;
+      e.has_best = 0;
+      e.a_star = -1;
+      S.len = 1;
+      RunQueue* q = kp.queues + 0;
+      const int slot = atomicAdd(&q->len, 1);
+      kp.items[slot].problem = p;
+      kp.items[slot].index = 0;
+      kp.items[slot].cap = kp.seg_cap;
+    }
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------ the kernel
+
+// Grid barrier + gpu-scope fences: segment lists and problem states are
+// written on one SM and read on another in the next phase; the fences make
+// those writes visible and drop stale L1 lines.
+__device__ __forceinline__ void gsync(cg::grid_group& grid) {
+  __threadfence();
+  grid.sync();
+  __threadfence();
+}
+
+__global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  WarpSmem* wsm = reinterpret_cast<WarpSmem*>(smem_raw);
+  int* smem_tmp = reinterpret_cast<int*>(smem_raw + sizeof(WarpSmem) * WARPS_PER_BLOCK);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  for (int p = blockIdx.x; p < kp.n_problems; p += gridDim.x) init_problem(kp, p);
+  gsync(grid);
+
+  int cur = 0;
+  for (int wave = 0; wave < kp.max_waves; ++wave) {
+    // ---- run phase
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      kp.queues[cur ^ 1].len = 0;
+      kp.queues[cur ^ 1].head = 0;
+    }
+    RunQueue* q = kp.queues + cur;
+    RunItem* items = kp.items + (size_t)cur * kp.qcap;
+    const int qlen = min(*((volatile int*)&q->len), kp.qcap);
+    while (true) {
+      int it = 0;
+      if (lane == 0) it = atomicAdd(&q->head, 1);
+      it = shfl(it, 0);
+      if (it >= qlen) break;
+      const RunItem item = items[it];
+      const GProb& P = kp.probs[item.problem];
+      GState& S = kp.states[item.problem];
+      Entry* L = list_ptr(kp, item.problem, S.cur);
+      Entry* E = L + item.index;
+      const double C = S.C;
+      RunOut o = run_segment(P, E, E, C, item.cap, wsm + warp, lane, kp.err);
+      if (lane == 0) {
+        E->cutoff_used = C;
+        E->ran = 1;
+        E->ran_now = 1;
+        E->visits = o.visits;
+        E->finished = o.finished ? 1 : 0;
+        E->dstop = (uint8_t)o.dstop;
+        E->has_best = o.has_best ? 1 : 0;
+        E->best_obj = o.best_obj;
+        E->best_G = o.best_G;
+        E->m = o.m;
+        E->a_star = o.a_star;
+        atomicAdd((unsigned long long*)&S.runs, 1ull);
+        atomicAdd((unsigned long long*)&S.run_visits, (unsigned long long)o.visits);
+      }
+      __syncwarp();
+    }
+    gsync(grid);
+    // ---- schedule phase
+    for (int p = blockIdx.x; p < kp.n_problems; p += gridDim.x)
+      schedule_problem(kp, p, cur ^ 1, smem_tmp);
+    gsync(grid);
+    if (*((volatile int*)kp.active) <= 0) break;
+    cur ^= 1;
+  }
+}
+
+// ------------------------------------------------------- serial replica
+
+struct SerialCand {
+  double obj, z;
+  int G;
+  uint8_t rgs[256];
+};
+
+// One thread replays dfs() of grouping.cpp:135-202 for one problem, with the
+// reference's exact state updates (+= / -=) and top_k bookkeeping.
+struct SerialProb {
+  int n, K, top_k;
+  long long budget;
+  double min_mem;
+  const double* p;
+  const double* m;
+  const int* tkey;
+  const int* nkey;
+  // outputs
+  int status, count, optimal;
+  long long visited;
+  double obj[HPK_MAX_TOPK], z[HPK_MAX_TOPK];
+  int* rgs_out;  // device [top_k * n]
+};
+
+__device__ void seed_rgs(const SerialProb& pb, int k, int* rgs) {
+  int distinct = 0;
+  for (int i = 0; i < pb.n; ++i) {
+    if (k == 0) {
+      rgs[i] = 0;
+    } else if (k == 1) {
+      rgs[i] = i;
+    } else {
+      const int* key = k == 2 ? pb.tkey : pb.nkey;
+      int j = 0;
+      while (key[j] != key[i]) ++j;
+      rgs[i] = j == i ? distinct++ : rgs[j];
+    }
+  }
+}
+
+__device__ bool s_better(double ao, int ag, double bo, int bg) {
+  if (ao != bo) return ao > bo;
+  return ag < bg;
+}
+
+__global__ void hpk_serial_kernel(SerialProb* probs, int n_probs, SerialCand* cands,
+                                  double* scratch, int* iscratch, int max_n) {
+  const int pi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pi >= n_probs) return;
+  SerialProb& pb = probs[pi];
+  const int n = pb.n;
+  double* gp = scratch + (size_t)pi * 2 * (max_n + 1);
+  double* gm = gp + (max_n + 1);
+  int* gc = iscratch + (size_t)pi * 4 * (max_n + 1);
+  int* rgs = gc + (max_n + 1);
+  int* fr_G = rgs + (max_n + 1);
+  int* fr_gi = fr_G + (max_n + 1);
+  SerialCand* best = cands + (size_t)pi * (HPK_MAX_TOPK + 1);
+  int n_best = 0;
+  const int top_k = pb.top_k < 1 ? 1 : pb.top_k;
+
+  // seeds (:206-225, :299-312)
+  double seed_obj = -1, seed_z = 0;
+  int seed_ix = -1;
+  {
+    for (int k = 0; k < 4; ++k) {
+      // build seed k into rgs (first-occurrence numbering, :213-221)
+      seed_rgs(pb, k, rgs);
+      int mg = 0;
+      for (int i = 0; i < n; ++i) mg = max(mg, rgs[i] + 1);
+      for (int g = 0; g < mg; ++g) { gp[g] = 0; gm[g] = 0; gc[g] = 0; }
+      for (int i = 0; i < n; ++i) { gp[rgs[i]] += pb.p[i]; gm[rgs[i]] += pb.m[i]; gc[rgs[i]] += 1; }
+      double z = 0, obj = 0;
+      bool ok = true;
+      for (int gi = 0; gi < mg; ++gi) {
+        if (gc[gi] == 0 || gm[gi] < pb.min_mem) { ok = false; break; }
+        const double rho = (double)(gc[gi] - 1) / (double)(pb.K + gc[gi] - 1);
+        const double gv = gp[gi] * (1.0 - rho);
+        z = gi == 0 ? gv : (gv < z ? gv : z);
+      }
+      obj = ok ? (double)mg * z : -1;
+      if (obj > seed_obj) {
+        seed_obj = obj;
+        seed_z = z;
+        seed_ix = k;
+      }
+    }
+  }
+  const double prune_floor = seed_obj;
+  long long visited = 0;
+  bool aborted = false;
+  int G = 0;
+  // iterative dfs: node at depth `next`
+  int next = 0;
+  int phase = 0;  // 0: process node at `next`; 1: iterate children of frame next; 2: return to parent
+  while (true) {
+    if (phase == 0) {
+      if (next == n) {  // leaf
+        double z = 0;
+        bool first = true, feas = true;
+        for (int gi = 0; gi < G; ++gi) {
+          if (gm[gi] < pb.min_mem) { feas = false; break; }
+          const double rho = (double)(gc[gi] - 1) / (double)(pb.K + gc[gi] - 1);
+          const double gv = gp[gi] * (1.0 - rho);
+          z = first ? gv : (gv < z ? gv : z);
+          first = false;
+        }
+        if (feas) {
+          const double objective = (double)G * z;
+          int pos = n_best;
+          for (int i = 0; i < n_best; ++i)
+            if (s_better(objective, G, best[i].obj, best[i].G)) { pos = i; break; }
+          bool dup = false;
+          for (int i = 0; i < n_best && !dup; ++i) {
+            bool same = true;
+            for (int t = 0; t < n; ++t)
+              if (best[i].rgs[t] != rgs[t]) { same = false; break; }
+            dup = same;
+          }
+          if (!dup) {
+            for (int i = n_best; i > pos; --i) best[i] = best[i - 1];
+            best[pos].obj = objective;
+            best[pos].z = z;
+            best[pos].G = G;
+            for (int t = 0; t < n; ++t) best[pos].rgs[t] = (uint8_t)rgs[t];
+            n_best = n_best + 1 > top_k ? top_k : n_best + 1;
+          }
+        }
+        phase = 2;
+        continue;
+      }
+      double bound = 0;
+      for (int gi = 0; gi < G; ++gi) {
+        const double rho = (double)(gc[gi] - 1) / (double)(pb.K + gc[gi] - 1);
+        bound += gp[gi] * (1.0 - rho);
+      }
+      double remaining_mem = 0;
+      for (int i = next; i < n; ++i) {
+        bound += pb.p[i];
+        remaining_mem += pb.m[i];
+      }
+      double cutoff = prune_floor;
+      if (n_best >= top_k) cutoff = prune_floor > best[n_best - 1].obj ? prune_floor : best[n_best - 1].obj;
+      if (cutoff >= 0 && bound < cutoff) { phase = 2; continue; }
+      double deficit = 0;
+      for (int gi = 0; gi < G; ++gi) {
+        const double d = pb.min_mem - gm[gi];
+        deficit += d > 0.0 ? d : 0.0;
+      }
+      if (deficit > remaining_mem) { phase = 2; continue; }
+      fr_G[next] = G;
+      fr_gi[next] = 0;
+      phase = 1;
+      continue;
+    }
+    if (phase == 1) {
+      const int gi = fr_gi[next];
+      const int ng = fr_G[next];
+      if (gi > ng) { phase = 2; continue; }
+      if (pb.budget >= 0 && visited >= pb.budget) { aborted = true; break; }
+      ++visited;
+      if (gi == ng) { gp[G] = pb.p[next]; gm[G] = pb.m[next]; gc[G] = 1; ++G; }
+      else { gp[gi] += pb.p[next]; gm[gi] += pb.m[next]; gc[gi] += 1; }
+      rgs[next] = gi;
+      ++next;
+      phase = 0;
+      continue;
+    }
+    // phase 2: return from node at `next` to its parent frame
+    if (next == 0) break;  // root finished
+    --next;
+    {
+      const int gi = fr_gi[next];
+      const int ng = fr_G[next];
+      if (gi == ng) { --G; }
+      else { gp[gi] -= pb.p[next]; gm[gi] -= pb.m[next]; gc[gi] -= 1; }
+      fr_gi[next] = gi + 1;
+    }
+    phase = 1;
+  }
+  // result rules (:316-334)
+  const bool optimal = !aborted;
+  pb.visited = visited;
+  pb.status = 0;
+  if (n_best == 0) {
+    if (seed_obj < 0) { pb.status = 3; return; }
+  }
+  if (n_best == 0 || (!optimal && seed_obj > best[0].obj)) {
+    // rebuild the winning seed
+    seed_rgs(pb, seed_ix, rgs);
+    for (int i = 0; i < n; ++i) pb.rgs_out[i] = rgs[i];
+    pb.count = 1;
+    pb.obj[0] = seed_obj;
+    pb.z[0] = seed_z;
+    pb.optimal = 0;
+    return;
+  }
+  pb.count = n_best;
+  for (int k = 0; k < n_best; ++k) {
+    pb.obj[k] = best[k].obj;
+    pb.z[k] = best[k].z;
+    for (int i = 0; i < n; ++i) pb.rgs_out[(size_t)k * n + i] = best[k].rgs[i];
+  }
+  pb.optimal = optimal ? 1 : 0;
+}
+
+}  // namespace hpk
+
+// ================================================================== host
+
+namespace {
+
+using namespace hpk;
+
+struct DeviceCtx {
+  int device = -1;
+  int sms = 0;
+  int blocks_per_sm = 0;
+  size_t cap_probs = 0, cap_lists = 0, cap_items = 0;
+  GProb* probs = nullptr;
+  GState* states = nullptr;
+  Entry* lists = nullptr;
+  int* scratch = nullptr;
+  RunQueue* queues = nullptr;
+  RunItem* items = nullptr;
+  int* active = nullptr;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::mutex mu;
+};
+
+DeviceCtx g_ctx[16];
+
+thread_local std::string t_err;
+thread_local hpk_timing t_timing;
+
+int fail(int code, const std::string& msg) {
+  t_err = msg;
+  return code;
+}
+
+#define HPK_CUDA(call)                                                                    \
+  do {                                                                                    \
+    cudaError_t _e = (call);                                                              \
+    if (_e != cudaSuccess)                                                                \
+      return fail(5, std::string("hetplan_b200 CUDA error: ") + cudaGetErrorString(_e) + \
+                         " at " #call);                                                   \
+  } while (0)
+
+int ensure_ctx(DeviceCtx& c, int device) {
+  if (c.device == device) return 0;
+  HPK_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  HPK_CUDA(cudaGetDeviceProperties(&prop, device));
+  c.sms = prop.multiProcessorCount;
+  const size_t smem = sizeof(WarpSmem) * WARPS_PER_BLOCK + sizeof(int) * (BLOCK_THREADS + 8);
+  HPK_CUDA(cudaFuncSetAttribute(hpk_wave_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+  int bps = 0;
+  HPK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, hpk_wave_kernel, BLOCK_THREADS,
+                                                         smem));
+  if (bps < 1) return fail(5, "hetplan_b200: wave kernel cannot be resident");
+  c.blocks_per_sm = bps;
+  HPK_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+  HPK_CUDA(cudaEventCreate(&c.ev0));
+  HPK_CUDA(cudaEventCreate(&c.ev1));
+  HPK_CUDA(cudaMalloc(&c.active, sizeof(int) * 2));
+  HPK_CUDA(cudaMalloc(&c.queues, sizeof(RunQueue) * 2));
+  c.device = device;
+  return 0;
+}
+
+template <typename T>
+int grow(T*& ptr, size_t& cap, size_t need) {
+  if (need <= cap) return 0;
+  if (ptr) cudaFree(ptr);
+  ptr = nullptr;
+  size_t want = std::max(need, cap * 2);
+  HPK_CUDA(cudaMalloc(&ptr, sizeof(T) * want));
+  cap = want;
+  return 0;
+}
+
+// Values exactly summable in fp64: all multiples of a common power of two with
+// the total (in those units) below 2^53 -> every partial sum, in any order,
+// is exact, so the reference's path-dependent += / -= sums equal ours.
+bool exact_sums(const double* v, int n, double extra, bool include_extra) {
+  int emin = 100000;
+  double total = 0;
+  auto lowexp = [](double x, int* e) -> bool {
+    if (!(x >= 0) || std::isinf(x)) return false;
+    if (x == 0) {
+      *e = 100000;
+      return true;
+    }
+    int ex;
+    double mant = std::frexp(x, &ex);  // x = mant * 2^ex, mant in [0.5,1)
+    // lowest set bit of the 53-bit significand
+    long long sig = (long long)std::ldexp(mant, 53);
+    int tz = 0;
+    while ((sig & 1) == 0) {
+      sig >>= 1;
+      ++tz;
+    }
+    *e = ex - 53 + tz;
+    return true;
+  };
+  for (int i = 0; i < n; ++i) {
+    int e;
+    if (!lowexp(v[i], &e)) return false;
+    emin = std::min(emin, e);
+    total += std::fabs(v[i]);
+  }
+  if (include_extra) {
+    int e;
+    if (!lowexp(extra, &e)) return false;
+    emin = std::min(emin, e);
+    total += std::fabs(extra);
+  }
+  if (emin == 100000) return true;
+  // total in units of 2^emin must stay below 2^53
+  return std::ldexp(total, -emin) < 9007199254740992.0 * 0.5;
+}
+
+}  // namespace
+
+// Hooks shared with hpk_partition.cu (same thread-local error / timing).
+void hpkp_fail(const std::string& msg) { t_err = msg; }
+namespace hpk_timing_bridge {
+void add_partition(double ms, long long h2d, long long d2h) {
+  t_timing.partition_ms += ms;
+  t_timing.h2d_bytes += h2d;
+  t_timing.d2h_bytes += d2h;
+  t_timing.kernel_launches += 1;
+}
+void reset() { t_timing = hpk_timing{}; }
+}  // namespace hpk_timing_bridge
+
+extern "C" {
+
+const char* hpk_version(void) { return "hetplan-b200 0.1.0 (sm_100a)"; }
+const char* hpk_last_error(void) { return t_err.c_str(); }
+
+int hpk_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+void hpk_search_config_init(hpk_search_config* cfg) {
+  if (!cfg) return;
+  cfg->device = -1;
+  cfg->segment_cap = 0;
+  cfg->max_list = 0;
+  cfg->force_serial = 0;
+  cfg->max_waves = 0;
+}
+
+void hpk_last_timing(hpk_timing* out) {
+  if (out) *out = t_timing;
+}
+
+void hpk_reset_timing(void) { t_timing = hpk_timing{}; }
+
+int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
+                        hpk_grouping_result* results, const hpk_search_config* cfg_in) {
+  t_err.clear();
+  if (n_problems <= 0) return 0;
+  hpk_search_config cfg;
+  hpk_search_config_init(&cfg);
+  if (cfg_in) cfg = *cfg_in;
+  const int ndev = hpk_device_count();
+  if (ndev <= 0)
+    return fail(5, "hetplan_b200: no CUDA device visible; the B200 planner has no CPU "
+                   "fallback");
+  int device = cfg.device;
+  if (device < 0) {
+    if (cudaGetDevice(&device) != cudaSuccess) device = 0;
+  }
+  if (device >= ndev || device >= 16) return fail(6, "hetplan_b200: bad device ordinal");
+  DeviceCtx& c = g_ctx[device];
+  std::lock_guard<std::mutex> lock(c.mu);
+  if (int rc = ensure_ctx(c, device)) return rc;
+  HPK_CUDA(cudaSetDevice(device));
+
+  // Partition problems between the engines.
+  std::vector<int> wave_ix, serial_ix;
+  for (int i = 0; i < n_problems; ++i) {
+    const hpk_grouping_problem& pr = problems[i];
+    results[i].status = 0;
+    results[i].count = 0;
+    results[i].optimal = 0;
+    results[i].visited = 0;
+    results[i].waves = 0;
+    results[i].segment_runs = 0;
+    results[i].segment_visits = 0;
+    results[i].max_list = 0;
+    if (pr.n < 1) return fail(6, "grouping: no devices");
+    if (pr.top_k > HPK_MAX_TOPK) return fail(6, "hetplan_b200: top_k above 16 unsupported");
+    const bool contract = exact_sums(pr.power, pr.n, 0, false) &&
+                          exact_sums(pr.memory, pr.n, 0, false);
+    const bool wave_ok = !cfg.force_serial && pr.n <= MAXN && pr.top_k <= 1 && contract;
+    (wave_ok ? wave_ix : serial_ix).push_back(i);
+  }
+
+  // ---------------- wave engine
+  if (!wave_ix.empty()) {
+    const int P = (int)wave_ix.size();
+    const long long seg_cap = cfg.segment_cap > 0 ? cfg.segment_cap : 2048;
+    int lcap = cfg.max_list > 0 ? cfg.max_list : 8192;
+    // keep the list buffers within ~2 GB for large batches
+    const size_t per = sizeof(Entry) * 2;
+    while (lcap > 256 && (size_t)P * lcap * per > (size_t)2 << 30) lcap /= 2;
+    std::vector<GProb> hp(P);
+    for (int k = 0; k < P; ++k) {
+      const hpk_grouping_problem& pr = problems[wave_ix[k]];
+      GProb& g = hp[k];
+      std::memset(&g, 0, sizeof(GProb));
+      g.n = pr.n;
+      g.K = pr.n_microbatches;
+      g.budget = pr.n <= pr.exact_threshold ? -1 : pr.node_budget;
+      g.min_mem = pr.min_mem;
+      g.exact_mem = exact_sums(pr.memory, pr.n, pr.min_mem, true) ? 1 : 0;
+      for (int i = 0; i < pr.n; ++i) {
+        g.p[i] = pr.power[i];
+        g.m[i] = pr.memory[i];
+        g.tkey[i] = pr.type_key[i];
+        g.nkey[i] = pr.node_key[i];
+      }
+    }
+    size_t cap_entries = c.cap_lists;
+    if (int rc = grow(c.probs, c.cap_probs, (size_t)P)) return rc;
+    if (int rc = grow(c.lists, cap_entries, (size_t)P * 2 * lcap)) return rc;
+    c.cap_lists = cap_entries;
+    // states / scratch sized with probs
+    if (c.states) cudaFree(c.states);
+    if (c.scratch) cudaFree(c.scratch);
+    c.states = nullptr;
+    c.scratch = nullptr;
+    HPK_CUDA(cudaMalloc(&c.states, sizeof(GState) * P));
+    HPK_CUDA(cudaMalloc(&c.scratch, sizeof(int) * (size_t)P * (lcap + 1)));
+    const int grid = c.sms * c.blocks_per_sm;
+    const int nwarps = grid * WARPS_PER_BLOCK;
+    const int qmax = std::max(1, (2 * nwarps) / P);
+    const int qcap = P * qmax + P + 64;
+    if (int rc = grow(c.items, c.cap_items, (size_t)2 * qcap)) return rc;
+
+    HPK_CUDA(cudaMemcpyAsync(c.probs, hp.data(), sizeof(GProb) * P, cudaMemcpyHostToDevice,
+                             c.stream));
+    HPK_CUDA(cudaMemsetAsync(c.queues, 0, sizeof(RunQueue) * 2, c.stream));
+    const int init_flags[2] = {P, 0};
+    HPK_CUDA(cudaMemcpyAsync(c.active, init_flags, sizeof(int) * 2, cudaMemcpyHostToDevice,
+                             c.stream));
+    t_timing.h2d_bytes += sizeof(GProb) * P + sizeof(int);
+
+    KParams kp;
+    kp.probs = c.probs;
+    kp.states = c.states;
+    kp.lists = c.lists;
+    kp.scratch = c.scratch;
+    kp.queues = c.queues;
+    kp.items = c.items;
+    kp.active = c.active;
+    kp.err = c.active + 1;
+    kp.n_problems = P;
+    kp.lcap = lcap;
+    kp.qcap = qcap;
+    kp.qmax = qmax;
+    kp.seg_cap = seg_cap;
+    kp.max_waves = cfg.max_waves > 0 ? cfg.max_waves : 200000;  // watchdog
+    const size_t smem = sizeof(WarpSmem) * WARPS_PER_BLOCK + sizeof(int) * (BLOCK_THREADS + 8);
+    void* args[] = {&kp};
+    HPK_CUDA(cudaEventRecord(c.ev0, c.stream));
+    HPK_CUDA(cudaLaunchCooperativeKernel((void*)hpk_wave_kernel, dim3(grid),
+                                         dim3(BLOCK_THREADS), args, smem, c.stream));
+    HPK_CUDA(cudaEventRecord(c.ev1, c.stream));
+    t_timing.kernel_launches += 1;
+    std::vector<GState> hs(P);
+    int flags_out[2] = {0, 0};
+    HPK_CUDA(cudaMemcpyAsync(hs.data(), c.states, sizeof(GState) * P, cudaMemcpyDeviceToHost,
+                             c.stream));
+    HPK_CUDA(cudaMemcpyAsync(flags_out, c.active, sizeof(int) * 2, cudaMemcpyDeviceToHost,
+                             c.stream));
+    HPK_CUDA(cudaStreamSynchronize(c.stream));
+    if (flags_out[1]) return fail(5, "hetplan_b200: wave engine watchdog tripped");
+    t_timing.d2h_bytes += sizeof(GState) * P;
+    float ms = 0;
+    HPK_CUDA(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
+    t_timing.search_ms += ms;
+    for (int k = 0; k < P; ++k) {
+      const int i = wave_ix[k];
+      const hpk_grouping_problem& pr = problems[i];
+      hpk_grouping_result& r = results[i];
+      const GState& s = hs[k];
+      r.engine = 0;
+      r.waves = s.waves;
+      r.segment_runs = s.runs;
+      r.segment_visits = s.run_visits;
+      r.max_list = s.max_list;
+      r.visited = s.V;
+      if (!s.done)
+        return fail(5, "hetplan_b200: wave engine did not converge within " +
+                           std::to_string(kp.max_waves) + " waves (problem " +
+                           std::to_string(i) + ", waves " + std::to_string(s.waves) +
+                           ", visits " + std::to_string(s.V) + ")");
+      const bool optimal = !s.aborted;
+      // result rules, grouping.cpp:316-334
+      if (!s.has_best) {
+        if (s.seed_obj < 0) {
+          r.status = 3;
+          continue;
+        }
+      }
+      if (!s.has_best || (!optimal && s.seed_obj > s.best_obj)) {
+        r.count = 1;
+        r.objective[0] = s.seed_obj;
+        r.z[0] = s.seed_z;
+        r.optimal = 0;
+        for (int u = 0; u < pr.n; ++u) r.rgs[u] = s.seed_rgs[u];
+        continue;
+      }
+      r.count = 1;
+      r.objective[0] = s.best_obj;
+      // z = objective / G is not how the reference gets z; recompute it from
+      // the partition exactly as the leaf did (min effective power).
+      {
+        double pw[MAXN] = {0}, me[MAXN] = {0};
+        int cn[MAXN] = {0};
+        for (int u = 0; u < pr.n; ++u) {
+          pw[s.best_rgs[u]] += pr.power[u];
+          me[s.best_rgs[u]] += pr.memory[u];
+          cn[s.best_rgs[u]] += 1;
+        }
+        double z = 0;
+        for (int gi = 0; gi < s.best_G; ++gi) {
+          const double rho = (double)(cn[gi] - 1) / (double)(pr.n_microbatches + cn[gi] - 1);
+          const double gv = pw[gi] * (1.0 - rho);
+          z = gi == 0 ? gv : (gv < z ? gv : z);
+        }
+        r.z[0] = z;
+      }
+      r.optimal = optimal ? 1 : 0;
+      for (int u = 0; u < pr.n; ++u) r.rgs[u] = s.best_rgs[u];
+    }
+  }
+
+  // ---------------- serial replica engine
+  if (!serial_ix.empty()) {
+    const int P = (int)serial_ix.size();
+    int max_n = 0;
+    size_t tot_units = 0;
+    for (int i : serial_ix) {
+      max_n = std::max(max_n, problems[i].n);
+      tot_units += problems[i].n;
+    }
+    if (max_n > 255) return fail(6, "hetplan_b200: more than 255 TP units unsupported");
+    std::vector<double> hpw, hme;
+    std::vector<int> htk, hnk;
+    std::vector<size_t> off(P);
+    size_t rgs_total = 0;
+    std::vector<size_t> rgs_off(P);
+    for (int k = 0; k < P; ++k) {
+      const hpk_grouping_problem& pr = problems[serial_ix[k]];
+      off[k] = hpw.size();
+      hpw.insert(hpw.end(), pr.power, pr.power + pr.n);
+      hme.insert(hme.end(), pr.memory, pr.memory + pr.n);
+      htk.insert(htk.end(), pr.type_key, pr.type_key + pr.n);
+      hnk.insert(hnk.end(), pr.node_key, pr.node_key + pr.n);
+      rgs_off[k] = rgs_total;
+      rgs_total += (size_t)std::max(1, pr.top_k) * pr.n;
+    }
+    double *d_pw, *d_me, *d_scr;
+    int *d_tk, *d_nk, *d_iscr, *d_rgs;
+    SerialProb* d_probs;
+    SerialCand* d_cands;
+    HPK_CUDA(cudaMalloc(&d_pw, sizeof(double) * tot_units));
+    HPK_CUDA(cudaMalloc(&d_me, sizeof(double) * tot_units));
+    HPK_CUDA(cudaMalloc(&d_tk, sizeof(int) * tot_units));
+    HPK_CUDA(cudaMalloc(&d_nk, sizeof(int) * tot_units));
+    HPK_CUDA(cudaMalloc(&d_scr, sizeof(double) * (size_t)P * 2 * (max_n + 1)));
+    HPK_CUDA(cudaMalloc(&d_iscr, sizeof(int) * (size_t)P * 4 * (max_n + 1)));
+    HPK_CUDA(cudaMalloc(&d_rgs, sizeof(int) * rgs_total));
+    HPK_CUDA(cudaMalloc(&d_probs, sizeof(SerialProb) * P));
+    HPK_CUDA(cudaMalloc(&d_cands, sizeof(SerialCand) * (size_t)P * (HPK_MAX_TOPK + 1)));
+    std::vector<SerialProb> sp(P);
+    for (int k = 0; k < P; ++k) {
+      const hpk_grouping_problem& pr = problems[serial_ix[k]];
+      SerialProb& s = sp[k];
+      std::memset(&s, 0, sizeof(s));
+      s.n = pr.n;
+      s.K = pr.n_microbatches;
+      s.top_k = std::max(1, pr.top_k);
+      s.budget = pr.n <= pr.exact_threshold ? -1 : pr.node_budget;
+      s.min_mem = pr.min_mem;
+      s.p = d_pw + off[k];
+      s.m = d_me + off[k];
+      s.tkey = d_tk + off[k];
+      s.nkey = d_nk + off[k];
+      s.rgs_out = d_rgs + rgs_off[k];
+    }
+    HPK_CUDA(cudaMemcpyAsync(d_pw, hpw.data(), sizeof(double) * tot_units,
+                             cudaMemcpyHostToDevice, c.stream));
+    HPK_CUDA(cudaMemcpyAsync(d_me, hme.data(), sizeof(double) * tot_units,
+                             cudaMemcpyHostToDevice, c.stream));
+    HPK_CUDA(cudaMemcpyAsync(d_tk, htk.data(), sizeof(int) * tot_units, cudaMemcpyHostToDevice,
+                             c.stream));
+    HPK_CUDA(cudaMemcpyAsync(d_nk, hnk.data(), sizeof(int) * tot_units, cudaMemcpyHostToDevice,
+                             c.stream));
+    HPK_CUDA(cudaMemcpyAsync(d_probs, sp.data(), sizeof(SerialProb) * P, cudaMemcpyHostToDevice,
+                             c.stream));
+    HPK_CUDA(cudaEventRecord(c.ev0, c.stream));
+    hpk_serial_kernel<<<(P + 31) / 32, 32, 0, c.stream>>>(d_probs, P, d_cands, d_scr, d_iscr,
+                                                          max_n);
+    HPK_CUDA(cudaGetLastError());
+    HPK_CUDA(cudaEventRecord(c.ev1, c.stream));
+    t_timing.kernel_launches += 1;
+    HPK_CUDA(cudaMemcpyAsync(sp.data(), d_probs, sizeof(SerialProb) * P, cudaMemcpyDeviceToHost,
+                             c.stream));
+    std::vector<int> hrgs(rgs_total);
+    HPK_CUDA(cudaMemcpyAsync(hrgs.data(), d_rgs, sizeof(int) * rgs_total,
+                             cudaMemcpyDeviceToHost, c.stream));
+    HPK_CUDA(cudaStreamSynchronize(c.stream));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, c.ev0, c.ev1);
+    t_timing.serial_ms += ms;
+    for (int k = 0; k < P; ++k) {
+      const int i = serial_ix[k];
+      const hpk_grouping_problem& pr = problems[i];
+      hpk_grouping_result& r = results[i];
+      const SerialProb& s = sp[k];
+      r.engine = 1;
+      r.status = s.status;
+      r.count = s.count;
+      r.optimal = s.optimal;
+      r.visited = s.visited;
+      for (int t = 0; t < s.count; ++t) {
+        r.objective[t] = s.obj[t];
+        r.z[t] = s.z[t];
+        for (int u = 0; u < pr.n; ++u) r.rgs[(size_t)t * pr.n + u] = hrgs[rgs_off[k] + t * pr.n + u];
+      }
+    }
+    cudaFree(d_pw);
+    cudaFree(d_me);
+    cudaFree(d_tk);
+    cudaFree(d_nk);
+    cudaFree(d_scr);
+    cudaFree(d_iscr);
+    cudaFree(d_rgs);
+    cudaFree(d_probs);
+    cudaFree(d_cands);
+  }
+  return 0;
+}
+
+}  // extern "C"

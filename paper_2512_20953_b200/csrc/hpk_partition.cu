@@ -1,0 +1,596 @@
+// hpk_partition.cu — layer-to-stage partition (Eq. 4) and the Eq. (1) cost
+// model on the B200, batched over candidate plans.
+//
+// One CTA per candidate plan. For each DP group of the candidate the CTA
+//   1. builds the per-type stage-time table t[type][l] as the reference's
+//      ascending-bit sum (estimate_stage_time, P/src/profile.cpp:180-190) —
+//      NOT a prefix sum, which would round differently;
+//   2. finds the first missing profile entry in the reference's evaluation
+//      order (stage ascending, layer count ascending, only where the memory
+//      check passes; P/src/partition.cpp:60-70), which the reference raises as
+//      InvalidArgumentError;
+//   3. runs the min-max DP best[i][r] = min_l max(eval[i][l], best[i+1][r-l])
+//      (partition.cpp:72-83) with one thread per r, eval computed on the fly
+//      from the time table and the memory model (estimate_memory with the
+//      TOTAL microbatch count, profile.cpp:200-232 via partition.cpp:41-47);
+//   4. reconstructs the split giving earlier stages the most layers
+//      (partition.cpp:91-106) with warp ballots;
+// then evaluates the cost (cost.cpp:29-147): per-group fill/peak/steady with
+// boundary transfers, and T_sync over layers in ascending order.
+// min/max are exact; every add/mul/div follows the reference's order and the
+// library is built with -fmad=false.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "hetplan_b200.h"
+
+namespace hpkp {
+
+constexpr int THREADS = 256;
+
+struct Cand {
+  int n_layers, tp, k_total, n_groups;
+  double ppb, pab, opt_mult, intra_bw, inter_bw;
+  double cost_ppb, cost_pab;
+  int sync_max, allow_zero, n_types, n_bits;
+  int stage_base;  // offset into the stage arrays
+  int group_base;  // offset into the group arrays
+  int prof_base;   // offset into prof
+  int tt_base;     // offset into the time-table scratch
+  int best_base;   // offset into global best scratch (when it does not fit smem)
+  int use_gmem;
+};
+
+struct Outs {
+  int status, fail_group, fail_kind, missing_stage, missing_layers;
+  double t_sync, t_star;
+};
+
+struct Args {
+  const Cand* cands;
+  const int* group_stage_off;  // [total groups + n_cands] (per candidate n_groups+1)
+  const int* microbatches;
+  const int* stage_type;
+  const int* stage_index;
+  const double* stage_cap;
+  const int* stage_node;
+  const int* stage_rank0;
+  const double* prof;
+  double* ttab;     // [sum over cands of n_types*(L+1)]
+  unsigned char* tmiss;  // first missing bit +1 per ttab cell (0 = present)
+  double* gbest;    // global fallback best tables
+  int* out_layers;
+  double* out_time;
+  double* out_mem;
+  double* out_fill;
+  double* out_steady;
+  double* out_total;
+  double* out_bubble;
+  Outs* outs;
+  size_t smem_best_doubles;
+};
+
+// estimate_memory (profile.cpp:226-232): fixed + variable, reference order.
+__device__ __forceinline__ double stage_memory(const Cand& c, int layers, int stage_index,
+                                               int P) {
+  if (layers == 0) return 0;
+  const double fixed = (double)layers * c.ppb * (1.0 + c.opt_mult) / (double)c.tp;
+  const int in_flight = min(c.k_total, P - stage_index + 1);
+  const double variable = (double)layers * c.pab * (double)in_flight / (double)c.tp;
+  return fixed + variable;
+}
+
+__global__ void __launch_bounds__(THREADS) partition_cost_kernel(Args a) {
+  extern __shared__ __align__(16) double sbest[];
+  __shared__ int s_first_missing;
+  __shared__ double s_bottleneck;
+  __shared__ int s_status;
+  const int ci = blockIdx.x;
+  const Cand c = a.cands[ci];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int L = c.n_layers;
+  const int W = L + 1;
+  double* tt = a.ttab + c.tt_base;
+  unsigned char* tm = a.tmiss + c.tt_base;
+  const double* prof = a.prof + c.prof_base;
+
+  // 1. time table: t[type][l] = sum over set bits of l, ascending (profile.cpp:180-190)
+  for (int x = tid; x < c.n_types * W; x += blockDim.x) {
+    const int ty = x / W, l = x % W;
+    double total = 0;
+    int miss = 0;
+    for (int bit = 0; (1 << bit) <= l; ++bit) {
+      if (l & (1 << bit)) {
+        const double v = bit < c.n_bits ? prof[ty * c.n_bits + bit] : 0.0;
+        if (!(v > 0)) {
+          if (!miss) miss = bit + 1;  // first missing bit (ascending): what at() throws on
+        } else {
+          total += v;
+        }
+      }
+    }
+    tt[x] = total;
+    tm[x] = (unsigned char)miss;
+  }
+  if (tid == 0) s_status = 0;
+  __syncthreads();
+
+  const int* goff = a.group_stage_off + c.group_base + ci;  // n_groups+1 entries
+  const int min_l = c.allow_zero ? 0 : 1;
+  double* gbest = a.gbest + c.best_base;
+  double worst = 0;  // thread 0 only
+
+  for (int j = 0; j < c.n_groups; ++j) {
+    const int s0 = c.stage_base + goff[j];
+    const int P = goff[j + 1] - goff[j];
+    double* best = c.use_gmem ? gbest : sbest;
+    // (a) every stage needs a layer (partition.cpp:54-58)
+    if (L < min_l * P) {
+      if (tid == 0) {
+        a.outs[ci].status = 3;
+        a.outs[ci].fail_group = j;
+        a.outs[ci].fail_kind = 1;
+        s_status = 3;
+      }
+      __syncthreads();
+      break;
+    }
+    // (b) first missing profile entry in evaluation order (i asc, l asc)
+    if (tid == 0) s_first_missing = 0x7fffffff;
+    __syncthreads();
+    for (int x = tid; x < P * W; x += blockDim.x) {
+      const int i = x / W, l = x % W;
+      if (l < min_l || l == 0) continue;
+      const int ty = a.stage_type[s0 + i];
+      if (tm[ty * W + l] == 0) continue;
+      const double bytes = stage_memory(c, l, a.stage_index[s0 + i], P);
+      if (bytes <= a.stage_cap[s0 + i]) atomicMin(&s_first_missing, x);
+    }
+    __syncthreads();
+    if (s_first_missing != 0x7fffffff) {
+      if (tid == 0) {
+        const int x = s_first_missing;
+        const int i = x / W, l = x % W;
+        const int ty = a.stage_type[s0 + i];
+        a.outs[ci].status = 6;
+        a.outs[ci].fail_group = j;
+        a.outs[ci].missing_stage = goff[j] + i;
+        a.outs[ci].missing_layers = 1 << (tm[ty * W + l] - 1);
+        s_status = 6;
+      }
+      __syncthreads();
+      break;
+    }
+    // (c) DP, stage P-1 .. 0; thread r owns best[i][r]
+    for (int r = tid; r < W; r += blockDim.x) best[(size_t)P * W + r] = r == 0 ? 0.0 : INFINITY;
+    __syncthreads();
+    for (int i = P - 1; i >= 0; --i) {
+      const int ty = a.stage_type[s0 + i];
+      const int sidx = a.stage_index[s0 + i];
+      const double cap = a.stage_cap[s0 + i];
+      const double* nb = best + (size_t)(i + 1) * W;
+      for (int r = tid; r < W; r += blockDim.x) {
+        double b = INFINITY;
+        for (int l = min_l; l <= r; ++l) {
+          const double nv = nb[r - l];
+          if (nv == INFINITY) continue;
+          double e;
+          if (l == 0) {
+            e = 0;  // allow_zero: time[0] = 0 (partition.cpp:68)
+          } else {
+            if (!(stage_memory(c, l, sidx, P) <= cap)) continue;
+            e = tt[ty * W + l];
+          }
+          const double mx = e < nv ? nv : e;  // std::max(e, nv)
+          b = mx < b ? mx : b;                // std::min
+        }
+        best[(size_t)i * W + r] = b;
+      }
+      __syncthreads();
+    }
+    if (tid == 0) s_bottleneck = best[L];
+    __syncthreads();
+    const double bottleneck = s_bottleneck;
+    if (bottleneck == INFINITY) {  // partition.cpp:85-89
+      if (tid == 0) {
+        a.outs[ci].status = 3;
+        a.outs[ci].fail_group = j;
+        a.outs[ci].fail_kind = 2;
+        s_status = 3;
+      }
+      __syncthreads();
+      break;
+    }
+    // (d) reconstruction (partition.cpp:91-106): largest feasible l per stage
+    if (warp == 0) {
+      int remaining = L;
+      for (int i = 0; i < P; ++i) {
+        const int ty = a.stage_type[s0 + i];
+        const int sidx = a.stage_index[s0 + i];
+        const double cap = a.stage_cap[s0 + i];
+        int chosen = -1;
+        for (int top = remaining; top >= min_l && chosen < 0; top -= 32) {
+          const int l = top - lane;
+          bool okl = false;
+          if (l >= min_l) {
+            double e;
+            bool feas;
+            if (l == 0) {
+              e = 0;
+              feas = true;
+            } else {
+              feas = stage_memory(c, l, sidx, P) <= cap;
+              e = tt[ty * W + l];
+            }
+            okl = feas && e <= bottleneck && best[(size_t)(i + 1) * W + (remaining - l)] <= bottleneck;
+          }
+          const unsigned bal = __ballot_sync(0xffffffffu, okl);
+          if (bal) chosen = top - (__ffs(bal) - 1);
+        }
+        if (lane == 0) {
+          a.out_layers[s0 + i] = chosen;
+          a.out_time[s0 + i] = chosen == 0 ? 0.0 : tt[ty * W + chosen];
+          a.out_mem[s0 + i] = stage_memory(c, chosen, sidx, P);
+        }
+        remaining -= chosen;
+      }
+    }
+    __syncthreads();
+    // (e) group cost (cost.cpp:43-69, 122-143), stage order, thread 0
+    if (tid == 0) {
+      const double pab = c.cost_pab;
+      double fill = 0, peak = 0;
+      bool zero_layers = false;
+      for (int i = 0; i < P; ++i) {
+        const int l = a.out_layers[s0 + i];
+        if (l < 1) zero_layers = true;
+        double t = a.out_time[s0 + i];
+        if (i + 1 < P) {
+          const double bw =
+              a.stage_node[s0 + i] == a.stage_node[s0 + i + 1] ? c.intra_bw : c.inter_bw;
+          t += pab / bw;
+        }
+        if (i > 0) {
+          const double bw =
+              a.stage_node[s0 + i - 1] == a.stage_node[s0 + i] ? c.intra_bw : c.inter_bw;
+          t += pab / bw;
+        }
+        fill += t;
+        peak = peak < t ? t : peak;
+      }
+      const int gix = c.group_base + j;
+      const int Kj = a.microbatches[gix];
+      a.out_fill[gix] = fill;
+      a.out_steady[gix] = (double)(Kj - 1) * peak;
+      a.out_total[gix] = a.out_fill[gix] + a.out_steady[gix];
+      a.out_bubble[gix] = (double)(P - 1) / (double)(Kj + P - 1);
+      worst = worst < a.out_total[gix] ? a.out_total[gix] : worst;
+      if (zero_layers) {  // estimate_stage_time rejects n_layers < 1 (profile.cpp:181)
+        a.outs[ci].status = 6;
+        a.outs[ci].fail_group = j;
+        a.outs[ci].missing_layers = 0;
+        s_status = 6;
+      }
+    }
+    __syncthreads();
+    if (s_status) break;
+  }
+  if (s_status) return;
+
+  // T_sync (cost.cpp:73-120): per layer, holders = first stage holding it in
+  // each group, ring over their representatives sorted by global rank.
+  double* sec = sbest;  // reuse smem (size >= L): per-layer seconds
+  __syncthreads();
+  const int G = c.n_groups;
+  for (int layer = tid; layer < L; layer += blockDim.x) {
+    // collect holders (G <= 64 in practice; loop-carried insertion sort on ranks)
+    int rk[256], nd[256];
+    int d = 0;
+    for (int j = 0; j < G && d < 256; ++j) {
+      const int s0 = c.stage_base + goff[j];
+      const int P = goff[j + 1] - goff[j];
+      int begin = 0;
+      for (int i = 0; i < P; ++i) {
+        const int end = begin + a.out_layers[s0 + i];
+        if (layer >= begin && layer < end) {
+          int pos = d;
+          const int rr = a.stage_rank0[s0 + i];
+          while (pos > 0 && rk[pos - 1] > rr) {
+            rk[pos] = rk[pos - 1];
+            nd[pos] = nd[pos - 1];
+            --pos;
+          }
+          rk[pos] = rr;
+          nd[pos] = a.stage_node[s0 + i];
+          ++d;
+          break;
+        }
+        begin = end;
+      }
+    }
+    double seconds = 0;
+    if (d >= 2) {
+      double min_bw = 0;
+      for (int i = 0; i < d; ++i) {
+        const double bw = nd[i] == nd[(i + 1) % d] ? c.intra_bw : c.inter_bw;
+        min_bw = i == 0 ? bw : (bw < min_bw ? bw : min_bw);
+      }
+      const double volume = c.cost_ppb / (double)c.tp;
+      seconds = 2.0 * (double)(d - 1) / (double)d * volume / min_bw;
+    }
+    sec[layer] = seconds;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double total = 0;
+    for (int layer = 0; layer < L; ++layer) {
+      const double s = sec[layer];
+      total = c.sync_max ? (total < s ? s : total) : total + s;
+    }
+    a.outs[ci].status = 0;
+    a.outs[ci].t_sync = total;
+    a.outs[ci].t_star = worst + total;
+  }
+}
+
+struct Ctx {
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::mutex mu;
+};
+Ctx g_ctx[16];
+
+thread_local std::string t_err;
+
+}  // namespace hpkp
+
+namespace hpk_timing_bridge {
+void add_partition(double ms, long long h2d, long long d2h);
+}
+
+using namespace hpkp;
+
+#define HPKP_CUDA(call)                                                                   \
+  do {                                                                                    \
+    cudaError_t _e = (call);                                                              \
+    if (_e != cudaSuccess) {                                                              \
+      hpkp_fail(std::string("hetplan_b200 CUDA error: ") + cudaGetErrorString(_e) +       \
+                " at " #call);                                                            \
+      return 5;                                                                           \
+    }                                                                                     \
+  } while (0)
+
+void hpkp_fail(const std::string& msg);
+
+extern "C" int hpk_partition_cost(const hpk_plan_candidate* cands, int n_cands,
+                                  hpk_plan_result* results, int device) {
+  if (n_cands <= 0) return 0;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0) {
+    cudaGetLastError();
+    hpkp_fail("hetplan_b200: no CUDA device visible; the B200 planner has no CPU fallback");
+    return 5;
+  }
+  if (device < 0) {
+    if (cudaGetDevice(&device) != cudaSuccess) device = 0;
+  }
+  if (device >= ndev || device >= 16) {
+    hpkp_fail("hetplan_b200: bad device ordinal");
+    return 6;
+  }
+  Ctx& cx = g_ctx[device];
+  std::lock_guard<std::mutex> lock(cx.mu);
+  HPKP_CUDA(cudaSetDevice(device));
+  if (cx.device != device) {
+    HPKP_CUDA(cudaStreamCreateWithFlags(&cx.stream, cudaStreamNonBlocking));
+    HPKP_CUDA(cudaEventCreate(&cx.ev0));
+    HPKP_CUDA(cudaEventCreate(&cx.ev1));
+    cx.device = device;
+  }
+  // Flatten the batch.
+  std::vector<Cand> hc(n_cands);
+  std::vector<int> goff, mb, sty, sidx, snode, srank;
+  std::vector<double> scap, prof;
+  size_t tt_total = 0, gbest_total = 0;
+  size_t max_smem_best = 0;
+  int total_groups = 0, total_stages = 0;
+  const size_t smem_limit = 200 * 1024;
+  for (int k = 0; k < n_cands; ++k) {
+    const hpk_plan_candidate& in = cands[k];
+    Cand& c = hc[k];
+    c.n_layers = in.n_layers;
+    c.tp = in.tp;
+    c.k_total = in.k_total;
+    c.n_groups = in.n_groups;
+    c.ppb = in.ppb;
+    c.pab = in.pab;
+    c.opt_mult = in.opt_mult;
+    c.cost_ppb = in.cost_ppb;
+    c.cost_pab = in.cost_pab;
+    c.intra_bw = in.intra_bw;
+    c.inter_bw = in.inter_bw;
+    c.sync_max = in.sync_max;
+    c.allow_zero = in.allow_zero;
+    c.n_types = in.n_types;
+    c.n_bits = in.n_bits;
+    c.stage_base = total_stages;
+    c.group_base = total_groups;
+    c.prof_base = (int)prof.size();
+    c.tt_base = (int)tt_total;
+    const int W = in.n_layers + 1;
+    tt_total += (size_t)in.n_types * W;
+    int maxP = 0;
+    for (int j = 0; j < in.n_groups; ++j) {
+      goff.push_back(in.group_stage_off[j]);
+      mb.push_back(in.microbatches[j]);
+      maxP = std::max(maxP, in.group_stage_off[j + 1] - in.group_stage_off[j]);
+    }
+    goff.push_back(in.group_stage_off[in.n_groups]);
+    const int ns = in.group_stage_off[in.n_groups];
+    for (int s = 0; s < ns; ++s) {
+      sty.push_back(in.stage_type[s]);
+      sidx.push_back(in.stage_index[s]);
+      scap.push_back(in.stage_mem_capacity[s]);
+      snode.push_back(in.stage_node[s]);
+      srank.push_back(in.stage_rank0[s]);
+    }
+    prof.insert(prof.end(), in.prof, in.prof + (size_t)in.n_types * in.n_bits);
+    const size_t need = (size_t)(maxP + 1) * W;
+    c.best_base = (int)gbest_total;
+    if (need * sizeof(double) > smem_limit) {
+      c.use_gmem = 1;
+      gbest_total += need;
+    } else {
+      c.use_gmem = 0;
+      max_smem_best = std::max(max_smem_best, need);
+    }
+    max_smem_best = std::max(max_smem_best, (size_t)W);
+    total_groups += in.n_groups;
+    total_stages += ns;
+  }
+  // device buffers (per call; small)
+  Cand* d_c;
+  int *d_goff, *d_mb, *d_sty, *d_sidx, *d_snode, *d_srank, *d_layers;
+  double *d_scap, *d_prof, *d_tt, *d_gbest, *d_time, *d_mem, *d_fill, *d_steady, *d_total,
+      *d_bubble;
+  unsigned char* d_tm;
+  Outs* d_outs;
+  const size_t S = std::max(1, total_stages), Gn = std::max(1, total_groups);
+  HPKP_CUDA(cudaMalloc(&d_c, sizeof(Cand) * n_cands));
+  HPKP_CUDA(cudaMalloc(&d_goff, sizeof(int) * goff.size()));
+  HPKP_CUDA(cudaMalloc(&d_mb, sizeof(int) * Gn));
+  HPKP_CUDA(cudaMalloc(&d_sty, sizeof(int) * S));
+  HPKP_CUDA(cudaMalloc(&d_sidx, sizeof(int) * S));
+  HPKP_CUDA(cudaMalloc(&d_snode, sizeof(int) * S));
+  HPKP_CUDA(cudaMalloc(&d_srank, sizeof(int) * S));
+  HPKP_CUDA(cudaMalloc(&d_layers, sizeof(int) * S));
+  HPKP_CUDA(cudaMalloc(&d_scap, sizeof(double) * S));
+  HPKP_CUDA(cudaMalloc(&d_prof, sizeof(double) * std::max<size_t>(1, prof.size())));
+  HPKP_CUDA(cudaMalloc(&d_tt, sizeof(double) * std::max<size_t>(1, tt_total)));
+  HPKP_CUDA(cudaMalloc(&d_tm, std::max<size_t>(1, tt_total)));
+  HPKP_CUDA(cudaMalloc(&d_gbest, sizeof(double) * std::max<size_t>(1, gbest_total)));
+  HPKP_CUDA(cudaMalloc(&d_time, sizeof(double) * S));
+  HPKP_CUDA(cudaMalloc(&d_mem, sizeof(double) * S));
+  HPKP_CUDA(cudaMalloc(&d_fill, sizeof(double) * Gn));
+  HPKP_CUDA(cudaMalloc(&d_steady, sizeof(double) * Gn));
+  HPKP_CUDA(cudaMalloc(&d_total, sizeof(double) * Gn));
+  HPKP_CUDA(cudaMalloc(&d_bubble, sizeof(double) * Gn));
+  HPKP_CUDA(cudaMalloc(&d_outs, sizeof(Outs) * n_cands));
+  auto up = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+    if (!bytes) return cudaSuccess;
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, cx.stream);
+  };
+  HPKP_CUDA(up(d_c, hc.data(), sizeof(Cand) * n_cands));
+  HPKP_CUDA(up(d_goff, goff.data(), sizeof(int) * goff.size()));
+  HPKP_CUDA(up(d_mb, mb.data(), sizeof(int) * mb.size()));
+  HPKP_CUDA(up(d_sty, sty.data(), sizeof(int) * sty.size()));
+  HPKP_CUDA(up(d_sidx, sidx.data(), sizeof(int) * sidx.size()));
+  HPKP_CUDA(up(d_snode, snode.data(), sizeof(int) * snode.size()));
+  HPKP_CUDA(up(d_srank, srank.data(), sizeof(int) * srank.size()));
+  HPKP_CUDA(up(d_scap, scap.data(), sizeof(double) * scap.size()));
+  HPKP_CUDA(up(d_prof, prof.data(), sizeof(double) * prof.size()));
+  HPKP_CUDA(cudaMemsetAsync(d_outs, 0, sizeof(Outs) * n_cands, cx.stream));
+  const long long h2d = (long long)(sizeof(Cand) * n_cands + sizeof(int) * (goff.size() + mb.size() + 4 * sty.size()) +
+                                    sizeof(double) * (scap.size() + prof.size()));
+  Args a;
+  a.cands = d_c;
+  a.group_stage_off = d_goff;
+  a.microbatches = d_mb;
+  a.stage_type = d_sty;
+  a.stage_index = d_sidx;
+  a.stage_cap = d_scap;
+  a.stage_node = d_snode;
+  a.stage_rank0 = d_srank;
+  a.prof = d_prof;
+  a.ttab = d_tt;
+  a.tmiss = d_tm;
+  a.gbest = d_gbest;
+  a.out_layers = d_layers;
+  a.out_time = d_time;
+  a.out_mem = d_mem;
+  a.out_fill = d_fill;
+  a.out_steady = d_steady;
+  a.out_total = d_total;
+  a.out_bubble = d_bubble;
+  a.outs = d_outs;
+  const size_t smem = max_smem_best * sizeof(double);
+  a.smem_best_doubles = max_smem_best;
+  HPKP_CUDA(cudaFuncSetAttribute(partition_cost_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  HPKP_CUDA(cudaEventRecord(cx.ev0, cx.stream));
+  partition_cost_kernel<<<n_cands, THREADS, smem, cx.stream>>>(a);
+  HPKP_CUDA(cudaGetLastError());
+  HPKP_CUDA(cudaEventRecord(cx.ev1, cx.stream));
+  std::vector<Outs> ho(n_cands);
+  std::vector<int> hl(S);
+  std::vector<double> htime(S), hmem(S), hfill(Gn), hsteady(Gn), htotal(Gn), hbub(Gn);
+  auto down = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, cx.stream);
+  };
+  HPKP_CUDA(down(ho.data(), d_outs, sizeof(Outs) * n_cands));
+  HPKP_CUDA(down(hl.data(), d_layers, sizeof(int) * S));
+  HPKP_CUDA(down(htime.data(), d_time, sizeof(double) * S));
+  HPKP_CUDA(down(hmem.data(), d_mem, sizeof(double) * S));
+  HPKP_CUDA(down(hfill.data(), d_fill, sizeof(double) * Gn));
+  HPKP_CUDA(down(hsteady.data(), d_steady, sizeof(double) * Gn));
+  HPKP_CUDA(down(htotal.data(), d_total, sizeof(double) * Gn));
+  HPKP_CUDA(down(hbub.data(), d_bubble, sizeof(double) * Gn));
+  HPKP_CUDA(cudaStreamSynchronize(cx.stream));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, cx.ev0, cx.ev1);
+  const long long d2h = (long long)(sizeof(Outs) * n_cands + S * (sizeof(int) + 2 * sizeof(double)) +
+                                    4 * Gn * sizeof(double));
+  hpk_timing_bridge::add_partition(ms, h2d, d2h);
+  for (int k = 0; k < n_cands; ++k) {
+    const Cand& c = hc[k];
+    hpk_plan_result& r = results[k];
+    const Outs& o = ho[k];
+    r.status = o.status;
+    r.fail_group = o.fail_group;
+    r.fail_kind = o.fail_kind;
+    r.missing_stage = o.missing_stage;
+    r.missing_layers = o.missing_layers;
+    r.t_sync = o.t_sync;
+    r.t_star = o.t_star;
+    const int ns = cands[k].group_stage_off[c.n_groups];
+    for (int s = 0; s < ns; ++s) {
+      if (r.stage_layers) r.stage_layers[s] = hl[c.stage_base + s];
+      if (r.stage_time) r.stage_time[s] = htime[c.stage_base + s];
+      if (r.stage_mem) r.stage_mem[s] = hmem[c.stage_base + s];
+    }
+    for (int j = 0; j < c.n_groups; ++j) {
+      if (r.group_fill) r.group_fill[j] = hfill[c.group_base + j];
+      if (r.group_steady) r.group_steady[j] = hsteady[c.group_base + j];
+      if (r.group_total) r.group_total[j] = htotal[c.group_base + j];
+      if (r.group_bubble) r.group_bubble[j] = hbub[c.group_base + j];
+    }
+  }
+  cudaFree(d_c);
+  cudaFree(d_goff);
+  cudaFree(d_mb);
+  cudaFree(d_sty);
+  cudaFree(d_sidx);
+  cudaFree(d_snode);
+  cudaFree(d_srank);
+  cudaFree(d_layers);
+  cudaFree(d_scap);
+  cudaFree(d_prof);
+  cudaFree(d_tt);
+  cudaFree(d_tm);
+  cudaFree(d_gbest);
+  cudaFree(d_time);
+  cudaFree(d_mem);
+  cudaFree(d_fill);
+  cudaFree(d_steady);
+  cudaFree(d_total);
+  cudaFree(d_bubble);
+  cudaFree(d_outs);
+  return 0;
+}

@@ -1,0 +1,505 @@
+// planner_b200.cpp — drop-in replacement of the reference planner translation
+// unit (P/src/planner.cpp; P = /root/reference/proj): the same
+//   hetplan::plan_cluster(spec, cfg, profile, memmodel, PlannerOptions)
+// (P/include/hetplan/planner.hpp:43-45), reached from hp_plan_compute
+// (P/src/c_api.cpp:185-208) unchanged.
+//
+// Control flow, status strings and exception behaviour follow planner.cpp
+// line by line; the arithmetic of the hot path runs on the B200:
+//   * every TP dimension's DP-grouping search is one problem of ONE batched
+//     hpk_grouping_search launch (grouping.cpp:269-335 semantics, bit-exact);
+//   * every candidate's layer partition + Eq. (1) cost is one CTA of ONE
+//     batched hpk_partition_cost launch (partition.cpp:51-110, cost.cpp:29-147).
+// Host work left here: option handling, TP-unit formation (build_tp_units,
+// reference code), the reference stage mapper (map_nodes_and_stages,
+// stage_map.cpp:63-216) and plan assembly/validation. There is no CPU
+// fallback: without a CUDA device plan_cluster throws InternalError.
+#include <algorithm>
+#include <cmath>
+#include <iostream>
+#include <map>
+#include <optional>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "hetplan/cost.hpp"
+#include "hetplan/grouping.hpp"
+#include "hetplan/partition.hpp"
+#include "hetplan/planner.hpp"
+#include "hetplan/stage_map.hpp"
+#include "hetplan/util.hpp"
+#include "hetplan_b200.h"
+
+
+namespace hetplan {
+
+namespace {
+
+// planner.cpp:34-50 — devices in spec order with (derived) powers.
+std::vector<GroupingDevice> grouping_devices(const ClusterSpec& spec,
+                                             const std::map<std::string, double>* powers) {
+  std::vector<GroupingDevice> out;
+  for (const auto& d : spec.all_devices()) {
+    const GpuType& t = spec.type_of(d);
+    double g = t.compute_power;
+    if (powers) {
+      auto it = powers->find(t.name);
+      if (it == powers->end()) {
+        throw InvalidArgumentError("derived powers missing GPU type " + t.name);
+      }
+      g = it->second;
+    }
+    out.push_back({d, t.name, g, t.memory});
+  }
+  return out;
+}
+
+// split_microbatches (plan.cpp:53-62): earlier groups take the remainder.
+std::vector<int> microbatch_split(int total, int n_groups) {
+  HP_CHECK(n_groups >= 1, "at least one group");
+  std::vector<int> out(n_groups, 0);
+  const int base = total / n_groups;
+  const int rem = total % n_groups;
+  for (int j = 0; j < n_groups; ++j) out[j] = std::max(1, base + (j < rem ? 1 : 0));
+  return out;
+}
+
+// Deferred exception, re-thrown where the reference would have thrown it.
+struct Pending {
+  enum Kind { NONE, INVALID, INFEASIBLE, INTERNAL } kind = NONE;
+  std::string msg;
+  [[noreturn]] void raise() const {
+    if (kind == INVALID) throw InvalidArgumentError(msg);
+    if (kind == INFEASIBLE) throw InfeasibleError(msg);
+    throw InternalError(msg);
+  }
+};
+
+template <typename Fn>
+Pending capture(Fn&& fn) {
+  Pending p;
+  try {
+    fn();
+  } catch (const InvalidArgumentError& e) {
+    p.kind = Pending::INVALID;
+    p.msg = e.what();
+  } catch (const InfeasibleError& e) {
+    p.kind = Pending::INFEASIBLE;
+    p.msg = e.what();
+  } catch (const InternalError& e) {
+    p.kind = Pending::INTERNAL;
+    p.msg = e.what();
+  }
+  return p;
+}
+
+// One candidate = one grouping of one TP dimension, mapped to stages.
+struct Candidate {
+  int tp = 0;
+  const GroupingSolution* grouping = nullptr;
+  Pending map_error;  // from map_nodes_and_stages
+  StageMapping mapping;
+  std::vector<int> microbatches;
+  // flattened GPU inputs
+  std::vector<int> goff, stype, sindex, snode, srank0;
+  std::vector<double> scap, prof;
+  std::vector<std::string> type_rows;
+  int n_bits = 0;
+  // GPU outputs
+  std::vector<int> layers;
+  std::vector<double> stime, smem, fill, steady, total, bubble;
+  hpk_plan_result res{};
+};
+
+struct TpWork {
+  int tp = 0;
+  CandidateSummary summary;
+  bool decided = false;          // summary final before search (divisibility, (3b) total)
+  Pending pre;                   // exception the reference raises before/inside the search
+  std::vector<TpUnit> units;
+  double min_mem = 0;
+  int problem = -1;              // index into the GPU search batch
+  std::vector<GroupingSolution> groupings;
+  std::vector<int> cand_ix;      // into candidates, grouping order
+};
+
+[[noreturn]] void gpu_fail(int rc) {
+  const char* msg = hpk_last_error();
+  std::string m = msg && *msg ? msg : "hetplan_b200: GPU engine failure";
+  if (rc == 6) throw InvalidArgumentError(m);
+  throw InternalError(m);
+}
+
+}  // namespace
+
+ParallelPlan plan_cluster(const ClusterSpec& spec, const ModelConfig& cfg,
+                          const ProfileTable& profile, const MemoryModel& memmodel,
+                          const PlannerOptions& options) {
+  hpk_reset_timing();
+  // planner.cpp:119-126
+  std::vector<int> tp_dims = options.tp_dims;
+  const std::vector<int> valid = enumerate_tp_dims(spec);
+  if (tp_dims.empty()) {
+    tp_dims = valid;
+  } else {
+    std::sort(tp_dims.begin(), tp_dims.end());
+    tp_dims.erase(std::unique(tp_dims.begin(), tp_dims.end()), tp_dims.end());
+  }
+  // planner.cpp:128-133
+  std::optional<std::map<std::string, double>> derived;
+  if (options.derive_power) {
+    std::string ref = options.power_reference;
+    if (ref.empty()) ref = spec.gpu_types.begin()->first;
+    derived = derive_power(profile, ref, 1);
+  }
+  std::map<std::string, int> type_key;
+  for (const auto& [name, t] : spec.gpu_types) {
+    (void)t;
+    type_key.emplace(name, (int)type_key.size());
+  }
+
+  // ---- phase 1: per-TP prechecks in the reference's order (grouping.cpp:270-289)
+  std::vector<TpWork> work(tp_dims.size());
+  std::vector<hpk_grouping_problem> problems;
+  std::vector<std::vector<double>> pw, pm;
+  std::vector<std::vector<int>> tk, nk;
+  problems.reserve(tp_dims.size());
+  for (size_t w = 0; w < tp_dims.size(); ++w) {
+    TpWork& tw = work[w];
+    const int tp = tp_dims[w];
+    tw.tp = tp;
+    tw.summary.tp_dim = tp;
+    if (std::find(valid.begin(), valid.end(), tp) == valid.end()) {
+      tw.summary.status = "infeasible: tp_dim does not divide every node's GPU count "
+                          "(divisibility)";
+      tw.decided = true;
+      continue;
+    }
+    std::vector<GroupingDevice> devices;
+    tw.pre = capture([&] {
+      devices = grouping_devices(spec, derived ? &*derived : nullptr);
+      tw.min_mem = options.min_mem_override > 0 ? options.min_mem_override
+                                                : memmodel.required_group_memory(cfg, tp);
+      double total_dev = 0;
+      for (const auto& d : devices) total_dev += d.memory;
+      const double big_l = std::max(total_dev, tw.min_mem) * 2 + 1;
+      if (cfg.n_microbatches < 1) {
+        throw InvalidArgumentError("grouping: n_microbatches must be >= 1");
+      }
+      tw.units = build_tp_units(devices, tp);
+      if (tw.units.empty()) throw InvalidArgumentError("grouping: no devices");
+      double total_mem = 0;
+      for (const auto& u : tw.units) total_mem += u.memory;
+      if (big_l > 0 && big_l <= tw.min_mem) {
+        throw InvalidArgumentError("grouping: big_l must exceed min_mem");
+      }
+      if (total_mem < tw.min_mem) {
+        throw InfeasibleError("grouping infeasible: total memory " + format_double(total_mem) +
+                              " B < MIN_mem " + format_double(tw.min_mem) +
+                              " B; no DP group assignment can satisfy the group memory "
+                              "constraint (3b)");
+      }
+    });
+    if (tw.pre.kind == Pending::INFEASIBLE) {
+      tw.summary.status = std::string("infeasible: ") + tw.pre.msg;
+      tw.pre = Pending{};
+      tw.decided = true;
+      continue;
+    }
+    if (tw.pre.kind != Pending::NONE) continue;  // raised when this TP is reached
+    const int n = (int)tw.units.size();
+    pw.emplace_back(n);
+    pm.emplace_back(n);
+    tk.emplace_back(n);
+    nk.emplace_back(n);
+    for (int i = 0; i < n; ++i) {
+      pw.back()[i] = tw.units[i].power;
+      pm.back()[i] = tw.units[i].memory;
+      tk.back()[i] = type_key.at(tw.units[i].gpu_type);
+      nk.back()[i] = tw.units[i].node_id;
+    }
+    hpk_grouping_problem pr;
+    pr.n = n;
+    pr.n_microbatches = cfg.n_microbatches;
+    pr.min_mem = tw.min_mem;
+    pr.exact_threshold = options.exact_threshold;
+    pr.node_budget = options.node_budget;
+    pr.top_k = std::max(1, options.top_k);
+    tw.problem = (int)problems.size();
+    problems.push_back(pr);
+  }
+  for (size_t k = 0; k < problems.size(); ++k) {
+    problems[k].power = pw[k].data();
+    problems[k].memory = pm[k].data();
+    problems[k].type_key = tk[k].data();
+    problems[k].node_key = nk[k].data();
+  }
+
+  // ---- phase 2: one batched GPU search over every TP dimension
+  std::vector<hpk_grouping_result> gres(problems.size());
+  std::vector<std::vector<int>> rgs_buf(problems.size());
+  for (size_t k = 0; k < problems.size(); ++k) {
+    rgs_buf[k].assign((size_t)problems[k].top_k * problems[k].n, 0);
+    gres[k].rgs = rgs_buf[k].data();
+  }
+  if (!problems.empty()) {
+    if (hpk_device_count() <= 0) {
+      throw InternalError("hetplan_b200: no CUDA device visible; the B200 planner has no CPU "
+                          "fallback");
+    }
+    const int rc = hpk_grouping_search(problems.data(), (int)problems.size(), gres.data(),
+                                       nullptr);
+    if (rc != 0) gpu_fail(rc);
+  }
+
+  // ---- phase 3: groupings -> stage mapping -> candidate inputs (host)
+  std::vector<Candidate> cands;
+  for (auto& tw : work) {
+    if (tw.problem < 0) continue;
+    const hpk_grouping_result& r = gres[tw.problem];
+    if (r.status == 3) {
+      tw.summary.status = "infeasible: grouping infeasible: no partition satisfies the group "
+                          "memory constraint (3b)";
+      tw.decided = true;
+      continue;
+    }
+    const int n = (int)tw.units.size();
+    for (int k = 0; k < r.count; ++k) {  // make_solution, grouping.cpp:249-265
+      GroupingSolution sol;
+      const int* rgs = r.rgs + (size_t)k * n;
+      const int m = *std::max_element(rgs, rgs + n) + 1;
+      sol.groups.assign(m, {});
+      for (int i = 0; i < n; ++i) {
+        sol.groups[rgs[i]].push_back(tw.units[i]);
+        for (const auto& d : tw.units[i].devices) sol.assignment[d] = rgs[i];
+      }
+      for (int gi = 0; gi < m; ++gi) sol.valid_groups.push_back(gi);
+      sol.z = r.z[k];
+      sol.objective = r.objective[k];
+      sol.optimal = r.optimal != 0;
+      sol.nodes_visited = r.visited;
+      tw.groupings.push_back(std::move(sol));
+    }
+  }
+  for (auto& tw : work) {
+    for (size_t k = 0; k < tw.groupings.size(); ++k) {
+      Candidate c;
+      c.tp = tw.tp;
+      c.grouping = &tw.groupings[k];
+      c.map_error = capture([&] { c.mapping = map_nodes_and_stages(spec, *c.grouping, tw.tp); });
+      tw.cand_ix.push_back((int)cands.size());
+      cands.push_back(std::move(c));
+    }
+  }
+  int n_bits = 0;
+  while ((1 << n_bits) <= cfg.n_layers) ++n_bits;
+  std::vector<hpk_plan_candidate> pin;
+  std::vector<int> pin_of(cands.size(), -1);
+  for (size_t ci = 0; ci < cands.size(); ++ci) {
+    Candidate& c = cands[ci];
+    if (c.map_error.kind != Pending::NONE) continue;
+    const int G = (int)c.mapping.groups.size();
+    c.microbatches = microbatch_split(cfg.n_microbatches, G);
+    std::map<std::string, int> row;
+    c.goff.push_back(0);
+    for (int j = 0; j < G; ++j) {
+      for (const auto& slot : c.mapping.groups[j].stages) {
+        auto it = row.find(slot.unit.gpu_type);
+        if (it == row.end()) {
+          it = row.emplace(slot.unit.gpu_type, (int)c.type_rows.size()).first;
+          c.type_rows.push_back(slot.unit.gpu_type);
+        }
+        c.stype.push_back(it->second);
+        c.sindex.push_back(slot.stage_index);
+        c.scap.push_back(spec.gpu_types.at(slot.unit.gpu_type).memory);
+        c.snode.push_back(slot.unit.node_id);
+        c.srank0.push_back(spec.global_rank(slot.unit.devices.front()));
+      }
+      c.goff.push_back((int)c.stype.size());
+    }
+    c.n_bits = n_bits;
+    for (const auto& t : c.type_rows) {
+      for (int b = 0; b < n_bits; ++b) {
+        c.prof.push_back(profile.has(t, c.tp, 1 << b) ? profile.at(t, c.tp, 1 << b) : 0.0);
+      }
+    }
+    const size_t S = c.stype.size();
+    c.layers.assign(S, 0);
+    c.stime.assign(S, 0);
+    c.smem.assign(S, 0);
+    c.fill.assign(G, 0);
+    c.steady.assign(G, 0);
+    c.total.assign(G, 0);
+    c.bubble.assign(G, 0);
+    hpk_plan_candidate p;
+    p.n_layers = cfg.n_layers;
+    p.tp = c.tp;
+    p.k_total = cfg.n_microbatches;
+    p.n_groups = G;
+    p.ppb = memmodel.per_layer_param_bytes;
+    p.pab = memmodel.per_layer_activation_bytes;
+    p.opt_mult = memmodel.optimizer_multiplier;
+    p.cost_ppb = cfg.per_layer_param_bytes;
+    p.cost_pab = cfg.per_layer_activation_bytes;
+    p.intra_bw = spec.intra_node_bw;
+    p.inter_bw = spec.inter_node_bw;
+    p.sync_max = options.sync_overlap == SyncOverlap::max ? 1 : 0;
+    p.allow_zero = options.allow_zero_layer_stages ? 1 : 0;
+    p.group_stage_off = c.goff.data();
+    p.microbatches = c.microbatches.data();
+    p.stage_type = c.stype.data();
+    p.stage_index = c.sindex.data();
+    p.stage_mem_capacity = c.scap.data();
+    p.stage_node = c.snode.data();
+    p.stage_rank0 = c.srank0.data();
+    p.n_types = (int)c.type_rows.size();
+    p.n_bits = n_bits;
+    p.prof = c.prof.data();
+    pin_of[ci] = (int)pin.size();
+    pin.push_back(p);
+  }
+  // ---- phase 4: one batched GPU launch for every candidate's partition + cost
+  std::vector<hpk_plan_result> pres(pin.size());
+  for (size_t ci = 0; ci < cands.size(); ++ci) {
+    if (pin_of[ci] < 0) continue;
+    Candidate& c = cands[ci];
+    hpk_plan_result& r = pres[pin_of[ci]];
+    r.stage_layers = c.layers.data();
+    r.stage_time = c.stime.data();
+    r.stage_mem = c.smem.data();
+    r.group_fill = c.fill.data();
+    r.group_steady = c.steady.data();
+    r.group_total = c.total.data();
+    r.group_bubble = c.bubble.data();
+  }
+  if (!pin.empty()) {
+    const int rc = hpk_partition_cost(pin.data(), (int)pin.size(), pres.data(), -1);
+    if (rc != 0) gpu_fail(rc);
+  }
+
+  // ---- phase 5: the reference's selection loop (planner.cpp:138-205), replayed
+  std::optional<ParallelPlan> best;
+  std::vector<CandidateSummary> summaries;
+  for (auto& tw : work) {
+    if (tw.pre.kind != Pending::NONE) tw.pre.raise();
+    if (tw.decided) {
+      summaries.push_back(tw.summary);
+      continue;
+    }
+    CandidateSummary summary = tw.summary;
+    bool produced = false;
+    std::string last_error;
+    for (int ci : tw.cand_ix) {
+      Candidate& c = cands[ci];
+      if (c.map_error.kind != Pending::NONE) {
+        if (c.map_error.kind == Pending::INFEASIBLE) {
+          last_error = c.map_error.msg;
+          continue;
+        }
+        c.map_error.raise();
+      }
+      const hpk_plan_result& r = pres[pin_of[ci]];
+      const int G = (int)c.mapping.groups.size();
+      if (r.status == 3) {  // balance_workload InfeasibleError (partition.cpp:55-58, 85-89)
+        const int j = r.fail_group;
+        const int P = c.goff[j + 1] - c.goff[j];
+        if (r.fail_kind == 1) {
+          last_error = "balance_workload: " + std::to_string(cfg.n_layers) + " layers over " +
+                       std::to_string(P) + " stages; every stage needs at least one";
+        } else {
+          last_error =
+              "balance_workload: no layer split fits every stage's memory capacity (the "
+              "per-stage memory constraint is binding)";
+        }
+        continue;
+      }
+      if (r.status == 6) {  // ProfileTable::at / estimate_stage_time (profile.cpp:95-103,181)
+        if (r.missing_layers <= 0) {
+          throw InvalidArgumentError("estimate_stage_time: n_layers must be >= 1");
+        }
+        throw InvalidArgumentError("profile table: no entry for " +
+                                   c.type_rows[c.stype[r.missing_stage]] +
+                                   " tp=" + std::to_string(c.tp) +
+                                   " layers=" + std::to_string(r.missing_layers));
+      }
+      // assemble (planner.cpp:54-112)
+      ParallelPlan plan;
+      plan.tp_dim = c.tp;
+      plan.n_layers = cfg.n_layers;
+      plan.n_microbatches_total = cfg.n_microbatches;
+      plan.grouping.objective = c.grouping->objective;
+      plan.grouping.z = c.grouping->z;
+      plan.grouping.optimal = c.grouping->optimal;
+      plan.sync_overlap = options.sync_overlap == SyncOverlap::sum ? "sum" : "max";
+      int s = 0;
+      for (int j = 0; j < G; ++j) {
+        const auto& stages = c.mapping.groups[j].stages;
+        GroupPlan group;
+        group.microbatches = c.microbatches[j];
+        int cursor = 0;
+        for (const auto& slot : stages) {
+          StagePlan st;
+          st.stage_index = slot.stage_index;
+          st.gpu_type = slot.unit.gpu_type;
+          st.devices = slot.unit.devices;
+          st.layer_begin = cursor;
+          st.layer_end = cursor + c.layers[s];
+          cursor = st.layer_end;
+          st.est_time_s = c.stime[s];
+          st.est_mem_bytes = c.smem[s];
+          st.mem_capacity_bytes = spec.gpu_types.at(st.gpu_type).memory;
+          group.stages.push_back(std::move(st));
+          ++s;
+        }
+        plan.groups.push_back(std::move(group));
+        GroupCost gc;
+        gc.microbatches = c.microbatches[j];
+        gc.pipeline_fill = c.fill[j];
+        gc.steady = c.steady[j];
+        gc.total = c.total[j];
+        gc.bubble_ratio = c.bubble[j];
+        plan.cost.per_group.push_back(gc);
+      }
+      plan.cost.t_sync = r.t_sync;
+      plan.cost.t_star = r.t_star;
+      plan.validate();
+      summary.grouping_objective = c.grouping->objective;
+      summary.t_star = plan.cost.t_star;
+      summary.status = "candidate";
+      produced = true;
+      if (!best || plan.cost.t_star < best->cost.t_star) best = std::move(plan);
+      break;  // groupings are ordered best-first; take the first that maps
+    }
+    if (!produced) summary.status = "infeasible: " + last_error;
+    summaries.push_back(summary);
+  }
+
+  if (!best) {  // planner.cpp:193-200
+    std::ostringstream os;
+    os << "no feasible plan; per-TP-dimension binding constraints:";
+    for (const auto& s : summaries) os << "\n  tp=" << s.tp_dim << ": " << s.status;
+    throw InfeasibleError(os.str());
+  }
+  for (auto& s : summaries) {
+    if (s.status == "candidate" && s.tp_dim == best->tp_dim) s.status = "selected";
+  }
+  best->candidates = summaries;
+
+  if (options.validate_with_sim) {  // planner.cpp:207-219 (reference simulator, host)
+    SimOptions sim_opts;
+    sim_opts.combined_time = true;
+    PlanSimResult sim = simulate_1f1b(*best, profile, cfg, spec, sim_opts);
+    for (size_t j = 0; j < sim.groups.size(); ++j) {
+      const double estimated = best->cost.per_group[j].total;
+      const double simulated = sim.groups[j].pipeline.makespan;
+      if (estimated > 0 && std::abs(simulated - estimated) / estimated > 0.01) {
+        std::cerr << "warning: group " << j << " simulated makespan " << simulated
+                  << "s diverges >1% from estimate " << estimated << "s\n";
+      }
+    }
+  }
+  return *best;
+}
+
+}  // namespace hetplan
