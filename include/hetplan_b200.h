@@ -167,7 +167,8 @@ typedef struct hpk_search_config {
   long long segment_cap; /* visits per segment run per wave (0: default) */
   int max_list;          /* segment list capacity per problem (0: default) */
   int force_serial;      /* 1: use the serial replica kernel for every problem */
-  int max_waves;         /* watchdog on the wave loop (0: default 200000) */
+  int max_waves;         /* watchdog on the wave loop (0: default 1000000) */
+  double max_seconds;    /* device wall-clock watchdog (0: default 120 s) */
 } hpk_search_config;
 
 void hpk_search_config_init(hpk_search_config* cfg);
@@ -228,6 +229,10 @@ typedef struct hpk_timing {
 } hpk_timing;
 void hpk_last_timing(hpk_timing* out);
 void hpk_reset_timing(void);
+
+/* Issue-rate microbenchmarks (roofline denominators for this FP64/INT32-issue
+ * bound path): fp64 DMUL+DADD ops/s and int32 IADD+LOP ops/s on `device`. */
+int hpk_measure_issue_peaks(int device, double* fp64_ops_per_s, double* int_ops_per_s);
 
 #ifdef __cplusplus
 } /* extern "C" */

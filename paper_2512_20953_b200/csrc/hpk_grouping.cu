@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -59,20 +60,20 @@ struct GProb {
   double RM[MAXN + 1];  // remaining_mem from d, serial as grouping.cpp:156-160
 };
 
+// A segment of the ordered DFS list, stored in a per-problem entry pool; the
+// list itself holds 4-byte pool ids plus contiguous per-position state.
 struct __align__(16) Entry {
   uint8_t u[MAXN];         // segment root (entered by this segment's run)
   uint8_t end[MAXN];       // PREFIX: end marker (first node NOT in the segment)
-  uint8_t stop[MAXN];      // run output: next node to enter when the cap hit
-  uint8_t best_rgs[MAXN];  // run output: best leaf
-  double cutoff_used;
+  uint8_t best_rgs[MAXN];  // run output: best leaf of the segment
   double m;                // max feasible leaf objective (-1: none)
   double best_obj;
   long long visits;
   int best_G;
   int a_star;              // PREFIX re-run: depth of the pruned ancestor of `end`
-  uint8_t du, dend, dstop, kind;
-  uint8_t ran, finished, has_best, ran_now;
-  uint8_t capped, pad[7];
+  int cver;                // cutoff version of the last run (-1: never ran)
+  uint8_t du, dend, kind, finished;
+  uint8_t has_best, capped, pad[2];
 };
 
 struct GState {
@@ -80,8 +81,11 @@ struct GState {
   long long V;       // committed visits
   double best_obj;
   int best_G, has_best;
+  int cver;          // version of C (bumped whenever C changes)
   int cur, head, len;
-  int done, aborted, rerun_pending, pad;
+  int done, aborted, rerun_pending, pool_cur;
+  int pool_top;      // bump allocator of the active pool (atomic)
+  int pad0;
   long long rerun_cap;
   double seed_obj, seed_z;
   int seed_ix, waves;
@@ -92,7 +96,7 @@ struct GState {
 };
 
 struct RunItem {
-  int problem, index;
+  int problem, pos, id, front;
   long long cap;
 };
 
@@ -104,20 +108,29 @@ struct RunQueue {
 struct KParams {
   GProb* probs;
   GState* states;
-  Entry* lists;       // [P][2][lcap]
+  Entry* pools;       // [P][2][pcap]
+  int* lists;         // [P][2][4][lcap]: ids, pcver, cnt, pfirst
   int* scratch;       // [P][lcap + 1]
   RunQueue* queues;   // [2]
   RunItem* items;     // [2][qcap]
   int* active;        // problems still running
   int* err;           // watchdog flags
   int n_problems;
-  int lcap, qcap, qmax;
+  int lcap, pcap, qcap, qmax, reserve;
   long long seg_cap;
   int max_waves;
+  unsigned long long deadline_ns;  // %globaltimer watchdog (relative at launch)
+  unsigned long long* deadline_slot;
+  int trace;                       // HPK_TRACE=1: per-wave scheduler printf (debug)
 };
 
-__device__ __forceinline__ Entry* list_ptr(const KParams& kp, int p, int buf) {
-  return kp.lists + ((size_t)p * 2 + buf) * kp.lcap;
+__device__ __forceinline__ Entry* pool_ptr(const KParams& kp, int p, int which) {
+  return kp.pools + ((size_t)p * 2 + which) * kp.pcap;
+}
+// list arrays of buffer `buf`: 0 ids, 1 pcver (cutoff version of a finished
+// run at this position, -1 = needs a run), 2 cnt (expansion count), 3 pfirst
+__device__ __forceinline__ int* list_arr(const KParams& kp, int p, int buf, int which) {
+  return kp.lists + (((size_t)p * 2 + buf) * 4 + which) * kp.lcap;
 }
 
 // --------------------------------------------------------------- warp DFS
@@ -243,12 +256,15 @@ struct RunOut {
   double m;
   bool finished, has_best;
   double best_obj;
-  int best_G, a_star, dstop;
+  int best_G, a_star;
+  int dstop;   // unfinished: the stop node is path[0..dstop-1) + [stop_c]
+  int stop_c;
 };
 
 // DFS of subtree(E.u) in preorder (PREFIX: stopping before E.end), cap visits.
 __device__ RunOut run_segment(const GProb& P, const Entry* E, Entry* Eout, double C,
-                              long long cap, WarpSmem* sm, int lane, int* err) {
+                              long long cap, WarpSmem* sm, int lane, int* err,
+                              unsigned long long deadline) {
   const int n = P.n;
   const int du = E->du;
   const bool prefix = E->kind == KIND_PREFIX;
@@ -262,6 +278,7 @@ __device__ RunOut run_segment(const GProb& P, const Entry* E, Entry* Eout, doubl
     z.best_G = 0;
     z.a_star = -1;
     z.dstop = 0;
+    z.stop_c = 0;
     return z;
   }
   const int dend = prefix ? E->dend : 0;
@@ -282,6 +299,7 @@ __device__ RunOut run_segment(const GProb& P, const Entry* E, Entry* Eout, doubl
     if (grp == G) ++G;
     if (lane == 0) sm->Gat[i + 1] = (uint8_t)G;
   }
+  __syncwarp();
   RunOut o;
   o.visits = 0;
   o.m = -1.0;
@@ -291,10 +309,12 @@ __device__ RunOut run_segment(const GProb& P, const Entry* E, Entry* Eout, doubl
   o.best_G = 0;
   o.a_star = -1;
   o.dstop = 0;
+  o.stop_c = 0;
   double cut = C;
   int match = prefix ? du : -1;
   long long iters = 0;
-  const long long max_iters = 4 * cap + 4 * MAXN + 64;  // watchdog (never hit when correct)
+  // watchdog (never hit when correct): each iteration visits, pops or batches
+  const long long max_iters = cap > (1LL << 40) ? (1LL << 62) : 4 * cap + 4 * MAXN + 64;
 
   // Enter the segment root u.
   {
@@ -303,6 +323,7 @@ __device__ RunOut run_segment(const GProb& P, const Entry* E, Entry* Eout, doubl
     add_unit(g, lane, grp, P.p[i], P.m[i]);
     if (grp == G) ++G;
     if (lane == 0) sm->Gat[du] = (uint8_t)G;
+    __syncwarp();
     o.visits = 1;
   }
   int d = du;
@@ -356,6 +377,16 @@ __device__ RunOut run_segment(const GProb& P, const Entry* E, Entry* Eout, doubl
       if (lane == 0) atomicOr(err, 1);
       o.finished = true;
       break;
+    }
+    if ((iters & 1023) == 0) {  // wall-clock watchdog (uniform: lane 0's clock)
+      unsigned long long now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      now = __shfl_sync(HPK_FULL_MASK, now, 0);
+      if (now > deadline) {
+        if (lane == 0) atomicOr(err, 2);
+        o.finished = true;
+        break;
+      }
     }
     if (d == n - 1) {
       // ---- leaf batch: children c = c0..G are leaves (unit n-1) ----
@@ -469,15 +500,15 @@ __device__ RunOut run_segment(const GProb& P, const Entry* E, Entry* Eout, doubl
             o.best_G = best_Gc;
             for (int i = lane; i < n - 1; i += 32) sm->best[i] = sm->path[i];
             if (lane == 0) sm->best[n - 1] = (uint8_t)best_c;
+            __syncwarp();
           }
           o.m = mx > o.m ? mx : o.m;
           cut = mx > cut ? mx : cut;
         }
       }
       if (cap_hit) {
-        for (int i = lane; i < d; i += 32) Eout->stop[i] = sm->path[i];
-        if (lane == 0) Eout->stop[d] = (uint8_t)(c0 + count);
         o.dstop = d + 1;
+        o.stop_c = c0 + count;
         o.finished = false;
         break;
       }
@@ -509,14 +540,14 @@ __device__ RunOut run_segment(const GProb& P, const Entry* E, Entry* Eout, doubl
       }
     }
     if (o.visits >= cap) {
-      for (int i = lane; i < d; i += 32) Eout->stop[i] = sm->path[i];
-      if (lane == 0) Eout->stop[d] = (uint8_t)c;
       o.dstop = d + 1;
+      o.stop_c = c;
       o.finished = false;
       break;
     }
     o.visits += 1;
     if (lane == 0) sm->nxt[d] = (uint8_t)(c + 1);
+    __syncwarp();  // every lane re-reads nxt[d] at the next iteration
     // ---- check child c (internal node at depth d+1) on its owner lane ----
     int dec;
     {
@@ -566,6 +597,7 @@ __device__ RunOut run_segment(const GProb& P, const Entry* E, Entry* Eout, doubl
     }
     // ---- descend into child c ----
     if (lane == 0) sm->path[d] = (uint8_t)c;
+    __syncwarp();
     add_unit(g, lane, c, P.p[d], P.m[d]);
     if (c == G) ++G;
     if (prefix && match == d && c == sm->endp[d]) match = d + 1;
@@ -601,37 +633,65 @@ __device__ __forceinline__ bool is_prefix_of(const uint8_t* a, int la, const uin
   return true;
 }
 
-// number of remainder pieces of subtree(u) after stop point q
-__device__ int n_pieces(const Entry& e) {
-  int pm[MAXN + 1];  // pm[d] = #groups of q[0..d)
-  pm[0] = 0;
-  for (int i = 0; i < e.dstop; ++i) pm[i + 1] = max(pm[i], (int)e.stop[i] + 1);
-  int cnt = 1;
-  for (int d = e.dstop - 1; d >= (int)e.du; --d) cnt += pm[d] - e.stop[d];
-  return cnt;
-}
-
-// piece k (0-based) of the remainder: writes its path into out, returns depth
-__device__ int piece_path(const Entry& e, int k, uint8_t* out) {
-  const int dq = e.dstop;
-  if (k == 0) {
-    for (int i = 0; i < dq; ++i) out[i] = e.stop[i];
-    return dq;
+// Split of an unfinished run (warp-level, right after the run): the entry
+// becomes the PREFIX record [u, stop) and the remainder of subtree(u) becomes
+// new FULL pieces in preorder — subtree(stop), then the right siblings of stop
+// and of each of its ancestors down to u's children. Pieces are allocated from
+// the problem's entry pool; returns the piece count (0: pool full, run dropped).
+__device__ int split_run(const KParams& kp, int p, GState& S, Entry* E, const RunOut& o,
+                         WarpSmem* sm, int lane, bool front, int* first_out) {
+  const int du = E->du;
+  const int d = o.dstop - 1;  // the stop node is child stop_c of path[0..d)
+  // level table: lev = d (siblings after stop_c), then lev = d-1 .. du
+  int count = 1 + ((int)sm->Gat[d] - o.stop_c);
+  for (int lev = d - 1; lev >= du; --lev) count += (int)sm->Gat[lev] - (int)sm->path[lev];
+  int first = 0;
+  if (lane == 0) {
+    const int limit = kp.pcap - (front ? 0 : kp.reserve);
+    first = atomicAdd(&S.pool_top, count);
+    if (first + count > limit) first = -1;
   }
-  int pm[MAXN + 1];
-  pm[0] = 0;
-  for (int i = 0; i < dq; ++i) pm[i + 1] = max(pm[i], (int)e.stop[i] + 1);
-  int idx = k - 1;
-  for (int d = dq - 1; d >= (int)e.du; --d) {
-    const int cnt = pm[d] - e.stop[d];
-    if (idx < cnt) {
-      for (int i = 0; i < d; ++i) out[i] = e.stop[i];
-      out[d] = (uint8_t)(e.stop[d] + 1 + idx);
-      return d + 1;
+  first = shfl(first, 0);
+  if (first < 0) return 0;
+  Entry* pool = pool_ptr(kp, p, S.pool_cur);
+  for (int k = lane; k < count; k += 32) {
+    int lev, child;
+    if (k == 0) {
+      lev = d;
+      child = o.stop_c;
+    } else {
+      int idx = k - 1;
+      lev = d;
+      int base = o.stop_c;
+      int cnt = (int)sm->Gat[d] - base;
+      while (idx >= cnt) {
+        idx -= cnt;
+        --lev;
+        base = sm->path[lev];
+        cnt = (int)sm->Gat[lev] - base;
+      }
+      child = base + 1 + idx;
     }
-    idx -= cnt;
+    Entry& q = pool[first + k];
+    for (int i = 0; i < lev; ++i) q.u[i] = sm->path[i];
+    q.u[lev] = (uint8_t)child;
+    q.du = (uint8_t)(lev + 1);
+    q.kind = KIND_FULL;
+    q.cver = -1;
+    q.finished = 0;
+    q.capped = 0;
+    q.has_best = 0;
+    q.a_star = -1;
   }
-  return -1;  // unreachable
+  // the entry itself becomes the prefix record [u, stop)
+  for (int i = lane; i < d; i += 32) E->end[i] = sm->path[i];
+  if (lane == 0) {
+    E->end[d] = (uint8_t)o.stop_c;
+    E->dend = (uint8_t)(d + 1);
+    E->kind = KIND_PREFIX;
+  }
+  *first_out = first;
+  return count;
 }
 
 // Block-wide exclusive scan of a[0..len) in place; returns the total.
@@ -643,14 +703,22 @@ __device__ int block_scan_excl(int* a, int len, int* smem_tmp) {
   for (int i = lo; i < hi; ++i) s += a[i];
   smem_tmp[tid] = s;
   __syncthreads();
-  if (tid == 0) {
-    int run = 0;
-    for (int t = 0; t < nt; ++t) {
+  if (tid < 32) {  // warp scan over the nt partial sums
+    const int per2 = (nt + 31) / 32;
+    int loc = 0;
+    for (int t = tid * per2; t < min(nt, (tid + 1) * per2); ++t) loc += smem_tmp[t];
+    int inc = loc;
+    for (int off = 1; off < 32; off <<= 1) {
+      const int v = __shfl_up_sync(HPK_FULL_MASK, inc, off);
+      if (tid >= off) inc += v;
+    }
+    int run = inc - loc;
+    for (int t = tid * per2; t < min(nt, (tid + 1) * per2); ++t) {
       const int v = smem_tmp[t];
       smem_tmp[t] = run;
       run += v;
     }
-    smem_tmp[nt] = run;
+    if (tid == 31) smem_tmp[nt] = inc;
   }
   __syncthreads();
   int run = smem_tmp[tid];
@@ -664,54 +732,60 @@ __device__ int block_scan_excl(int* a, int len, int* smem_tmp) {
   return total;
 }
 
-__device__ void push_items(const KParams& kp, int queue, int p, const Entry* L, int head, int len,
-                           double C, int lane) {
-  // first qmax entries (list order) that need a run at cutoff C
-  RunQueue* q = kp.queues + queue;
-  RunItem* items = kp.items + (size_t)queue * kp.qcap;
-  int pushed = 0;
-  for (int base = 0; base < len && pushed < kp.qmax; base += 32) {
-    const int i = base + lane;
-    bool need = false;
-    if (i < len) {
-      const Entry& e = L[head + i];
-      need = !(e.ran && e.cutoff_used == C) && !e.capped;
-    }
-    const unsigned bal = __ballot_sync(HPK_FULL_MASK, need);
-    int cnt = __popc(bal);
-    if (pushed + cnt > kp.qmax) cnt = kp.qmax - pushed;
-    int slot0 = 0;
-    if (lane == 0 && cnt > 0) slot0 = atomicAdd(&q->len, cnt);
-    slot0 = shfl(slot0, 0);
-    const int rank = __popc(bal & ((1u << lane) - 1));
-    if (need && rank < cnt && slot0 + rank < kp.qcap) {
-      items[slot0 + rank].problem = p;
-      items[slot0 + rank].index = head + i;
-      items[slot0 + rank].cap = kp.seg_cap;
-    }
-    pushed += cnt;
-  }
-}
-
 __device__ void finish_problem(const KParams& kp, GState& S) {
   S.done = 1;
   atomicSub(kp.active, 1);
 }
 
-// Per-problem scheduler: split, ordered commit, queue the next wave.
+// Queue the first qmax positions (list order) that need a run at cutoff version cver.
+__device__ void push_items(const KParams& kp, int queue, int p, const int* ids, const int* pcv,
+                           int head, int len, int cver, int qmax, int lane) {
+  RunQueue* q = kp.queues + queue;
+  RunItem* items = kp.items + (size_t)queue * kp.qcap;
+  int pushed = 0;
+  for (int base = 0; base < len && pushed < qmax; base += 32) {
+    const int i = base + lane;
+    const bool need = i < len && pcv[head + i] != cver;
+    const unsigned bal = __ballot_sync(HPK_FULL_MASK, need);
+    int cnt = __popc(bal);
+    if (pushed + cnt > qmax) cnt = qmax - pushed;
+    int slot0 = 0;
+    if (lane == 0 && cnt > 0) slot0 = atomicAdd(&q->len, cnt);
+    slot0 = shfl(slot0, 0);
+    const int rank = __popc(bal & ((1u << lane) - 1));
+    if (need && rank < cnt && slot0 + rank < kp.qcap) {
+      RunItem& it = items[slot0 + rank];
+      it.problem = p;
+      it.pos = head + i;
+      it.id = ids[head + i];
+      it.front = (i == 0);
+      it.cap = kp.seg_cap;
+    }
+    pushed += cnt;
+  }
+}
+
+// Per-problem scheduler (one CTA): expand splits, ordered commit, compaction,
+// queue the next wave.
 __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* smem_tmp) {
   GState& S = kp.states[p];
   const GProb& P = kp.probs[p];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (S.done) return;
-  Entry* Lin = list_ptr(kp, p, S.cur);
-  Entry* Lout = list_ptr(kp, p, S.cur ^ 1);
-  const int head = S.head, len = S.len;
+  const int cur = S.cur, head = S.head, len = S.len;
+  int* ids_in = list_arr(kp, p, cur, 0);
+  int* pcv_in = list_arr(kp, p, cur, 1);
+  int* cnt_in = list_arr(kp, p, cur, 2);
+  int* pf_in = list_arr(kp, p, cur, 3);
+  int* ids_out = list_arr(kp, p, cur ^ 1, 0);
+  int* pcv_out = list_arr(kp, p, cur ^ 1, 1);
+  int* cnt_out = list_arr(kp, p, cur ^ 1, 2);
+  Entry* pool = pool_ptr(kp, p, S.pool_cur);
 
   if (S.rerun_pending) {
     // the capped re-run of the overflow segment (at the head) is back
     if (tid == 0) {
-      const Entry& e = Lin[head];
+      const Entry& e = pool[ids_in[head]];
       if (e.has_best && (!S.has_best || e.best_obj > S.best_obj ||
                          (e.best_obj == S.best_obj && e.best_G < S.best_G))) {
         S.has_best = 1;
@@ -728,95 +802,76 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
     return;
   }
 
-  // ---- A. split: unfinished FULL runs -> PREFIX record + remainder pieces
-  int* cnt = kp.scratch + (size_t)p * (kp.lcap + 1);
-  for (int i = tid; i < len; i += blockDim.x) {
-    const Entry& e = Lin[head + i];
-    int c = 1;
-    if (e.ran_now && e.kind == KIND_FULL && !e.finished && !e.capped) c += n_pieces(e);
-    cnt[i] = c;
-  }
+  // ---- A. expand the splits made by this wave's runs (cnt = 1 + pieces)
+  int* off = kp.scratch + (size_t)p * (kp.lcap + 1);
+  for (int i = tid; i < len; i += blockDim.x) off[i] = cnt_in[head + i];
   __syncthreads();
-  if (tid == 0) {
-    // capacity: keep splits in list order while they fit; the first split
-    // always proceeds (progress guarantee). Dropped splits are re-run later.
-    long long total = 0;
-    for (int i = 0; i < len; ++i) total += cnt[i];
-    if (total > kp.lcap) {
-      long long run = 0;
-      bool first = true;
+  int total = block_scan_excl(off, len, smem_tmp);
+  if (total > kp.lcap) {
+    // Not enough list room: keep expansions in list order while they fit; the
+    // others are reverted to unrun FULL segments (their pieces become garbage).
+    if (tid == 0) {
+      int budget = kp.lcap - len;
       for (int i = 0; i < len; ++i) {
-        if (cnt[i] > 1) {
-          if (first || run + cnt[i] + (len - i - 1) <= kp.lcap) {
-            first = false;
+        const int c = (i + 1 < len ? off[i + 1] : total) - off[i];
+        off[i] = c;
+        if (c > 1) {
+          if (c - 1 <= budget) {
+            budget -= c - 1;
           } else {
-            cnt[i] = 1;
-            Lin[head + i].ran = 0;  // discard the partial run
-            Lin[head + i].ran_now = 0;
+            off[i] = 1;
+            Entry& e = pool[ids_in[head + i]];
+            e.kind = KIND_FULL;
+            e.cver = -1;
+            e.finished = 0;
+            pcv_in[head + i] = -1;
           }
         }
-        run += cnt[i];
       }
     }
+    __syncthreads();
+    total = block_scan_excl(off, len, smem_tmp);
   }
+  if (tid == 0) off[len] = total;
   __syncthreads();
-  const int total = block_scan_excl(cnt, len, smem_tmp);
-  if (tid == 0) cnt[len] = total;
-  __syncthreads();
-  // write the new list: one output slot per thread iteration
   for (int o = tid; o < total; o += blockDim.x) {
-    int lo = 0, hi = len;  // largest i with cnt[i] <= o
+    int lo = 0, hi = len;  // largest i with off[i] <= o
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
-      if (cnt[mid] <= o) lo = mid;
+      if (off[mid] <= o) lo = mid;
       else hi = mid;
     }
-    const int i = lo;
-    const int k = o - cnt[i];
-    const Entry& e = Lin[head + i];
-    const bool split = (cnt[i + 1] - cnt[i]) > 1;
-    Entry& out = Lout[o];
+    const int k = o - off[lo];
     if (k == 0) {
-      out = e;
-      out.ran_now = 0;
-      if (split) {
-        out.kind = KIND_PREFIX;
-        for (int j = 0; j < e.dstop; ++j) out.end[j] = e.stop[j];
-        out.dend = e.dstop;
-        out.finished = 1;
-      }
+      ids_out[o] = ids_in[head + lo];
+      pcv_out[o] = pcv_in[head + lo];
     } else {
-      const int du = piece_path(e, k - 1, out.u);
-      out.du = (uint8_t)du;
-      out.kind = KIND_FULL;
-      out.ran = 0;
-      out.ran_now = 0;
-      out.finished = 0;
-      out.capped = 0;
-      out.has_best = 0;
-      out.a_star = -1;
+      ids_out[o] = pf_in[head + lo] + k - 1;
+      pcv_out[o] = -1;
     }
+    cnt_out[o] = 1;
   }
   __syncthreads();
 
   // ---- B. ordered commit walk (warp 0)
+  __shared__ int sh_head, sh_flag;
+  __shared__ long long sh_cap;
   if (warp == 0) {
     double C = S.C;
+    int cver = S.cver;
     long long V = S.V;
     const long long B = P.budget;
     int i = 0;
-    int new_head = 0;
     int done = 0, aborted = 0, rerun = 0;
     long long rerun_cap = 0;
     while (i < total) {
       const int j = i + lane;
-      bool ok = false;
+      const bool ok = j < total && pcv_out[j] == cver;
       long long v = 0;
       double m = -1, bo = 0;
       int bg = 0, hb = 0, ast = -1, kind = 0;
-      if (j < total) {
-        const Entry& e = Lout[j];
-        ok = e.ran && e.cutoff_used == C && e.finished && !e.capped;
+      if (ok) {
+        const Entry& e = pool[ids_out[j]];
         v = e.visits;
         m = e.m;
         hb = e.has_best;
@@ -827,12 +882,11 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
       }
       const unsigned bad = __ballot_sync(HPK_FULL_MASK, !ok);
       const int first_bad = bad ? __ffs(bad) - 1 : 32;
-      // inclusive scan of visits
-      long long cum = v;
+      long long cum = v;  // inclusive scan of visits
 #pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const long long t = __shfl_up_sync(HPK_FULL_MASK, cum, off);
-        if (lane >= off) cum += t;
+      for (int o2 = 1; o2 < 32; o2 <<= 1) {
+        const long long t = __shfl_up_sync(HPK_FULL_MASK, cum, o2);
+        if (lane >= o2) cum += t;
       }
       const bool imp = ok && m > C;
       const bool del = ok && kind == KIND_PREFIX && ast >= 0;
@@ -842,8 +896,7 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
       int kc = first_bad;  // lanes [0, kc) are processed this chunk
       if (first_sp < kc) kc = first_sp + 1;
       const bool special_last = kc > 0 && first_sp == kc - 1;
-      // budget overflow inside the special lane: do not commit it, re-run capped
-      bool overflow = false;
+      bool overflow = false;  // budget runs out INSIDE the special lane: re-run it capped
       if (special_last) {
         const long long cum_l = shfl(cum, kc - 1);
         const int over_l = shfl((int)over, kc - 1);
@@ -860,23 +913,23 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
       }
       double mm = (lane < kcommit) ? m : -1.0;
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        const double oo = __shfl_xor_sync(HPK_FULL_MASK, ko, off);
-        const int og = __shfl_xor_sync(HPK_FULL_MASK, kg, off);
-        const int oi = __shfl_xor_sync(HPK_FULL_MASK, ki, off);
+      for (int o2 = 16; o2 > 0; o2 >>= 1) {
+        const double oo = __shfl_xor_sync(HPK_FULL_MASK, ko, o2);
+        const int og = __shfl_xor_sync(HPK_FULL_MASK, kg, o2);
+        const int oi = __shfl_xor_sync(HPK_FULL_MASK, ki, o2);
         if (oo >= 0 && (ko < 0 || key_better(oo, og, oi, ko, kg, ki))) {
           ko = oo;
           kg = og;
           ki = oi;
         }
-        const double om = __shfl_xor_sync(HPK_FULL_MASK, mm, off);
+        const double om = __shfl_xor_sync(HPK_FULL_MASK, mm, o2);
         mm = om > mm ? om : mm;
       }
       const int gh = *((volatile int*)&S.has_best);
       const double gbo = *((volatile double*)&S.best_obj);
       const int gbg = *((volatile int*)&S.best_G);
       if (ko >= 0 && (!gh || ko > gbo || (ko == gbo && kg < gbg))) {
-        const Entry& w = Lout[i + ki];
+        const Entry& w = pool[ids_out[i + ki]];
         for (int t = lane; t < P.n; t += 32) S.best_rgs[t] = w.best_rgs[t];
         if (lane == 0) {
           S.has_best = 1;
@@ -886,7 +939,10 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
       }
       __syncwarp();
       if (kcommit > 0) V += shfl(cum, kcommit - 1);
-      C = mm > C ? mm : C;
+      if (mm > C) {
+        C = mm;
+        ++cver;
+      }
       i += kcommit;
       if (overflow) {
         rerun = 1;
@@ -897,13 +953,16 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
         const int jl = i - 1;  // the special entry, now committed
         const int del_l = shfl((int)del, kc - 1);
         if (del_l) {
-          const Entry& e = Lout[jl];
+          const Entry& e = pool[ids_out[jl]];
           const int la = e.a_star;
           int ndel = 0;
           for (int base = jl + 1; base < total; base += 32) {
             const int t = base + lane;
             bool inside = false;
-            if (t < total) inside = is_prefix_of(e.end, la, Lout[t].u, Lout[t].du);
+            if (t < total) {
+              const Entry& f = pool[ids_out[t]];
+              inside = is_prefix_of(e.end, la, f.u, f.du);
+            }
             const unsigned bin = __ballot_sync(HPK_FULL_MASK, inside);
             const int firstout = (~bin) ? __ffs(~bin) - 1 : 32;
             ndel += firstout;
@@ -917,21 +976,23 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
         }
         break;  // entries after a special one ran under a different state
       }
-      if (kc < 32) break;  // reached an entry that still needs a run
+      if (kc < 32) break;  // reached a position that still needs a run
     }
-    new_head = i;
     if (lane == 0) {
+      if (kp.trace)
+        printf("[hpk] wave %d p %d len %d total %d commit %d V %lld C %.17g cver %d pool %d\n",
+               S.waves, p, len, total, i, V, C, cver, S.pool_top);
       S.C = C;
+      S.cver = cver;
       S.V = V;
-      S.cur ^= 1;
-      S.head = new_head;
-      S.len = total - new_head;
+      S.cur = cur ^ 1;
+      S.head = i;
+      S.len = total - i;
       S.waves += 1;
       S.max_list = max(S.max_list, total);
       if (rerun) {
         S.rerun_pending = 1;
         S.rerun_cap = rerun_cap;
-        Lout[new_head].capped = 1;
       }
       if (done) {
         S.aborted = aborted;
@@ -940,20 +1001,57 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
         S.aborted = 0;
         finish_problem(kp, S);
       }
+      sh_head = i;
+      sh_flag = (S.done ? 0 : 1) | (rerun ? 2 : 0);
+      sh_cap = rerun_cap;
     }
-    __syncwarp();
-    const int flag = shfl(lane == 0 ? ((S.done ? 0 : 1) | (rerun ? 2 : 0)) : 0, 0);
+  }
+  __syncthreads();
+  const int flag = sh_flag;
+  int nhead = sh_head;
+  const int nlen = total - nhead;
+  // ---- C. pool compaction when the bump allocator is nearly exhausted
+  if ((flag & 1) && S.pool_top > kp.pcap - 2 * kp.reserve - 64 * 32) {
+    Entry* np = pool_ptr(kp, p, S.pool_cur ^ 1);
+    int* pcv_tmp = list_arr(kp, p, cur, 1);  // the input buffer is free now
+    for (int k = tid; k < nlen; k += blockDim.x) {
+      np[k] = pool[ids_out[nhead + k]];
+      pcv_tmp[k] = pcv_out[nhead + k];
+    }
+    __syncthreads();
+    for (int k = tid; k < nlen; k += blockDim.x) {
+      ids_out[k] = k;
+      pcv_out[k] = pcv_tmp[k];
+      cnt_out[k] = 1;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      S.pool_cur ^= 1;
+      S.pool_top = nlen;
+      S.head = 0;
+    }
+    nhead = 0;
+    __syncthreads();
+  }
+  // ---- D. queue the next wave
+  if (warp == 0) {
     if (flag & 2) {
       if (lane == 0) {
+        Entry& e = pool_ptr(kp, p, S.pool_cur)[ids_out[nhead]];
+        e.capped = 1;
         RunQueue* q = kp.queues + next_queue;
         const int slot = atomicAdd(&q->len, 1);
-        RunItem* items = kp.items + (size_t)next_queue * kp.qcap;
-        items[slot].problem = p;
-        items[slot].index = new_head;
-        items[slot].cap = rerun_cap;
+        RunItem& it = kp.items[(size_t)next_queue * kp.qcap + slot];
+        it.problem = p;
+        it.pos = nhead;
+        it.id = ids_out[nhead];
+        it.front = 1;
+        it.cap = sh_cap;
       }
     } else if (flag & 1) {
-      push_items(kp, next_queue, p, Lout, new_head, total - new_head, C, lane);
+      const int act = max(1, *((volatile int*)kp.active));
+      const int qmax = max(32, kp.qmax / act);
+      push_items(kp, next_queue, p, ids_out, pcv_out, nhead, nlen, S.cver, qmax, lane);
     }
   }
   __syncthreads();
@@ -1071,26 +1169,33 @@ __device__ void init_problem(const KParams& kp, int p) {
     double bound = 0;
     for (int i = 0; i < n; ++i) bound += P.p[i];
     const bool pruned = (S.C >= 0 && bound < S.C) || (0.0 > P.RM[0]);
+    S.cver = 0;
+    S.pool_cur = 0;
+    S.pool_top = 1;
     if (pruned) {
       S.len = 0;
       S.done = 1;
       atomicSub(kp.active, 1);
     } else {
-      Entry& e = list_ptr(kp, p, 0)[0];
+      Entry& e = pool_ptr(kp, p, 0)[0];
       e.u[0] = 0;  // root has no groups: its only child is [0]
       e.du = 1;
       e.kind = KIND_FULL;
-      e.ran = 0;
-      e.ran_now = 0;
+      e.cver = -1;
       e.finished = 0;
       e.capped = 0;
       e.has_best = 0;
       e.a_star = -1;
+      list_arr(kp, p, 0, 0)[0] = 0;   // id
+      list_arr(kp, p, 0, 1)[0] = -1;  // needs a run
+      list_arr(kp, p, 0, 2)[0] = 1;
       S.len = 1;
       RunQueue* q = kp.queues + 0;
       const int slot = atomicAdd(&q->len, 1);
       kp.items[slot].problem = p;
-      kp.items[slot].index = 0;
+      kp.items[slot].pos = 0;
+      kp.items[slot].id = 0;
+      kp.items[slot].front = 1;
       kp.items[slot].cap = kp.seg_cap;
     }
   }
@@ -1115,8 +1220,15 @@ __global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
   int* smem_tmp = reinterpret_cast<int*>(smem_raw + sizeof(WarpSmem) * WARPS_PER_BLOCK);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    kp.deadline_ns += now;  // relative budget -> absolute
+    *kp.deadline_slot = kp.deadline_ns;
+  }
   for (int p = blockIdx.x; p < kp.n_problems; p += gridDim.x) init_problem(kp, p);
   gsync(grid);
+  kp.deadline_ns = *((volatile unsigned long long*)kp.deadline_slot);
 
   int cur = 0;
   for (int wave = 0; wave < kp.max_waves; ++wave) {
@@ -1128,30 +1240,51 @@ __global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
     RunQueue* q = kp.queues + cur;
     RunItem* items = kp.items + (size_t)cur * kp.qcap;
     const int qlen = min(*((volatile int*)&q->len), kp.qcap);
+    if (kp.trace && blockIdx.x == 0 && threadIdx.x == 0)
+      printf("[hpk] wave %d run phase: %d items (active %d)\n", wave, qlen, *((volatile int*)kp.active));
     while (true) {
       int it = 0;
       if (lane == 0) it = atomicAdd(&q->head, 1);
       it = shfl(it, 0);
       if (it >= qlen) break;
       const RunItem item = items[it];
-      const GProb& P = kp.probs[item.problem];
-      GState& S = kp.states[item.problem];
-      Entry* L = list_ptr(kp, item.problem, S.cur);
-      Entry* E = L + item.index;
+      const int p = item.problem;
+      const GProb& P = kp.probs[p];
+      GState& S = kp.states[p];
+      Entry* E = pool_ptr(kp, p, S.pool_cur) + item.id;
       const double C = S.C;
-      RunOut o = run_segment(P, E, E, C, item.cap, wsm + warp, lane, kp.err);
+      const int cver = S.cver;
+      RunOut o = run_segment(P, E, E, C, item.cap, wsm + warp, lane, kp.err, kp.deadline_ns);
+      int* pcv = list_arr(kp, p, S.cur, 1);
+      int* cnt = list_arr(kp, p, S.cur, 2);
+      int* pfirst = list_arr(kp, p, S.cur, 3);
+      int pieces = 0, first = 0;
+      bool keep = true;
+      if (!o.finished && !E->capped) {
+        pieces = split_run(kp, p, S, E, o, wsm + warp, lane, item.front != 0, &first);
+        keep = pieces > 0;  // pool full: drop the run, it re-runs later
+      }
       if (lane == 0) {
-        E->cutoff_used = C;
-        E->ran = 1;
-        E->ran_now = 1;
         E->visits = o.visits;
-        E->finished = o.finished ? 1 : 0;
-        E->dstop = (uint8_t)o.dstop;
+        E->finished = 1;
         E->has_best = o.has_best ? 1 : 0;
         E->best_obj = o.best_obj;
         E->best_G = o.best_G;
         E->m = o.m;
         E->a_star = o.a_star;
+        if (E->capped) {
+          E->cver = cver;  // budget re-run: consumed directly by the scheduler
+        } else if (keep) {
+          E->cver = cver;
+          pcv[item.pos] = cver;
+          cnt[item.pos] = 1 + pieces;
+          pfirst[item.pos] = first;
+        } else {
+          E->cver = -1;
+          E->finished = 0;
+          pcv[item.pos] = -1;
+          cnt[item.pos] = 1;
+        }
         atomicAdd((unsigned long long*)&S.runs, 1ull);
         atomicAdd((unsigned long long*)&S.run_visits, (unsigned long long)o.visits);
       }
@@ -1161,6 +1294,14 @@ __global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
     // ---- schedule phase
     for (int p = blockIdx.x; p < kp.n_problems; p += gridDim.x)
       schedule_problem(kp, p, cur ^ 1, smem_tmp);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      unsigned long long now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (now > kp.deadline_ns) {  // wall-clock watchdog: stop every block
+        atomicOr(kp.err, 2);
+        atomicExch(kp.active, -1000000);
+      }
+    }
     gsync(grid);
     if (*((volatile int*)kp.active) <= 0) break;
     cur ^= 1;
@@ -1386,10 +1527,12 @@ struct DeviceCtx {
   int device = -1;
   int sms = 0;
   int blocks_per_sm = 0;
-  size_t cap_probs = 0, cap_lists = 0, cap_items = 0;
+  size_t cap_probs = 0, cap_pools = 0, cap_lists = 0, cap_items = 0, cap_states = 0,
+         cap_scratch = 0;
   GProb* probs = nullptr;
   GState* states = nullptr;
-  Entry* lists = nullptr;
+  Entry* pools = nullptr;
+  int* lists = nullptr;
   int* scratch = nullptr;
   RunQueue* queues = nullptr;
   RunItem* items = nullptr;
@@ -1434,7 +1577,7 @@ int ensure_ctx(DeviceCtx& c, int device) {
   HPK_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
   HPK_CUDA(cudaEventCreate(&c.ev0));
   HPK_CUDA(cudaEventCreate(&c.ev1));
-  HPK_CUDA(cudaMalloc(&c.active, sizeof(int) * 2));
+  HPK_CUDA(cudaMalloc(&c.active, sizeof(int) * 4));
   HPK_CUDA(cudaMalloc(&c.queues, sizeof(RunQueue) * 2));
   c.device = device;
   return 0;
@@ -1527,6 +1670,7 @@ void hpk_search_config_init(hpk_search_config* cfg) {
   cfg->max_list = 0;
   cfg->force_serial = 0;
   cfg->max_waves = 0;
+  cfg->max_seconds = 0;
 }
 
 void hpk_last_timing(hpk_timing* out) {
@@ -1580,10 +1724,20 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
   if (!wave_ix.empty()) {
     const int P = (int)wave_ix.size();
     const long long seg_cap = cfg.segment_cap > 0 ? cfg.segment_cap : 2048;
-    int lcap = cfg.max_list > 0 ? cfg.max_list : 8192;
-    // keep the list buffers within ~2 GB for large batches
-    const size_t per = sizeof(Entry) * 2;
-    while (lcap > 256 && (size_t)P * lcap * per > (size_t)2 << 30) lcap /= 2;
+    // list capacity (ids) and entry-pool capacity per problem; large by default
+    // (the list must hold the whole speculative frontier), scaled down so that
+    // big batches (cfg5 sweeps) stay within ~4 GB of HBM.
+    int lcap = cfg.max_list > 0 ? cfg.max_list : (1 << 16);
+    int pcap = 2 * lcap;
+    while (lcap > 4096 &&
+           (size_t)P * ((size_t)pcap * 2 * sizeof(Entry) + (size_t)lcap * 36) > ((size_t)4 << 30)) {
+      lcap /= 2;
+      pcap /= 2;
+    }
+    int max_n = 1;
+    for (int k = 0; k < P; ++k) max_n = std::max(max_n, problems[wave_ix[k]].n);
+    const int reserve = max_n * (max_n + 1) / 2 + 32;  // pieces of one split, worst case
+    if (pcap < 4 * reserve) pcap = 4 * reserve;
     std::vector<GProb> hp(P);
     for (int k = 0; k < P; ++k) {
       const hpk_grouping_problem& pr = problems[wave_ix[k]];
@@ -1601,21 +1755,15 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
         g.nkey[i] = pr.node_key[i];
       }
     }
-    size_t cap_entries = c.cap_lists;
     if (int rc = grow(c.probs, c.cap_probs, (size_t)P)) return rc;
-    if (int rc = grow(c.lists, cap_entries, (size_t)P * 2 * lcap)) return rc;
-    c.cap_lists = cap_entries;
-    // states / scratch sized with probs
-    if (c.states) cudaFree(c.states);
-    if (c.scratch) cudaFree(c.scratch);
-    c.states = nullptr;
-    c.scratch = nullptr;
-    HPK_CUDA(cudaMalloc(&c.states, sizeof(GState) * P));
-    HPK_CUDA(cudaMalloc(&c.scratch, sizeof(int) * (size_t)P * (lcap + 1)));
+    if (int rc = grow(c.states, c.cap_states, (size_t)P)) return rc;
+    if (int rc = grow(c.pools, c.cap_pools, (size_t)P * 2 * pcap)) return rc;
+    if (int rc = grow(c.lists, c.cap_lists, (size_t)P * 2 * 4 * lcap)) return rc;
+    if (int rc = grow(c.scratch, c.cap_scratch, (size_t)P * (lcap + 1))) return rc;
     const int grid = c.sms * c.blocks_per_sm;
     const int nwarps = grid * WARPS_PER_BLOCK;
-    const int qmax = std::max(1, (2 * nwarps) / P);
-    const int qcap = P * qmax + P + 64;
+    const int qmax = 2 * nwarps;  // total run slots per wave, shared by active problems
+    const int qcap = qmax + 33 * P + 64;
     if (int rc = grow(c.items, c.cap_items, (size_t)2 * qcap)) return rc;
 
     HPK_CUDA(cudaMemcpyAsync(c.probs, hp.data(), sizeof(GProb) * P, cudaMemcpyHostToDevice,
@@ -1629,6 +1777,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     KParams kp;
     kp.probs = c.probs;
     kp.states = c.states;
+    kp.pools = c.pools;
     kp.lists = c.lists;
     kp.scratch = c.scratch;
     kp.queues = c.queues;
@@ -1637,10 +1786,15 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     kp.err = c.active + 1;
     kp.n_problems = P;
     kp.lcap = lcap;
+    kp.pcap = pcap;
+    kp.reserve = reserve;
     kp.qcap = qcap;
     kp.qmax = qmax;
     kp.seg_cap = seg_cap;
-    kp.max_waves = cfg.max_waves > 0 ? cfg.max_waves : 200000;  // watchdog
+    kp.max_waves = cfg.max_waves > 0 ? cfg.max_waves : 1000000;  // watchdog
+    kp.deadline_ns = (unsigned long long)(cfg.max_seconds > 0 ? cfg.max_seconds : 120.0) * 1000000000ull;
+    kp.deadline_slot = reinterpret_cast<unsigned long long*>(c.active + 2);
+    kp.trace = getenv("HPK_TRACE") ? atoi(getenv("HPK_TRACE")) : 0;
     const size_t smem = sizeof(WarpSmem) * WARPS_PER_BLOCK + sizeof(int) * (BLOCK_THREADS + 8);
     void* args[] = {&kp};
     HPK_CUDA(cudaEventRecord(c.ev0, c.stream));
@@ -1655,7 +1809,8 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     HPK_CUDA(cudaMemcpyAsync(flags_out, c.active, sizeof(int) * 2, cudaMemcpyDeviceToHost,
                              c.stream));
     HPK_CUDA(cudaStreamSynchronize(c.stream));
-    if (flags_out[1]) return fail(5, "hetplan_b200: wave engine watchdog tripped");
+    if (flags_out[1] & 1) return fail(5, "hetplan_b200: segment runner watchdog tripped");
+    if (flags_out[1] & 2) return fail(5, "hetplan_b200: wave engine exceeded its time budget");
     t_timing.d2h_bytes += sizeof(GState) * P;
     float ms = 0;
     HPK_CUDA(cudaEventElapsedTime(&ms, c.ev0, c.ev1));

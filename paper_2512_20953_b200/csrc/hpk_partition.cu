@@ -594,3 +594,72 @@ extern "C" int hpk_partition_cost(const hpk_plan_candidate* cands, int n_cands,
   cudaFree(d_outs);
   return 0;
 }
+
+// ----------------------------------------------------------------------------
+// Issue-rate microbenchmarks: the roofline denominators for this path
+// (MEASURED_PEAKS.json has no FP64 / INT32 entries).
+// Each thread runs 8 independent dependency chains so the pipe, not latency,
+// bounds the rate. Ops counted: one per DADD/DMUL (fp64) or IADD3/LOP3 (int).
+namespace hpkp {
+__global__ void fp64_issue_kernel(double* out, int iters, double a, double b) {
+  double x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3;
+  double x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+  for (int i = 0; i < iters; ++i) {
+    x0 = x0 * a + b; x1 = x1 * a + b; x2 = x2 * a + b; x3 = x3 * a + b;
+    x4 = x4 * a + b; x5 = x5 * a + b; x6 = x6 * a + b; x7 = x7 * a + b;
+  }
+  const double s = ((x0 + x1) + (x2 + x3)) + ((x4 + x5) + (x6 + x7));
+  if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+__global__ void int_issue_kernel(int* out, int iters, int a, int b) {
+  int x0 = threadIdx.x, x1 = x0 ^ 1, x2 = x0 ^ 2, x3 = x0 ^ 3;
+  int x4 = x0 ^ 4, x5 = x0 ^ 5, x6 = x0 ^ 6, x7 = x0 ^ 7;
+  for (int i = 0; i < iters; ++i) {
+    x0 = (x0 + a) ^ b; x1 = (x1 + a) ^ b; x2 = (x2 + a) ^ b; x3 = (x3 + a) ^ b;
+    x4 = (x4 + a) ^ b; x5 = (x5 + a) ^ b; x6 = (x6 + a) ^ b; x7 = (x7 + a) ^ b;
+  }
+  const int s = ((x0 + x1) + (x2 + x3)) + ((x4 + x5) + (x6 + x7));
+  if (s == 0x7f3a91) out[0] = s;
+}
+}  // namespace hpkp
+
+// Measures fp64 (DMUL+DADD, -fmad=false so not fused) and int32 (IADD+LOP)
+// issue rates in ops/s on `device`. Returns 0 on success.
+extern "C" int hpk_measure_issue_peaks(int device, double* fp64_ops_per_s,
+                                       double* int_ops_per_s) {
+  HPKP_CUDA(cudaSetDevice(device < 0 ? 0 : device));
+  cudaDeviceProp prop;
+  HPKP_CUDA(cudaGetDeviceProperties(&prop, device < 0 ? 0 : device));
+  const int blocks = prop.multiProcessorCount * 8, threads = 256, iters = 4096;
+  double* dd;
+  int* di;
+  HPKP_CUDA(cudaMalloc(&dd, sizeof(double)));
+  HPKP_CUDA(cudaMalloc(&di, sizeof(int)));
+  cudaEvent_t e0, e1;
+  HPKP_CUDA(cudaEventCreate(&e0));
+  HPKP_CUDA(cudaEventCreate(&e1));
+  float best_f = 1e30f, best_i = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    float ms = 0;
+    HPKP_CUDA(cudaEventRecord(e0));
+    hpkp::fp64_issue_kernel<<<blocks, threads>>>(dd, iters, 0.999999, 1e-9);
+    HPKP_CUDA(cudaEventRecord(e1));
+    HPKP_CUDA(cudaEventSynchronize(e1));
+    HPKP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    if (rep > 0) best_f = ms < best_f ? ms : best_f;
+    HPKP_CUDA(cudaEventRecord(e0));
+    hpkp::int_issue_kernel<<<blocks, threads>>>(di, iters, 0x1234567, 0x0f0f0f0f);
+    HPKP_CUDA(cudaEventRecord(e1));
+    HPKP_CUDA(cudaEventSynchronize(e1));
+    HPKP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    if (rep > 0) best_i = ms < best_i ? ms : best_i;
+  }
+  const double ops = (double)blocks * threads * iters * 8 * 2;  // 2 ops per chain step
+  *fp64_ops_per_s = ops / (best_f * 1e-3);
+  *int_ops_per_s = ops / (best_i * 1e-3);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(dd);
+  cudaFree(di);
+  return 0;
+}

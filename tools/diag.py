@@ -1,0 +1,19 @@
+import sys, os, time
+sys.path.insert(0, '/root/repo')
+from oracle.binding import Oracle, min_mem_for, units_for
+from paper_2512_20953_b200 import configs
+from paper_2512_20953_b200.engine import Engine, GroupingProblem
+eng = Engine(); orc = Oracle()
+name = sys.argv[1]; tp = int(sys.argv[2]); cap = int(sys.argv[3]); maxw = int(sys.argv[4])
+w = configs.get(name)
+P, M, T, N = units_for(w.cluster, tp)
+pb = GroupingProblem(P, M, w.model["n_microbatches"], min_mem_for(w.model), T, N)
+t = time.time()
+try:
+    r = eng.grouping_search([pb], segment_cap=cap, max_waves=maxw, max_seconds=15)[0]
+    print("RESULT", r.visited, r.objective, r.optimal, r.waves, r.segment_runs, r.segment_visits, r.max_list, flush=True)
+except Exception as e:
+    print("ERR", e, flush=True)
+print("time %.2f s kernel %.2f ms" % (time.time() - t, eng.timing().search_ms), flush=True)
+o = orc.solve_grouping(pb.power, pb.memory, pb.n_microbatches, pb.min_mem, pb.type_key, pb.node_key)
+print("ORACLE", o.visited, o.objective, o.optimal, flush=True)

@@ -30,7 +30,7 @@ def main():
             o = orc.solve_grouping(pb.power, pb.memory, 8, 5.0, pb.type_key, pb.node_key)
             log("small serial=%d" % fs, r.status, r.rgs, r.objective, r.visited, r.optimal,
                 "| oracle", o.rgs, o.objective, o.visited, o.optimal)
-    if "random" in which:
+    if "random" in which or any(a.startswith("cap:") for a in which):
         rng = random.Random(7)
         probs = []
         for trial in range(int(os.environ.get("NRAND", "300"))):
@@ -46,13 +46,14 @@ def main():
             thr = rng.choice([0, 8, 100])
             B = rng.randint(1, 3000)
             probs.append(GroupingProblem(P, M, K, MIN, T, N, thr, B))
-        for cap in (2, 5, 64, 2048):
+        caps = [int(a.split(":")[1]) for a in which if a.startswith("cap:")] or [2, 5, 64, 2048]
+        for cap in caps:
             t = time.time()
             if cap < 16:  # tiny caps only on small trees (progress is ~1 split per wave)
                 sub = [p for p in probs if p.n <= 8 or p.exact_threshold < p.n and p.node_budget <= 300]
             else:
                 sub = probs
-            res = eng.grouping_search(sub, segment_cap=cap)
+            res = eng.grouping_search(sub, segment_cap=cap, max_seconds=60)
             probs_run = sub
             bad = 0
             for pb, r in zip(probs_run, res):
@@ -71,7 +72,9 @@ def main():
                             o.visited, o.optimal)
             log("random cap=%d: %d problems, %d mismatches, %.2fs" % (cap, len(probs_run), bad,
                                                                      time.time() - t))
-        res = eng.grouping_search(probs, force_serial=True)
+        if "serial" not in which:
+            probs = []
+        res = eng.grouping_search(probs, force_serial=True) if probs else []
         bad = 0
         for pb, r in zip(probs, res):
             o = orc.solve_grouping(pb.power, pb.memory, pb.n_microbatches, pb.min_mem,
