@@ -73,7 +73,7 @@ struct __align__(16) Entry {
   int a_star;              // PREFIX re-run: depth of the pruned ancestor of `end`
   int cver;                // cutoff version of the last run (-1: never ran)
   uint8_t du, dend, kind, finished;
-  uint8_t has_best, capped, pad[2];
+  uint8_t has_best, capped, uncapped, pad;
 };
 
 struct GState {
@@ -110,6 +110,7 @@ struct KParams {
   GState* states;
   Entry* pools;       // [P][2][pcap]
   int* lists;         // [P][2][4][lcap]: ids, pcver, cnt, pfirst
+  long long* lvis;    // [P][2][lcap]: visits of the finished run at each position
   int* scratch;       // [P][lcap + 1]
   RunQueue* queues;   // [2]
   RunItem* items;     // [2][qcap]
@@ -131,6 +132,9 @@ __device__ __forceinline__ Entry* pool_ptr(const KParams& kp, int p, int which) 
 // run at this position, -1 = needs a run), 2 cnt (expansion count), 3 pfirst
 __device__ __forceinline__ int* list_arr(const KParams& kp, int p, int buf, int which) {
   return kp.lists + (((size_t)p * 2 + buf) * 4 + which) * kp.lcap;
+}
+__device__ __forceinline__ long long* list_vis(const KParams& kp, int p, int buf) {
+  return kp.lvis + ((size_t)p * 2 + buf) * kp.lcap;
 }
 
 // --------------------------------------------------------------- warp DFS
@@ -646,10 +650,22 @@ __device__ int split_run(const KParams& kp, int p, GState& S, Entry* E, const Ru
   int count = 1 + ((int)sm->Gat[d] - o.stop_c);
   for (int lev = d - 1; lev >= du; --lev) count += (int)sm->Gat[lev] - (int)sm->path[lev];
   int first = 0;
-  if (lane == 0) {
+  if (lane == 0) {  // CAS bump allocation: a failed attempt leaves no hole, and the
+    // list head alone may use the last `reserve` slots (progress guarantee)
     const int limit = kp.pcap - (front ? 0 : kp.reserve);
-    first = atomicAdd(&S.pool_top, count);
-    if (first + count > limit) first = -1;
+    int old = *((volatile int*)&S.pool_top);
+    while (true) {
+      if (old + count > limit) {
+        first = -1;
+        break;
+      }
+      const int prev = atomicCAS(&S.pool_top, old, old + count);
+      if (prev == old) {
+        first = old;
+        break;
+      }
+      old = prev;
+    }
   }
   first = shfl(first, 0);
   if (first < 0) return 0;
@@ -680,6 +696,7 @@ __device__ int split_run(const KParams& kp, int p, GState& S, Entry* E, const Ru
     q.cver = -1;
     q.finished = 0;
     q.capped = 0;
+    q.uncapped = 0;
     q.has_best = 0;
     q.a_star = -1;
   }
@@ -737,15 +754,31 @@ __device__ void finish_problem(const KParams& kp, GState& S) {
   atomicSub(kp.active, 1);
 }
 
-// Queue the first qmax positions (list order) that need a run at cutoff version cver.
+// Queue the first qmax positions (list order) that need a run at cutoff
+// version cver, but never a position that is provably past the budget's abort
+// point: the visits of the exact runs before it (others count 1, a lower
+// bound — a higher cutoff only prunes more) already exhaust the budget.
 __device__ void push_items(const KParams& kp, int queue, int p, const int* ids, const int* pcv,
-                           int head, int len, int cver, int qmax, int lane) {
+                           const long long* pvis, const Entry* pool, int head, int len, int cver,
+                           int qmax, long long budget_left, int lane) {
   RunQueue* q = kp.queues + queue;
   RunItem* items = kp.items + (size_t)queue * kp.qcap;
   int pushed = 0;
+  long long before = 0;  // lower bound of visits before the chunk
   for (int base = 0; base < len && pushed < qmax; base += 32) {
     const int i = base + lane;
-    const bool need = i < len && pcv[head + i] != cver;
+    const bool inl = i < len;
+    const bool exact = inl && pcv[head + i] == cver;
+    long long v = inl ? (exact ? pvis[head + i] : 1) : 0;
+    long long inc = v;  // inclusive scan
+#pragma unroll
+    for (int o2 = 1; o2 < 32; o2 <<= 1) {
+      const long long t = __shfl_up_sync(HPK_FULL_MASK, inc, o2);
+      if (lane >= o2) inc += t;
+    }
+    const long long excl = before + inc - v;
+    const bool within = budget_left < 0 || excl < budget_left;
+    const bool need = inl && !exact && within;
     const unsigned bal = __ballot_sync(HPK_FULL_MASK, need);
     int cnt = __popc(bal);
     if (pushed + cnt > qmax) cnt = qmax - pushed;
@@ -755,13 +788,16 @@ __device__ void push_items(const KParams& kp, int queue, int p, const int* ids, 
     const int rank = __popc(bal & ((1u << lane) - 1));
     if (need && rank < cnt && slot0 + rank < kp.qcap) {
       RunItem& it = items[slot0 + rank];
+      const int id = ids[head + i];
       it.problem = p;
       it.pos = head + i;
-      it.id = ids[head + i];
+      it.id = id;
       it.front = (i == 0);
-      it.cap = kp.seg_cap;
+      it.cap = pool[id].uncapped ? 0x3fffffffffffffffLL : kp.seg_cap;
     }
     pushed += cnt;
+    before += shfl(inc, 31);
+    if (budget_left >= 0 && before >= budget_left) break;
   }
 }
 
@@ -780,6 +816,8 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
   int* ids_out = list_arr(kp, p, cur ^ 1, 0);
   int* pcv_out = list_arr(kp, p, cur ^ 1, 1);
   int* cnt_out = list_arr(kp, p, cur ^ 1, 2);
+  long long* vis_in = list_vis(kp, p, cur);
+  long long* vis_out = list_vis(kp, p, cur ^ 1);
   Entry* pool = pool_ptr(kp, p, S.pool_cur);
 
   if (S.rerun_pending) {
@@ -807,23 +845,27 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
   for (int i = tid; i < len; i += blockDim.x) off[i] = cnt_in[head + i];
   __syncthreads();
   int total = block_scan_excl(off, len, smem_tmp);
-  if (total > kp.lcap) {
-    // Not enough list room: keep expansions in list order while they fit; the
-    // others are reverted to unrun FULL segments (their pieces become garbage).
+  if (total > kp.lcap - kp.reserve) {
+    // List nearly full: keep expansions in list order while they leave the
+    // head's reserve free; the others are reverted to unrun FULL segments
+    // (their pieces become garbage). If even the head cannot expand it re-runs
+    // uncapped (finishes in one run) — progress is guaranteed.
     if (tid == 0) {
-      int budget = kp.lcap - len;
+      int used = len;
       for (int i = 0; i < len; ++i) {
         const int c = (i + 1 < len ? off[i + 1] : total) - off[i];
         off[i] = c;
         if (c > 1) {
-          if (c - 1 <= budget) {
-            budget -= c - 1;
+          const int limit = i == 0 ? kp.lcap : kp.lcap - kp.reserve;
+          if (used + c - 1 <= limit) {
+            used += c - 1;
           } else {
             off[i] = 1;
             Entry& e = pool[ids_in[head + i]];
             e.kind = KIND_FULL;
             e.cver = -1;
             e.finished = 0;
+            if (i == 0) e.uncapped = 1;
             pcv_in[head + i] = -1;
           }
         }
@@ -845,9 +887,11 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
     if (k == 0) {
       ids_out[o] = ids_in[head + lo];
       pcv_out[o] = pcv_in[head + lo];
+      vis_out[o] = vis_in[head + lo];
     } else {
       ids_out[o] = pf_in[head + lo] + k - 1;
       pcv_out[o] = -1;
+      vis_out[o] = 0;
     }
     cnt_out[o] = 1;
   }
@@ -1014,14 +1058,17 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
   if ((flag & 1) && S.pool_top > kp.pcap - 2 * kp.reserve - 64 * 32) {
     Entry* np = pool_ptr(kp, p, S.pool_cur ^ 1);
     int* pcv_tmp = list_arr(kp, p, cur, 1);  // the input buffer is free now
+    long long* vis_tmp = vis_in;
     for (int k = tid; k < nlen; k += blockDim.x) {
       np[k] = pool[ids_out[nhead + k]];
       pcv_tmp[k] = pcv_out[nhead + k];
+      vis_tmp[k] = vis_out[nhead + k];
     }
     __syncthreads();
     for (int k = tid; k < nlen; k += blockDim.x) {
       ids_out[k] = k;
       pcv_out[k] = pcv_tmp[k];
+      vis_out[k] = vis_tmp[k];
       cnt_out[k] = 1;
     }
     __syncthreads();
@@ -1051,7 +1098,9 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
     } else if (flag & 1) {
       const int act = max(1, *((volatile int*)kp.active));
       const int qmax = max(32, kp.qmax / act);
-      push_items(kp, next_queue, p, ids_out, pcv_out, nhead, nlen, S.cver, qmax, lane);
+      const long long bl = P.budget < 0 ? -1 : P.budget - S.V;
+      push_items(kp, next_queue, p, ids_out, pcv_out, vis_out,
+                 pool_ptr(kp, p, S.pool_cur), nhead, nlen, S.cver, qmax, bl, lane);
     }
   }
   __syncthreads();
@@ -1184,8 +1233,10 @@ __device__ void init_problem(const KParams& kp, int p) {
       e.cver = -1;
       e.finished = 0;
       e.capped = 0;
+      e.uncapped = 0;
       e.has_best = 0;
       e.a_star = -1;
+      list_vis(kp, p, 0)[0] = 0;
       list_arr(kp, p, 0, 0)[0] = 0;   // id
       list_arr(kp, p, 0, 1)[0] = -1;  // needs a run
       list_arr(kp, p, 0, 2)[0] = 1;
@@ -1276,9 +1327,11 @@ __global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
           E->cver = cver;  // budget re-run: consumed directly by the scheduler
         } else if (keep) {
           E->cver = cver;
+          E->uncapped = 0;
           pcv[item.pos] = cver;
           cnt[item.pos] = 1 + pieces;
           pfirst[item.pos] = first;
+          list_vis(kp, p, S.cur)[item.pos] = o.visits;
         } else {
           E->cver = -1;
           E->finished = 0;
@@ -1533,6 +1586,8 @@ struct DeviceCtx {
   GState* states = nullptr;
   Entry* pools = nullptr;
   int* lists = nullptr;
+  long long* lvis = nullptr;
+  size_t cap_lvis = 0;
   int* scratch = nullptr;
   RunQueue* queues = nullptr;
   RunItem* items = nullptr;
@@ -1730,7 +1785,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     int lcap = cfg.max_list > 0 ? cfg.max_list : (1 << 16);
     int pcap = 2 * lcap;
     while (lcap > 4096 &&
-           (size_t)P * ((size_t)pcap * 2 * sizeof(Entry) + (size_t)lcap * 36) > ((size_t)4 << 30)) {
+           (size_t)P * ((size_t)pcap * 2 * sizeof(Entry) + (size_t)lcap * 52) > ((size_t)4 << 30)) {
       lcap /= 2;
       pcap /= 2;
     }
@@ -1760,6 +1815,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     if (int rc = grow(c.pools, c.cap_pools, (size_t)P * 2 * pcap)) return rc;
     if (int rc = grow(c.lists, c.cap_lists, (size_t)P * 2 * 4 * lcap)) return rc;
     if (int rc = grow(c.scratch, c.cap_scratch, (size_t)P * (lcap + 1))) return rc;
+    if (int rc = grow(c.lvis, c.cap_lvis, (size_t)P * 2 * lcap)) return rc;
     const int grid = c.sms * c.blocks_per_sm;
     const int nwarps = grid * WARPS_PER_BLOCK;
     const int qmax = 2 * nwarps;  // total run slots per wave, shared by active problems
@@ -1779,6 +1835,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     kp.states = c.states;
     kp.pools = c.pools;
     kp.lists = c.lists;
+    kp.lvis = c.lvis;
     kp.scratch = c.scratch;
     kp.queues = c.queues;
     kp.items = c.items;

@@ -1,0 +1,109 @@
+"""GPU parity of the grouping search (the hot loop) against the oracle and the
+reference's golden vectors: winner RGS, objective and z bit-exact, visits and
+the optimal flag identical — exhaustive and budget-truncated, both engines."""
+import math
+import random
+
+import pytest
+
+from oracle.binding import min_mem_for, units_for
+from paper_2512_20953_b200 import configs
+from paper_2512_20953_b200.engine import GroupingProblem
+
+pytestmark = pytest.mark.gpu
+
+
+def _same(r, o):
+    if o.status != 0:
+        return r.status == o.status
+    return (r.status == 0 and r.count == o.count and r.rgs == o.rgs
+            and r.objective == o.objective and r.z == o.z and r.visited == o.visited
+            and r.optimal == o.optimal)
+
+
+def _random_problems(seed, count, nmax=11):
+    rng = random.Random(seed)
+    out = []
+    for t in range(count):
+        n = rng.randint(1, nmax)
+        if t % 5 == 0:
+            P = [2.0] * n  # heavy ties
+            M = [8.0] * n
+        else:
+            P = [rng.choice([0.5, 1.0, 1.5, 2.0, 3.0]) for _ in range(n)]
+            M = [float(rng.randint(4, 20)) for _ in range(n)]
+        T = [int(p * 2) for p in P]
+        N = sorted(rng.randint(0, 3) for _ in range(n))
+        K = rng.randint(1, 16)
+        MIN = sum(M) * rng.uniform(0.1, 0.9) / rng.randint(1, 4)
+        if rng.random() < 0.5:
+            MIN = float(round(MIN))
+        thr = rng.choice([0, 4, 8])
+        B = rng.choice([0, 1, 2, 17, 300, 3000, 20000])
+        out.append(GroupingProblem(P, M, K, MIN, T, N, thr, B))
+    return out
+
+
+@pytest.mark.parametrize("cap", [3, 64, 2048])
+def test_wave_engine_random_batch(engine, oracle, cap):
+    probs = _random_problems(cap, 160, nmax=10 if cap < 16 else 11)
+    res = engine.grouping_search(probs, segment_cap=cap, max_seconds=60)
+    bad = []
+    for pb, r in zip(probs, res):
+        o = oracle.solve_grouping(pb.power, pb.memory, pb.n_microbatches, pb.min_mem,
+                                  pb.type_key, pb.node_key, pb.exact_threshold, pb.node_budget)
+        if not _same(r, o):
+            bad.append((pb, r, o.rgs, o.objective, o.visited, o.optimal))
+        assert r.engine == 0
+    assert not bad, bad[:2]
+
+
+def test_serial_engine_random_batch(engine, oracle):
+    probs = _random_problems(99, 120, nmax=10)
+    res = engine.grouping_search(probs, force_serial=True, max_seconds=60)
+    for pb, r in zip(probs, res):
+        o = oracle.solve_grouping(pb.power, pb.memory, pb.n_microbatches, pb.min_mem,
+                                  pb.type_key, pb.node_key, pb.exact_threshold, pb.node_budget)
+        assert r.engine == 1
+        assert _same(r, o), (pb, r)
+
+
+def test_golden_grouping_vectors(engine, golden_grouping):
+    probs = [GroupingProblem(g["power"], g["memory"], g["K"], g["min_mem"], g["type_key"],
+                             g["node_key"], g["exact_threshold"], g["node_budget"], g["top_k"])
+             for g in golden_grouping]
+    res = engine.grouping_search(probs, max_seconds=60)
+    for g, r in zip(golden_grouping, res):
+        assert r.status == g["status"], g
+        if g["status"] != 0:
+            continue
+        assert r.count == g["count"]
+        assert r.rgs == g["rgs"]
+        assert [x.hex() for x in r.objective] == g["objective"]
+        assert [x.hex() for x in r.z] == g["z"]
+        assert r.optimal == g["optimal"] and r.visited == g["visited"]
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4"])
+def test_configs_every_tp_dimension(engine, oracle, name):
+    w = configs.get(name)
+    g = 0
+    for nd in w.cluster["nodes"]:
+        g = math.gcd(g, nd["count"])
+    probs = []
+    for tp in [t for t in range(1, g + 1) if g % t == 0]:
+        P, M, T, N = units_for(w.cluster, tp)
+        probs.append(GroupingProblem(P, M, w.model["n_microbatches"], min_mem_for(w.model), T, N))
+    res = engine.grouping_search(probs, max_seconds=60)
+    for pb, r in zip(probs, res):
+        o = oracle.solve_grouping(pb.power, pb.memory, pb.n_microbatches, pb.min_mem,
+                                  pb.type_key, pb.node_key)
+        assert _same(r, o), (name, pb.n)
+
+
+def test_top_k_and_non_dyadic_take_the_serial_engine(engine, oracle):
+    pb = GroupingProblem([1.0, 1.0, 2.0, 0.7, 1.3], [8.0, 8.0, 8.0, 9.0, 7.0], 8, 6.0,
+                         [0, 0, 1, 2, 3], [0, 0, 1, 2, 3], top_k=3)
+    r = engine.grouping_search([pb])[0]
+    o = oracle.solve_grouping(pb.power, pb.memory, 8, 6.0, pb.type_key, pb.node_key, top_k=3)
+    assert r.engine == 1 and _same(r, o)

@@ -53,7 +53,7 @@ def main():
                 sub = [p for p in probs if p.n <= 8 or p.exact_threshold < p.n and p.node_budget <= 300]
             else:
                 sub = probs
-            res = eng.grouping_search(sub, segment_cap=cap, max_seconds=60)
+            res = eng.grouping_search(sub, segment_cap=cap, max_seconds=30)
             probs_run = sub
             bad = 0
             for pb, r in zip(probs_run, res):
