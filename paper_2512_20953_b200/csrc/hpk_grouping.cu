@@ -58,6 +58,8 @@ struct GProb {
   double f[MAXN + 2];   // f[d] = 1 - (d-1)/(K+d-1): Eq. (2) factor (grouping.cpp:103-108)
   double R[MAXN + 1];   // exact suffix sums of unit powers (contract: exact)
   double RM[MAXN + 1];  // remaining_mem from d, serial as grouping.cpp:156-160
+  double mb_abs;        // absolute error bound of the approximate bound sums
+  double md_abs;        // same for the deficit sums (0 when they are exact integers)
 };
 
 // A segment of the ordered DFS list, stored in a per-problem entry pool; the
@@ -122,6 +124,7 @@ struct KParams {
   int max_waves;
   unsigned long long deadline_ns;  // %globaltimer watchdog (relative at launch)
   unsigned long long* deadline_slot;
+  unsigned int* bar;               // grid barrier {count, generation}
   int trace;                       // HPK_TRACE=1: per-wave scheduler printf (debug)
 };
 
@@ -140,6 +143,8 @@ __device__ __forceinline__ long long* list_vis(const KParams& kp, int p, int buf
 // --------------------------------------------------------------- warp DFS
 
 struct WarpSmem {
+  // the problem's tables, staged per run (all hot-loop loads are LDS)
+  double tp[MAXN], tm[MAXN], tf[MAXN + 2], tR[MAXN + 1], tRM[MAXN + 1];
   double S[MAXN + 1];    // approx sum of Eq.(2) effective powers at each level
   double DEF[MAXN + 1];  // approx memory deficit at each level
   uint8_t path[MAXN];
@@ -149,17 +154,56 @@ struct WarpSmem {
   uint8_t best[MAXN];
 };
 
+// Problem view used by the runner: same member names as GProb, arrays in smem.
+struct PView {
+  const double* p;
+  const double* m;
+  const double* f;
+  const double* R;
+  const double* RM;
+  int n, exact_mem;
+  double min_mem, mb_abs, md_abs;
+};
+
+__device__ __forceinline__ PView stage_problem(const GProb& G, WarpSmem* sm, int lane) {
+  const int n = G.n;
+  for (int i = lane; i < n; i += 32) {
+    sm->tp[i] = G.p[i];
+    sm->tm[i] = G.m[i];
+  }
+  for (int i = lane; i <= n + 1; i += 32) sm->tf[i] = G.f[i];
+  for (int i = lane; i <= n; i += 32) {
+    sm->tR[i] = G.R[i];
+    sm->tRM[i] = G.RM[i];
+  }
+  __syncwarp();
+  PView v;
+  v.p = sm->tp;
+  v.m = sm->tm;
+  v.f = sm->tf;
+  v.R = sm->tR;
+  v.RM = sm->tRM;
+  v.n = n;
+  v.exact_mem = G.exact_mem;
+  v.min_mem = G.min_mem;
+  v.mb_abs = G.mb_abs;
+  v.md_abs = G.md_abs;
+  return v;
+}
+
 enum : int { DEC_PASS = 0, DEC_PRUNE = 1, DEC_EXACT = 2 };
 
 constexpr double kEps52 = 2.220446049250313e-16;  // 2^-52
 
-// Per-lane group registers: lane owns groups lane and lane+32.
+// Per-lane group registers: lane owns groups lane and lane+32; f0/f1 cache the
+// Eq. (2) factors for the current member count and for one more member.
 struct Groups {
-  double gp[2], gm[2];
+  double gp[2], gm[2], f0[2], f1[2];
   int gc[2];
 };
 
-__device__ __forceinline__ void add_unit(Groups& g, int lane, int grp, double up, double um) {
+__device__ __forceinline__ void add_unit(const PView& P, Groups& g, int lane, int grp, double up,
+                                         double um) {
   if ((grp & 31) == lane) {
     const int s = grp >> 5;
 #pragma unroll
@@ -174,12 +218,15 @@ __device__ __forceinline__ void add_unit(Groups& g, int lane, int grp, double up
           g.gm[k] += um;
           g.gc[k] += 1;
         }
+        g.f0[k] = g.f1[k];
+        g.f1[k] = P.f[g.gc[k] + 1];
       }
     }
   }
 }
 
-__device__ __forceinline__ void remove_unit(Groups& g, int lane, int grp, double up, double um) {
+__device__ __forceinline__ void remove_unit(const PView& P, Groups& g, int lane, int grp,
+                                            double up, double um) {
   if ((grp & 31) == lane) {
     const int s = grp >> 5;
 #pragma unroll
@@ -194,16 +241,31 @@ __device__ __forceinline__ void remove_unit(Groups& g, int lane, int grp, double
           g.gm[k] -= um;
           g.gc[k] -= 1;
         }
+        g.f1[k] = g.f0[k];
+        g.f0[k] = P.f[g.gc[k]];
       }
     }
   }
 }
 
-// eff of this lane's slot k (0 if the group does not exist)
-__device__ __forceinline__ double slot_eff(const GProb& P, const Groups& g, int k) {
-  return g.gc[k] > 0 ? g.gp[k] * P.f[g.gc[k]] : 0.0;
+__device__ __forceinline__ void groups_init(const PView& P, Groups& g) {
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    g.gp[k] = 0;
+    g.gm[k] = 0;
+    g.gc[k] = 0;
+    g.f0[k] = P.f[0];
+    g.f1[k] = P.f[1];
+  }
 }
-__device__ __forceinline__ double slot_def(const GProb& P, const Groups& g, int k) {
+
+// eff of this lane's slot k (0 if the group does not exist); f0 = f[gc] is the
+// reference's (1 - rho) for the group (grouping.cpp:103-108)
+__device__ __forceinline__ double slot_eff(const PView& P, const Groups& g, int k) {
+  (void)P;
+  return g.gc[k] > 0 ? g.gp[k] * g.f0[k] : 0.0;
+}
+__device__ __forceinline__ double slot_def(const PView& P, const Groups& g, int k) {
   if (g.gc[k] == 0) return 0.0;
   const double d = P.min_mem - g.gm[k];
   return d > 0.0 ? d : 0.0;  // std::max(0.0, d)
@@ -211,7 +273,7 @@ __device__ __forceinline__ double slot_def(const GProb& P, const Groups& g, int 
 
 // Exact node check in the reference's serial order (grouping.cpp:154-169) for
 // the node whose units 0..next-1 are applied. Warp-uniform result.
-__device__ bool exact_passes(const GProb& P, const Groups& g, int G, int next, double cut) {
+__device__ bool exact_passes(const PView& P, const Groups& g, int G, int next, double cut) {
   double bound = 0;
   for (int gi = 0; gi < G; ++gi) {
     const int k = gi >> 5;
@@ -229,27 +291,22 @@ __device__ bool exact_passes(const GProb& P, const Groups& g, int G, int next, d
   return !(deficit > P.RM[next]);
 }
 
-// Filter decision for a node given approximate sums; margins bound the gap
-// between the approximations and the reference's serial fp64 sums.
-__device__ __forceinline__ int decide(const GProb& P, double A, double Tabs, double D,
-                                      double Dabs, int Gn, int next, double cut) {
+// Filter decision for a node given approximate sums (incrementally maintained
+// along the path). P.mb_abs / P.md_abs bound the gap between the
+// approximations and the reference's serial fp64 sums; only a
+// cutoff inside that margin needs the exact serial evaluation.
+__device__ __forceinline__ int decide(const PView& P, double A, double D, int next, double cut) {
   int db = DEC_PASS;
   if (cut >= 0) {
-    const double mb = (double)(Gn + (P.n - next) + 16) * kEps52 * Tabs;
-    if (A + mb < cut) db = DEC_PRUNE;
-    else if (A - mb >= cut) db = DEC_PASS;
+    if (A + P.mb_abs < cut) db = DEC_PRUNE;
+    else if (A - P.mb_abs >= cut) db = DEC_PASS;
     else db = DEC_EXACT;
   }
   const double rem = P.RM[next];
   int dd;
-  if (P.exact_mem) {
-    dd = D > rem ? DEC_PRUNE : DEC_PASS;
-  } else {
-    const double md = (double)(Gn + 8) * kEps52 * (Dabs + rem);
-    if (D - md > rem) dd = DEC_PRUNE;
-    else if (D + md <= rem) dd = DEC_PASS;
-    else dd = DEC_EXACT;
-  }
+  if (D - P.md_abs > rem) dd = DEC_PRUNE;
+  else if (D + P.md_abs <= rem) dd = DEC_PASS;
+  else dd = DEC_EXACT;
   if (db == DEC_PRUNE || dd == DEC_PRUNE) return DEC_PRUNE;
   if (db == DEC_PASS && dd == DEC_PASS) return DEC_PASS;
   return DEC_EXACT;
@@ -266,7 +323,7 @@ struct RunOut {
 };
 
 // DFS of subtree(E.u) in preorder (PREFIX: stopping before E.end), cap visits.
-__device__ RunOut run_segment(const GProb& P, const Entry* E, Entry* Eout, double C,
+__device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, double C,
                               long long cap, WarpSmem* sm, int lane, int* err,
                               unsigned long long deadline) {
   const int n = P.n;
@@ -292,14 +349,12 @@ __device__ RunOut run_segment(const GProb& P, const Entry* E, Entry* Eout, doubl
   __syncwarp();
 
   Groups g;
-  g.gp[0] = g.gp[1] = 0;
-  g.gm[0] = g.gm[1] = 0;
-  g.gc[0] = g.gc[1] = 0;
+  groups_init(P, g);
   int G = 0;
   if (lane == 0) sm->Gat[0] = 0;
   for (int i = 0; i + 1 < du; ++i) {
     const int grp = sm->path[i];
-    add_unit(g, lane, grp, P.p[i], P.m[i]);
+    add_unit(P, g, lane, grp, P.p[i], P.m[i]);
     if (grp == G) ++G;
     if (lane == 0) sm->Gat[i + 1] = (uint8_t)G;
   }
@@ -324,7 +379,7 @@ __device__ RunOut run_segment(const GProb& P, const Entry* E, Entry* Eout, doubl
   {
     const int i = du - 1;
     const int grp = sm->path[i];
-    add_unit(g, lane, grp, P.p[i], P.m[i]);
+    add_unit(P, g, lane, grp, P.p[i], P.m[i]);
     if (grp == G) ++G;
     if (lane == 0) sm->Gat[du] = (uint8_t)G;
     __syncwarp();
@@ -361,7 +416,7 @@ __device__ RunOut run_segment(const GProb& P, const Entry* E, Entry* Eout, doubl
     const double S = warp_sum_approx(le);
     const double DEF = warp_sum_approx(ld);
     const double A = S + P.R[d];
-    int dec = decide(P, A, A, DEF, DEF, G, d, cut);
+    int dec = decide(P, A, DEF, d, cut);
     if (dec == DEC_EXACT) dec = exact_passes(P, g, G, d, cut) ? DEC_PASS : DEC_PRUNE;
     if (dec == DEC_PRUNE) {
       if (prefix) o.a_star = du;
@@ -458,7 +513,7 @@ __device__ RunOut run_segment(const GProb& P, const Entry* E, Entry* Eout, doubl
             double eff_new, mem_new, other_min;
             int others_inf, Gc;
             if (c < G) {
-              eff_new = (g.gp[k] + up) * P.f[g.gc[k] + 1];
+              eff_new = (g.gp[k] + up) * g.f1[k];
               mem_new = g.gm[k] + um;
               others_inf = n_inf - (inf_k[k] ? 1 : 0);
               other_min = (c == i1) ? m2 : m1;
@@ -530,7 +585,7 @@ __device__ RunOut run_segment(const GProb& P, const Entry* E, Entry* Eout, doubl
         break;
       }
       const int grp = sm->path[d - 1];
-      remove_unit(g, lane, grp, P.p[d - 1], P.m[d - 1]);
+      remove_unit(P, g, lane, grp, P.p[d - 1], P.m[d - 1]);
       G = sm->Gat[d - 1];
       --d;
       if (match > d) match = d;
@@ -553,47 +608,48 @@ __device__ RunOut run_segment(const GProb& P, const Entry* E, Entry* Eout, doubl
     if (lane == 0) sm->nxt[d] = (uint8_t)(c + 1);
     __syncwarp();  // every lane re-reads nxt[d] at the next iteration
     // ---- check child c (internal node at depth d+1) on its owner lane ----
+    // The child's level sums follow from the parent's in O(1):
+    //   S' = S - eff(c) + eff'(c),  DEF' = DEF - def(c) + def'(c)
     int dec;
+    double Sn, Dn;
     {
       const int owner = c & 31, k = c >> 5;
       int ldec = 0;
+      double lS = 0, lD = 0;
       if (lane == owner) {
         const double up = P.p[d], um = P.m[d];
         double eff_old, eff_new, def_old, def_new;
-        int Gc;
         const int gck = k == 0 ? g.gc[0] : g.gc[1];
         const double gpk = k == 0 ? g.gp[0] : g.gp[1];
         const double gmk = k == 0 ? g.gm[0] : g.gm[1];
         if (c < G) {
-          eff_old = gpk * P.f[gck];
-          eff_new = (gpk + up) * P.f[gck + 1];
+          eff_old = gpk * (k == 0 ? g.f0[0] : g.f0[1]);
+          eff_new = (gpk + up) * (k == 0 ? g.f1[0] : g.f1[1]);
           const double d0 = P.min_mem - gmk;
           def_old = d0 > 0.0 ? d0 : 0.0;
           const double d1 = P.min_mem - (gmk + um);
           def_new = d1 > 0.0 ? d1 : 0.0;
-          Gc = G;
         } else {
           eff_old = 0;
           eff_new = up * P.f[1];
           def_old = 0;
           const double d1 = P.min_mem - um;
           def_new = d1 > 0.0 ? d1 : 0.0;
-          Gc = G + 1;
         }
-        const double Sd = sm->S[d], Dd = sm->DEF[d];
-        const double R = P.R[d + 1];
-        const double A = ((Sd - eff_old) + eff_new) + R;
-        const double Tabs = Sd + eff_new + R;
-        const double Dn = (Dd - def_old) + def_new;
-        ldec = decide(P, A, Tabs, Dn, Dd + def_new, Gc, d + 1, cut);
+        (void)gck;
+        lS = (sm->S[d] - eff_old) + eff_new;
+        lD = (sm->DEF[d] - def_old) + def_new;
+        ldec = decide(P, lS + P.R[d + 1], lD, d + 1, cut);
       }
       dec = shfl(ldec, owner);
+      Sn = shfl(lS, owner);
+      Dn = shfl(lD, owner);
     }
     if (dec == DEC_EXACT) {
-      add_unit(g, lane, c, P.p[d], P.m[d]);
+      add_unit(P, g, lane, c, P.p[d], P.m[d]);
       const int Gc = c == G ? G + 1 : G;
       dec = exact_passes(P, g, Gc, d + 1, cut) ? DEC_PASS : DEC_PRUNE;
-      remove_unit(g, lane, c, P.p[d], P.m[d]);
+      remove_unit(P, g, lane, c, P.p[d], P.m[d]);
     }
     if (dec == DEC_PRUNE) {
       if (prefix && match == d && c == sm->endp[d] && o.a_star < 0) o.a_star = d + 1;
@@ -602,23 +658,17 @@ __device__ RunOut run_segment(const GProb& P, const Entry* E, Entry* Eout, doubl
     // ---- descend into child c ----
     if (lane == 0) sm->path[d] = (uint8_t)c;
     __syncwarp();
-    add_unit(g, lane, c, P.p[d], P.m[d]);
+    add_unit(P, g, lane, c, P.p[d], P.m[d]);
     if (c == G) ++G;
     if (prefix && match == d && c == sm->endp[d]) match = d + 1;
     ++d;
-    {
-      const double le = slot_eff(P, g, 0) + slot_eff(P, g, 1);
-      const double ld = slot_def(P, g, 0) + slot_def(P, g, 1);
-      const double S = warp_sum_approx(le);
-      const double DEF = warp_sum_approx(ld);
-      if (lane == 0) {
-        sm->Gat[d] = (uint8_t)G;
-        sm->S[d] = S;
-        sm->DEF[d] = DEF;
-        sm->nxt[d] = 0;
-      }
-      __syncwarp();
+    if (lane == 0) {
+      sm->Gat[d] = (uint8_t)G;
+      sm->S[d] = Sn;
+      sm->DEF[d] = Dn;
+      sm->nxt[d] = 0;
     }
+    __syncwarp();
   }
 done:
   __syncwarp();
@@ -711,42 +761,40 @@ __device__ int split_run(const KParams& kp, int p, GState& S, Entry* E, const Ru
   return count;
 }
 
-// Block-wide exclusive scan of a[0..len) in place; returns the total.
-__device__ int block_scan_excl(int* a, int len, int* smem_tmp) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int per = (len + nt - 1) / nt;
-  const int lo = min(len, tid * per), hi = min(len, lo + per);
-  int s = 0;
-  for (int i = lo; i < hi; ++i) s += a[i];
-  smem_tmp[tid] = s;
-  __syncthreads();
-  if (tid < 32) {  // warp scan over the nt partial sums
-    const int per2 = (nt + 31) / 32;
-    int loc = 0;
-    for (int t = tid * per2; t < min(nt, (tid + 1) * per2); ++t) loc += smem_tmp[t];
-    int inc = loc;
-    for (int off = 1; off < 32; off <<= 1) {
-      const int v = __shfl_up_sync(HPK_FULL_MASK, inc, off);
-      if (tid >= off) inc += v;
+// Block-wide exclusive scan of a[0..len) in place over coalesced tiles of
+// blockDim.x elements (warp shuffles + one smem round per tile); returns the total.
+template <typename T>
+__device__ T block_scan_tiles(T* a, int len, T* sh) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nw = blockDim.x >> 5;
+  T carry = 0;
+  for (int base = 0; base < len; base += blockDim.x) {
+    const int i = base + tid;
+    const T v = i < len ? a[i] : (T)0;
+    T x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const T t = __shfl_up_sync(HPK_FULL_MASK, x, o);
+      if (lane >= o) x += t;
     }
-    int run = inc - loc;
-    for (int t = tid * per2; t < min(nt, (tid + 1) * per2); ++t) {
-      const int v = smem_tmp[t];
-      smem_tmp[t] = run;
-      run += v;
+    if (lane == 31) sh[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      T w = lane < nw ? sh[lane] : (T)0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const T t = __shfl_up_sync(HPK_FULL_MASK, w, o);
+        if (lane >= o) w += t;
+      }
+      if (lane < nw) sh[lane] = w;
     }
-    if (tid == 31) smem_tmp[nt] = inc;
+    __syncthreads();
+    const T woff = warp == 0 ? (T)0 : sh[warp - 1];
+    if (i < len) a[i] = carry + woff + x - v;
+    carry += sh[nw - 1];
+    __syncthreads();
   }
-  __syncthreads();
-  int run = smem_tmp[tid];
-  for (int i = lo; i < hi; ++i) {
-    const int v = a[i];
-    a[i] = run;
-    run += v;
-  }
-  const int total = smem_tmp[nt];
-  __syncthreads();
-  return total;
+  return carry;
 }
 
 __device__ void finish_problem(const KParams& kp, GState& S) {
@@ -755,49 +803,76 @@ __device__ void finish_problem(const KParams& kp, GState& S) {
 }
 
 // Queue the first qmax positions (list order) that need a run at cutoff
-// version cver, but never a position that is provably past the budget's abort
-// point: the visits of the exact runs before it (others count 1, a lower
-// bound — a higher cutoff only prunes more) already exhaust the budget.
+// version cver (block-parallel over coalesced tiles), but never a position
+// that is provably past the budget's abort point: the visits of the exact
+// runs before it (others count 1, a lower bound — a higher cutoff only prunes
+// more) already exhaust the budget.
 __device__ void push_items(const KParams& kp, int queue, int p, const int* ids, const int* pcv,
                            const long long* pvis, const Entry* pool, int head, int len, int cver,
-                           int qmax, long long budget_left, int lane) {
+                           int qmax, long long budget_left, long long* shl, int* shi) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nw = blockDim.x >> 5;
   RunQueue* q = kp.queues + queue;
   RunItem* items = kp.items + (size_t)queue * kp.qcap;
+  long long before = 0;  // lower bound of visits before the tile
   int pushed = 0;
-  long long before = 0;  // lower bound of visits before the chunk
-  for (int base = 0; base < len && pushed < qmax; base += 32) {
-    const int i = base + lane;
-    const bool inl = i < len;
-    const bool exact = inl && pcv[head + i] == cver;
-    long long v = inl ? (exact ? pvis[head + i] : 1) : 0;
-    long long inc = v;  // inclusive scan
+  for (int base = 0; base < len; base += blockDim.x) {
+    const int j = base + tid;
+    const bool inl = j < len;
+    const bool exact = inl && pcv[head + j] == cver;
+    const long long v = inl ? (exact ? pvis[head + j] : 1) : 0;
+    // exclusive visit prefix within the tile
+    long long x = v;
 #pragma unroll
-    for (int o2 = 1; o2 < 32; o2 <<= 1) {
-      const long long t = __shfl_up_sync(HPK_FULL_MASK, inc, o2);
-      if (lane >= o2) inc += t;
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long t = __shfl_up_sync(HPK_FULL_MASK, x, o);
+      if (lane >= o) x += t;
     }
-    const long long excl = before + inc - v;
-    const bool within = budget_left < 0 || excl < budget_left;
-    const bool need = inl && !exact && within;
+    if (lane == 31) shl[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      long long w = lane < nw ? shl[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long t = __shfl_up_sync(HPK_FULL_MASK, w, o);
+        if (lane >= o) w += t;
+      }
+      if (lane < nw) shl[lane] = w;
+    }
+    __syncthreads();
+    const long long excl = before + (warp == 0 ? 0 : shl[warp - 1]) + x - v;
+    const bool need = inl && !exact && (budget_left < 0 || excl < budget_left);
+    // rank of the needing positions within the tile
     const unsigned bal = __ballot_sync(HPK_FULL_MASK, need);
-    int cnt = __popc(bal);
-    if (pushed + cnt > qmax) cnt = qmax - pushed;
-    int slot0 = 0;
-    if (lane == 0 && cnt > 0) slot0 = atomicAdd(&q->len, cnt);
-    slot0 = shfl(slot0, 0);
-    const int rank = __popc(bal & ((1u << lane) - 1));
-    if (need && rank < cnt && slot0 + rank < kp.qcap) {
+    if (lane == 0) shi[warp] = __popc(bal);
+    __syncthreads();
+    if (tid == 0) {
+      int run = 0;
+      for (int w = 0; w < nw; ++w) {
+        const int c = shi[w];
+        shi[w] = run;
+        run += c;
+      }
+      int take = min(run, qmax - pushed);
+      shi[nw] = take;
+      shi[nw + 1] = take > 0 ? atomicAdd(&q->len, take) : 0;
+    }
+    __syncthreads();
+    const int take = shi[nw], slot0 = shi[nw + 1];
+    const int rank = shi[warp] + __popc(bal & ((1u << lane) - 1));
+    if (need && rank < take && slot0 + rank < kp.qcap) {
       RunItem& it = items[slot0 + rank];
-      const int id = ids[head + i];
+      const int id = ids[head + j];
       it.problem = p;
-      it.pos = head + i;
+      it.pos = head + j;
       it.id = id;
-      it.front = (i == 0);
+      it.front = (j == 0);
       it.cap = pool[id].uncapped ? 0x3fffffffffffffffLL : kp.seg_cap;
     }
-    pushed += cnt;
-    before += shfl(inc, 31);
-    if (budget_left >= 0 && before >= budget_left) break;
+    pushed += take;
+    before += shl[nw - 1];
+    __syncthreads();
+    if (pushed >= qmax || (budget_left >= 0 && before >= budget_left)) break;
   }
 }
 
@@ -844,7 +919,7 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
   int* off = kp.scratch + (size_t)p * (kp.lcap + 1);
   for (int i = tid; i < len; i += blockDim.x) off[i] = cnt_in[head + i];
   __syncthreads();
-  int total = block_scan_excl(off, len, smem_tmp);
+  int total = block_scan_tiles<int>(off, len, smem_tmp);
   if (total > kp.lcap - kp.reserve) {
     // List nearly full: keep expansions in list order while they leave the
     // head's reserve free; the others are reverted to unrun FULL segments
@@ -872,28 +947,26 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
       }
     }
     __syncthreads();
-    total = block_scan_excl(off, len, smem_tmp);
+    total = block_scan_tiles<int>(off, len, smem_tmp);
   }
   if (tid == 0) off[len] = total;
   __syncthreads();
-  for (int o = tid; o < total; o += blockDim.x) {
-    int lo = 0, hi = len;  // largest i with off[i] <= o
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (off[mid] <= o) lo = mid;
-      else hi = mid;
-    }
-    const int k = o - off[lo];
-    if (k == 0) {
-      ids_out[o] = ids_in[head + lo];
-      pcv_out[o] = pcv_in[head + lo];
-      vis_out[o] = vis_in[head + lo];
-    } else {
-      ids_out[o] = pf_in[head + lo] + k - 1;
-      pcv_out[o] = -1;
-      vis_out[o] = 0;
-    }
+  for (int i = tid; i < len; i += blockDim.x) {  // scatter from the input side
+    const int o = off[i];
+    const int c = off[i + 1] - o;
+    ids_out[o] = ids_in[head + i];
+    pcv_out[o] = pcv_in[head + i];
+    vis_out[o] = vis_in[head + i];
     cnt_out[o] = 1;
+    if (c > 1) {
+      const int pf = pf_in[head + i];
+      for (int k = 1; k < c; ++k) {
+        ids_out[o + k] = pf + k - 1;
+        pcv_out[o + k] = -1;
+        vis_out[o + k] = 0;
+        cnt_out[o + k] = 1;
+      }
+    }
   }
   __syncthreads();
 
@@ -1017,8 +1090,12 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
         if (B >= 0 && V == B) {
           done = 1;
           aborted = i < total ? 1 : 0;
+          break;
         }
-        break;  // entries after a special one ran under a different state
+        // after an improvement the later runs used a stale cutoff: stop; after
+        // a pure deletion the cutoff is unchanged and the walk continues
+        if (shfl((int)imp, kc - 1)) break;
+        continue;
       }
       if (kc < 32) break;  // reached a position that still needs a run
     }
@@ -1081,6 +1158,14 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
     __syncthreads();
   }
   // ---- D. queue the next wave
+  if (!(flag & 2) && (flag & 1)) {
+    const int act = max(1, *((volatile int*)kp.active));
+    const int qmax = max(32, kp.qmax / act);
+    const long long bl = P.budget < 0 ? -1 : P.budget - S.V;
+    push_items(kp, next_queue, p, ids_out, pcv_out, vis_out, pool_ptr(kp, p, S.pool_cur), nhead,
+               nlen, S.cver, qmax, bl, reinterpret_cast<long long*>(smem_tmp + 64),
+               smem_tmp);
+  }
   if (warp == 0) {
     if (flag & 2) {
       if (lane == 0) {
@@ -1095,12 +1180,6 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
         it.front = 1;
         it.cap = sh_cap;
       }
-    } else if (flag & 1) {
-      const int act = max(1, *((volatile int*)kp.active));
-      const int qmax = max(32, kp.qmax / act);
-      const long long bl = P.budget < 0 ? -1 : P.budget - S.V;
-      push_items(kp, next_queue, p, ids_out, pcv_out, vis_out,
-                 pool_ptr(kp, p, S.pool_cur), nhead, nlen, S.cver, qmax, bl, lane);
     }
   }
   __syncthreads();
@@ -1174,6 +1253,17 @@ __device__ void init_problem(const KParams& kp, int p) {
     for (int d = n - 1; d >= 0; --d) {
       r += P.p[d];
       P.R[d] = r;
+    }
+    // Error budget of the incremental sums (<= ~4 roundings per level on
+    // quantities <= 2x the total power) plus the reference's own serial sum
+    // (<= n roundings): (8n + 64) ulps of the largest magnitude, doubled.
+    P.mb_abs = (double)(8 * n + 64) * kEps52 * 2.0 * (P.R[0] > 0 ? P.R[0] : 1.0);
+    if (P.exact_mem) {
+      P.md_abs = 0.0;
+    } else {
+      double mt = 0;
+      for (int i = 0; i < n; ++i) mt += fabs(P.m[i]);
+      P.md_abs = (double)(8 * n + 64) * kEps52 * 2.0 * ((double)n * fabs(P.min_mem) + mt);
     }
     // seeds: one group, singletons, by type, by node (grouping.cpp:206-225)
     uint8_t seeds[4][MAXN];
@@ -1255,17 +1345,36 @@ __device__ void init_problem(const KParams& kp, int p) {
 
 // ------------------------------------------------------------ the kernel
 
-// Grid barrier + gpu-scope fences: segment lists and problem states are
-// written on one SM and read on another in the next phase; the fences make
-// those writes visible and drop stale L1 lines.
-__device__ __forceinline__ void gsync(cg::grid_group& grid) {
-  __threadfence();
-  grid.sync();
-  __threadfence();
+// Grid barrier (all blocks are co-resident: cooperative launch). One thread
+// per block arrives and waits with __nanosleep; other warps wait on the block
+// barrier. cooperative_groups' grid.sync() spins with an L1 invalidation per
+// iteration (CCTL.IVALL in the loop, seen in the ncu source page), which wiped
+// the L1 of the warps still searching; here the invalidation happens once, in
+// the acquire fence after the release is observed.
+__device__ __forceinline__ void gsync(unsigned int* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* vgen = bar + 1;
+    const unsigned int gen = *vgen;
+    __threadfence();  // release this block's writes
+    const unsigned int arrived = atomicAdd(bar, 1u);
+    if (arrived == gridDim.x - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      unsigned int ns = 32;
+      while (*vgen == gen) {
+        __nanosleep(ns);
+        ns = ns < 256 ? ns * 2 : 256;
+      }
+    }
+    __threadfence();  // acquire: later reads see every block's writes
+  }
+  __syncthreads();
 }
 
 __global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
-  cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WarpSmem* wsm = reinterpret_cast<WarpSmem*>(smem_raw);
   int* smem_tmp = reinterpret_cast<int*>(smem_raw + sizeof(WarpSmem) * WARPS_PER_BLOCK);
@@ -1278,7 +1387,7 @@ __global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
     *kp.deadline_slot = kp.deadline_ns;
   }
   for (int p = blockIdx.x; p < kp.n_problems; p += gridDim.x) init_problem(kp, p);
-  gsync(grid);
+  gsync(kp.bar);
   kp.deadline_ns = *((volatile unsigned long long*)kp.deadline_slot);
 
   int cur = 0;
@@ -1291,8 +1400,9 @@ __global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
     RunQueue* q = kp.queues + cur;
     RunItem* items = kp.items + (size_t)cur * kp.qcap;
     const int qlen = min(*((volatile int*)&q->len), kp.qcap);
+    unsigned long long t_w0 = 0;
     if (kp.trace && blockIdx.x == 0 && threadIdx.x == 0)
-      printf("[hpk] wave %d run phase: %d items (active %d)\n", wave, qlen, *((volatile int*)kp.active));
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_w0));
     while (true) {
       int it = 0;
       if (lane == 0) it = atomicAdd(&q->head, 1);
@@ -1305,7 +1415,8 @@ __global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
       Entry* E = pool_ptr(kp, p, S.pool_cur) + item.id;
       const double C = S.C;
       const int cver = S.cver;
-      RunOut o = run_segment(P, E, E, C, item.cap, wsm + warp, lane, kp.err, kp.deadline_ns);
+      const PView PV = stage_problem(P, wsm + warp, lane);
+      RunOut o = run_segment(PV, E, E, C, item.cap, wsm + warp, lane, kp.err, kp.deadline_ns);
       int* pcv = list_arr(kp, p, S.cur, 1);
       int* cnt = list_arr(kp, p, S.cur, 2);
       int* pfirst = list_arr(kp, p, S.cur, 3);
@@ -1343,7 +1454,10 @@ __global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
       }
       __syncwarp();
     }
-    gsync(grid);
+    gsync(kp.bar);
+    unsigned long long t_w1 = 0;
+    if (kp.trace && blockIdx.x == 0 && threadIdx.x == 0)
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_w1));
     // ---- schedule phase
     for (int p = blockIdx.x; p < kp.n_problems; p += gridDim.x)
       schedule_problem(kp, p, cur ^ 1, smem_tmp);
@@ -1355,7 +1469,13 @@ __global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
         atomicExch(kp.active, -1000000);
       }
     }
-    gsync(grid);
+    gsync(kp.bar);
+    if (kp.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+      unsigned long long t_w2;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_w2));
+      printf("[hpk] wave %d: %d runs, run %.1f us, schedule %.1f us (active %d)\n", wave, qlen,
+             (t_w1 - t_w0) * 1e-3, (t_w2 - t_w1) * 1e-3, *((volatile int*)kp.active));
+    }
     if (*((volatile int*)kp.active) <= 0) break;
     cur ^= 1;
   }
@@ -1632,7 +1752,7 @@ int ensure_ctx(DeviceCtx& c, int device) {
   HPK_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
   HPK_CUDA(cudaEventCreate(&c.ev0));
   HPK_CUDA(cudaEventCreate(&c.ev1));
-  HPK_CUDA(cudaMalloc(&c.active, sizeof(int) * 4));
+  HPK_CUDA(cudaMalloc(&c.active, sizeof(int) * 8));
   HPK_CUDA(cudaMalloc(&c.queues, sizeof(RunQueue) * 2));
   c.device = device;
   return 0;
@@ -1825,8 +1945,8 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     HPK_CUDA(cudaMemcpyAsync(c.probs, hp.data(), sizeof(GProb) * P, cudaMemcpyHostToDevice,
                              c.stream));
     HPK_CUDA(cudaMemsetAsync(c.queues, 0, sizeof(RunQueue) * 2, c.stream));
-    const int init_flags[2] = {P, 0};
-    HPK_CUDA(cudaMemcpyAsync(c.active, init_flags, sizeof(int) * 2, cudaMemcpyHostToDevice,
+    const int init_flags[8] = {P, 0, 0, 0, 0, 0, 0, 0};
+    HPK_CUDA(cudaMemcpyAsync(c.active, init_flags, sizeof(int) * 8, cudaMemcpyHostToDevice,
                              c.stream));
     t_timing.h2d_bytes += sizeof(GProb) * P + sizeof(int);
 
@@ -1851,6 +1971,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     kp.max_waves = cfg.max_waves > 0 ? cfg.max_waves : 1000000;  // watchdog
     kp.deadline_ns = (unsigned long long)(cfg.max_seconds > 0 ? cfg.max_seconds : 120.0) * 1000000000ull;
     kp.deadline_slot = reinterpret_cast<unsigned long long*>(c.active + 2);
+    kp.bar = reinterpret_cast<unsigned int*>(c.active + 4);
     kp.trace = getenv("HPK_TRACE") ? atoi(getenv("HPK_TRACE")) : 0;
     const size_t smem = sizeof(WarpSmem) * WARPS_PER_BLOCK + sizeof(int) * (BLOCK_THREADS + 8);
     void* args[] = {&kp};
