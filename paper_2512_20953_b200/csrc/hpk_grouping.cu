@@ -125,6 +125,7 @@ struct KParams {
   unsigned long long deadline_ns;  // %globaltimer watchdog (relative at launch)
   unsigned long long* deadline_slot;
   unsigned int* bar;               // grid barrier {count, generation}
+  unsigned long long* prof;        // trace >= 2: runner phase cycle counters
   int trace;                       // HPK_TRACE=1: per-wave scheduler printf (debug)
 };
 
@@ -325,7 +326,10 @@ struct RunOut {
 // DFS of subtree(E.u) in preorder (PREFIX: stopping before E.end), cap visits.
 __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, double C,
                               long long cap, WarpSmem* sm, int lane, int* err,
-                              unsigned long long deadline) {
+                              unsigned long long deadline, unsigned long long* prof) {
+  // prof (trace >= 2): [0] leaf-batch cycles [1] batches [2] leaves
+  //                    [3] child-check cycles [4] checks [5] descend cycles [6] pop cycles
+  long long pc0 = 0;
   const int n = P.n;
   const int du = E->du;
   const bool prefix = E->kind == KIND_PREFIX;
@@ -449,6 +453,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
     }
     if (d == n - 1) {
       // ---- leaf batch: children c = c0..G are leaves (unit n-1) ----
+      if (prof) pc0 = clock64();
       const int c0 = sm->nxt[d];
       int count = G + 1 - c0;
       bool end_hit = false;
@@ -565,6 +570,11 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
           cut = mx > cut ? mx : cut;
         }
       }
+      if (prof && lane == 0) {
+        atomicAdd(prof + 0, (unsigned long long)(clock64() - pc0));
+        atomicAdd(prof + 1, 1ull);
+        atomicAdd(prof + 2, (unsigned long long)(count > 0 ? count : 0));
+      }
       if (cap_hit) {
         o.dstop = d + 1;
         o.stop_c = c0 + count;
@@ -584,10 +594,12 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
         o.finished = true;
         break;
       }
+      if (prof) pc0 = clock64();
       const int grp = sm->path[d - 1];
       remove_unit(P, g, lane, grp, P.p[d - 1], P.m[d - 1]);
       G = sm->Gat[d - 1];
       --d;
+      if (prof && lane == 0) atomicAdd(prof + 6, (unsigned long long)(clock64() - pc0));
       if (match > d) match = d;
       continue;
     }
@@ -604,6 +616,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
       o.finished = false;
       break;
     }
+    if (prof) pc0 = clock64();
     o.visits += 1;
     if (lane == 0) sm->nxt[d] = (uint8_t)(c + 1);
     __syncwarp();  // every lane re-reads nxt[d] at the next iteration
@@ -651,10 +664,15 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
       dec = exact_passes(P, g, Gc, d + 1, cut) ? DEC_PASS : DEC_PRUNE;
       remove_unit(P, g, lane, c, P.p[d], P.m[d]);
     }
+    if (prof && lane == 0) {
+      atomicAdd(prof + 3, (unsigned long long)(clock64() - pc0));
+      atomicAdd(prof + 4, 1ull);
+    }
     if (dec == DEC_PRUNE) {
       if (prefix && match == d && c == sm->endp[d] && o.a_star < 0) o.a_star = d + 1;
       continue;
     }
+    if (prof) pc0 = clock64();
     // ---- descend into child c ----
     if (lane == 0) sm->path[d] = (uint8_t)c;
     __syncwarp();
@@ -669,6 +687,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
       sm->nxt[d] = 0;
     }
     __syncwarp();
+    if (prof && lane == 0) atomicAdd(prof + 5, (unsigned long long)(clock64() - pc0));
   }
 done:
   __syncwarp();
@@ -1416,7 +1435,8 @@ __global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
       const double C = S.C;
       const int cver = S.cver;
       const PView PV = stage_problem(P, wsm + warp, lane);
-      RunOut o = run_segment(PV, E, E, C, item.cap, wsm + warp, lane, kp.err, kp.deadline_ns);
+      RunOut o = run_segment(PV, E, E, C, item.cap, wsm + warp, lane, kp.err, kp.deadline_ns,
+                              kp.trace >= 2 ? kp.prof : nullptr);
       int* pcv = list_arr(kp, p, S.cur, 1);
       int* cnt = list_arr(kp, p, S.cur, 2);
       int* pfirst = list_arr(kp, p, S.cur, 3);
@@ -1478,6 +1498,13 @@ __global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
     }
     if (*((volatile int*)kp.active) <= 0) break;
     cur ^= 1;
+  }
+  if (kp.trace >= 2 && blockIdx.x == 0 && threadIdx.x == 0) {
+    const unsigned long long* q = kp.prof;
+    printf("[hpk-prof] leaf batches %llu (leaves %llu): %.1f cyc/batch | child checks %llu: %.1f "
+           "cyc/check | descend %.1f cyc/check | pop total %llu cyc\n",
+           q[1], q[2], q[1] ? (double)q[0] / q[1] : 0.0, q[4], q[4] ? (double)q[3] / q[4] : 0.0,
+           q[4] ? (double)q[5] / q[4] : 0.0, q[6]);
   }
 }
 
@@ -1752,7 +1779,7 @@ int ensure_ctx(DeviceCtx& c, int device) {
   HPK_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
   HPK_CUDA(cudaEventCreate(&c.ev0));
   HPK_CUDA(cudaEventCreate(&c.ev1));
-  HPK_CUDA(cudaMalloc(&c.active, sizeof(int) * 8));
+  HPK_CUDA(cudaMalloc(&c.active, sizeof(int) * 32));
   HPK_CUDA(cudaMalloc(&c.queues, sizeof(RunQueue) * 2));
   c.device = device;
   return 0;
@@ -1945,8 +1972,9 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     HPK_CUDA(cudaMemcpyAsync(c.probs, hp.data(), sizeof(GProb) * P, cudaMemcpyHostToDevice,
                              c.stream));
     HPK_CUDA(cudaMemsetAsync(c.queues, 0, sizeof(RunQueue) * 2, c.stream));
-    const int init_flags[8] = {P, 0, 0, 0, 0, 0, 0, 0};
-    HPK_CUDA(cudaMemcpyAsync(c.active, init_flags, sizeof(int) * 8, cudaMemcpyHostToDevice,
+    int init_flags[32] = {0};
+    init_flags[0] = P;
+    HPK_CUDA(cudaMemcpyAsync(c.active, init_flags, sizeof(int) * 32, cudaMemcpyHostToDevice,
                              c.stream));
     t_timing.h2d_bytes += sizeof(GProb) * P + sizeof(int);
 
@@ -1972,6 +2000,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     kp.deadline_ns = (unsigned long long)(cfg.max_seconds > 0 ? cfg.max_seconds : 120.0) * 1000000000ull;
     kp.deadline_slot = reinterpret_cast<unsigned long long*>(c.active + 2);
     kp.bar = reinterpret_cast<unsigned int*>(c.active + 4);
+    kp.prof = reinterpret_cast<unsigned long long*>(c.active + 8);
     kp.trace = getenv("HPK_TRACE") ? atoi(getenv("HPK_TRACE")) : 0;
     const size_t smem = sizeof(WarpSmem) * WARPS_PER_BLOCK + sizeof(int) * (BLOCK_THREADS + 8);
     void* args[] = {&kp};
