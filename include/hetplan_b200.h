@@ -230,6 +230,12 @@ typedef struct hpk_timing {
 void hpk_last_timing(hpk_timing* out);
 void hpk_reset_timing(void);
 
+/* Device self-test of the grouping filter decision (regression pin for an
+ * nvcc 12.9 sm_100a miscompile): cases = n (A, D, cut) triplets,
+ * rem = rm4[2]; writes 0 pass / 1 prune / 2 exact per case. */
+int hpk_selftest_decide(const double* cases, int n, const double* rm4, double mb_abs,
+                        double md_abs, int* out_codes);
+
 /* Issue-rate microbenchmarks (roofline denominators for this FP64/INT32-issue
  * bound path): fp64 DMUL+DADD ops/s and int32 IADD+LOP ops/s on `device`. */
 int hpk_measure_issue_peaks(int device, double* fp64_ops_per_s, double* int_ops_per_s);

@@ -100,6 +100,7 @@ struct GState {
 struct RunItem {
   int problem, pos, id, front;
   long long cap;
+  double cut;  // predicted entering cutoff (exact-checked at commit)
 };
 
 struct RunQueue {
@@ -113,6 +114,7 @@ struct KParams {
   Entry* pools;       // [P][2][pcap]
   int* lists;         // [P][2][4][lcap]: ids, pcver, cnt, pfirst
   long long* lvis;    // [P][2][lcap]: visits of the finished run at each position
+  double* ldbl;       // [P][2][2][lcap]: cutoff the run at each position used, its max objective
   int* scratch;       // [P][lcap + 1]
   RunQueue* queues;   // [2]
   RunItem* items;     // [2][qcap]
@@ -127,6 +129,7 @@ struct KParams {
   unsigned int* bar;               // grid barrier {count, generation}
   unsigned long long* prof;        // trace >= 2: runner phase cycle counters
   int trace;                       // HPK_TRACE=1: per-wave scheduler printf (debug)
+  int trace_p;                     // HPK_TRACE_P: only this problem (-1: all)
 };
 
 __device__ __forceinline__ Entry* pool_ptr(const KParams& kp, int p, int which) {
@@ -140,6 +143,10 @@ __device__ __forceinline__ int* list_arr(const KParams& kp, int p, int buf, int 
 __device__ __forceinline__ long long* list_vis(const KParams& kp, int p, int buf) {
   return kp.lvis + ((size_t)p * 2 + buf) * kp.lcap;
 }
+// which: 0 = cutoff used by the run at the position, 1 = its max leaf objective
+__device__ __forceinline__ double* list_dbl(const KParams& kp, int p, int buf, int which) {
+  return kp.ldbl + (((size_t)p * 2 + buf) * 2 + which) * kp.lcap;
+}
 
 // --------------------------------------------------------------- warp DFS
 
@@ -148,6 +155,9 @@ struct WarpSmem {
   double tp[MAXN], tm[MAXN], tf[MAXN + 2], tR[MAXN + 1], tRM[MAXN + 1];
   double S[MAXN + 1];    // approx sum of Eq.(2) effective powers at each level
   double DEF[MAXN + 1];  // approx memory deficit at each level
+  unsigned long long mpass[MAXN + 1];   // per level: children that pass the check
+  unsigned long long mprune[MAXN + 1];  // per level: children that are pruned
+  double mcut[MAXN + 1];                // cutoff the masks were computed with
   uint8_t path[MAXN];
   uint8_t nxt[MAXN + 1];
   uint8_t Gat[MAXN + 1];
@@ -296,21 +306,40 @@ __device__ bool exact_passes(const PView& P, const Groups& g, int G, int next, d
 // along the path). P.mb_abs / P.md_abs bound the gap between the
 // approximations and the reference's serial fp64 sums; only a
 // cutoff inside that margin needs the exact serial evaluation.
+// NOTE: written as early returns on purpose. The equivalent if/else-chain
+// formulation (db/dd codes combined at the end) is miscompiled by nvcc 12.9 for
+// sm_100a at -O3 — it never returns PASS (found with the HPK_TRACE=2 counters:
+// 44% of child checks fell to the exact path); tools/ubench/decide_test2.cu
+// and hpk_selftest_decide() pin the correct behaviour on the device.
+__device__ __noinline__ int decide_core(double A, double D, double rem, double cut,
+                                       double mb_abs, double md_abs) {
+  const bool has_cut = cut >= 0;
+  const bool b_prune = has_cut && (A + mb_abs < cut);
+  const bool d_prune = D - md_abs > rem;
+  if (b_prune || d_prune) return DEC_PRUNE;
+  const bool b_pass = !has_cut || (A - mb_abs >= cut);
+  const bool d_pass = D + md_abs <= rem;
+  return (b_pass && d_pass) ? DEC_PASS : DEC_EXACT;
+}
 __device__ __forceinline__ int decide(const PView& P, double A, double D, int next, double cut) {
-  int db = DEC_PASS;
-  if (cut >= 0) {
-    if (A + P.mb_abs < cut) db = DEC_PRUNE;
-    else if (A - P.mb_abs >= cut) db = DEC_PASS;
-    else db = DEC_EXACT;
+  return decide_core(A, D, P.RM[next], cut, P.mb_abs, P.md_abs);
+}
+
+// Device self-test of the filter decision on a grid of cases (see note above).
+__global__ void hpk_selftest_decide_kernel(const double* in, int n, const double* rm,
+                                           double mb, double md, int* out) {
+  __shared__ double sRM[4];
+  if (threadIdx.x < 4) sRM[threadIdx.x] = rm[threadIdx.x];
+  __syncthreads();
+  PView P;
+  P.RM = sRM;
+  P.mb_abs = mb;
+  P.md_abs = md;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    int r = -1;
+    if ((threadIdx.x & 31) == (i & 31)) r = decide(P, in[3 * i], in[3 * i + 1], 2, in[3 * i + 2]);
+    out[i] = r;
   }
-  const double rem = P.RM[next];
-  int dd;
-  if (D - P.md_abs > rem) dd = DEC_PRUNE;
-  else if (D + P.md_abs <= rem) dd = DEC_PASS;
-  else dd = DEC_EXACT;
-  if (db == DEC_PRUNE || dd == DEC_PRUNE) return DEC_PRUNE;
-  if (db == DEC_PASS && dd == DEC_PASS) return DEC_PASS;
-  return DEC_EXACT;
 }
 
 struct RunOut {
@@ -326,7 +355,8 @@ struct RunOut {
 // DFS of subtree(E.u) in preorder (PREFIX: stopping before E.end), cap visits.
 __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, double C,
                               long long cap, WarpSmem* sm, int lane, int* err,
-                              unsigned long long deadline, unsigned long long* prof) {
+                              unsigned long long deadline, unsigned long long* prof,
+                              bool dbg) {
   // prof (trace >= 2): [0] leaf-batch cycles [1] batches [2] leaves
   //                    [3] child-check cycles [4] checks [5] descend cycles [6] pop cycles
   long long pc0 = 0;
@@ -431,6 +461,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
       sm->S[d] = S;
       sm->DEF[d] = DEF;
       sm->nxt[d] = 0;
+      sm->mcut[d] = __longlong_as_double(0x7ff8000000000000LL);  // NaN: masks invalid
     }
     __syncwarp();
   }
@@ -494,8 +525,10 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
           i1 = lane + 32;
           m2 = eff_k[0];
         }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
+        // reductions only span the lanes that own groups/children: width W =
+        // next power of two >= G+1 (the full warp once slot 1 is in use)
+        const int W = G + 1 > 32 ? 32 : (G + 1 <= 1 ? 1 : 1 << (32 - __clz(G)));
+        for (int off = W >> 1; off > 0; off >>= 1) {
           const double om1 = __shfl_xor_sync(HPK_FULL_MASK, m1, off);
           const int oi1 = __shfl_xor_sync(HPK_FULL_MASK, i1, off);
           const double om2 = __shfl_xor_sync(HPK_FULL_MASK, m2, off);
@@ -542,8 +575,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
             }
           }
         }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
+        for (int off = W >> 1; off > 0; off >>= 1) {
           const double oo = __shfl_xor_sync(HPK_FULL_MASK, best_o, off);
           const int og = __shfl_xor_sync(HPK_FULL_MASK, best_Gc, off);
           const int oc = __shfl_xor_sync(HPK_FULL_MASK, best_c, off);
@@ -554,6 +586,12 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
           }
           const double om = __shfl_xor_sync(HPK_FULL_MASK, mx, off);
           mx = om > mx ? om : mx;
+        }
+        if (W < 32) {  // make the block-[0,W) result warp-uniform
+          best_o = shfl(best_o, 0);
+          best_Gc = shfl(best_Gc, 0);
+          best_c = shfl(best_c, 0);
+          mx = shfl(mx, 0);
         }
         o.visits += count;
         if (best_o >= 0) {
@@ -574,6 +612,8 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
         atomicAdd(prof + 0, (unsigned long long)(clock64() - pc0));
         atomicAdd(prof + 1, 1ull);
         atomicAdd(prof + 2, (unsigned long long)(count > 0 ? count : 0));
+        if (prof[11] == 4)
+          printf("[hpk-t] leaves d %d G %d count %d cut %.17g\n", d, G, count, cut);
       }
       if (cap_hit) {
         o.dstop = d + 1;
@@ -620,21 +660,64 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
     o.visits += 1;
     if (lane == 0) sm->nxt[d] = (uint8_t)(c + 1);
     __syncwarp();  // every lane re-reads nxt[d] at the next iteration
-    // ---- check child c (internal node at depth d+1) on its owner lane ----
-    // The child's level sums follow from the parent's in O(1):
-    //   S' = S - eff(c) + eff'(c),  DEF' = DEF - def(c) + def'(c)
+    // ---- check child c (internal node at depth d+1) ----
+    // All children of the node at depth d are checked in ONE lane-parallel
+    // round (lane ci decides child ci); the outcome is kept as pass/prune
+    // bitmasks per level and reused until the cutoff changes. The child's
+    // level sums follow from the parent's in O(1):
+    //   S' = S - eff(ci) + eff'(ci),  DEF' = DEF - def(ci) + def'(ci)
+    if (sm->mcut[d] != cut) {
+      int ldec[2] = {DEC_PRUNE, DEC_PRUNE};
+      const double up = P.p[d], um = P.m[d];
+      const double Sd = sm->S[d], Dd = sm->DEF[d], Rn = P.R[d + 1];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int ci = lane + 32 * k;
+        if (ci <= G) {
+          double eff_old, eff_new, def_old, def_new;
+          if (ci < G) {
+            eff_old = g.gp[k] * g.f0[k];
+            eff_new = (g.gp[k] + up) * g.f1[k];
+            const double d0 = P.min_mem - g.gm[k];
+            def_old = d0 > 0.0 ? d0 : 0.0;
+            const double d1 = P.min_mem - (g.gm[k] + um);
+            def_new = d1 > 0.0 ? d1 : 0.0;
+          } else {
+            eff_old = 0;
+            eff_new = up * P.f[1];
+            def_old = 0;
+            const double d1 = P.min_mem - um;
+            def_new = d1 > 0.0 ? d1 : 0.0;
+          }
+          const double lS = (Sd - eff_old) + eff_new;
+          const double lD = (Dd - def_old) + def_new;
+          ldec[k] = decide(P, lS + Rn, lD, d + 1, cut);
+        }
+      }
+      const unsigned p0 = __ballot_sync(HPK_FULL_MASK, ldec[0] == DEC_PASS);
+      const unsigned p1 = __ballot_sync(HPK_FULL_MASK, ldec[1] == DEC_PASS);
+      const unsigned r0 = __ballot_sync(HPK_FULL_MASK, ldec[0] == DEC_PRUNE);
+      const unsigned r1 = __ballot_sync(HPK_FULL_MASK, ldec[1] == DEC_PRUNE);
+      if (lane == 0) {
+        sm->mpass[d] = (unsigned long long)p0 | ((unsigned long long)p1 << 32);
+        sm->mprune[d] = (unsigned long long)r0 | ((unsigned long long)r1 << 32);
+        sm->mcut[d] = cut;
+      }
+      __syncwarp();
+    }
     int dec;
-    double Sn, Dn;
     {
+      const unsigned long long bit = 1ull << c;
+      dec = (sm->mpass[d] & bit) ? DEC_PASS : ((sm->mprune[d] & bit) ? DEC_PRUNE : DEC_EXACT);
+    }
+    if (dbg) {  // HPK_TRACE=3: cross-check the mask against a direct owner-lane decision
       const int owner = c & 31, k = c >> 5;
-      int ldec = 0;
-      double lS = 0, lD = 0;
+      int ld = 0;
       if (lane == owner) {
         const double up = P.p[d], um = P.m[d];
-        double eff_old, eff_new, def_old, def_new;
-        const int gck = k == 0 ? g.gc[0] : g.gc[1];
         const double gpk = k == 0 ? g.gp[0] : g.gp[1];
         const double gmk = k == 0 ? g.gm[0] : g.gm[1];
+        double eff_old, eff_new, def_old, def_new;
         if (c < G) {
           eff_old = gpk * (k == 0 ? g.f0[0] : g.f0[1]);
           eff_new = (gpk + up) * (k == 0 ? g.f1[0] : g.f1[1]);
@@ -649,20 +732,54 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
           const double d1 = P.min_mem - um;
           def_new = d1 > 0.0 ? d1 : 0.0;
         }
-        (void)gck;
-        lS = (sm->S[d] - eff_old) + eff_new;
-        lD = (sm->DEF[d] - def_old) + def_new;
-        ldec = decide(P, lS + P.R[d + 1], lD, d + 1, cut);
+        const double lS = (sm->S[d] - eff_old) + eff_new;
+        const double lD = (sm->DEF[d] - def_old) + def_new;
+        ld = decide(P, lS + P.R[d + 1], lD, d + 1, cut);
+        if (ld != dec)
+          printf("[hpk-dbg] mask/direct mismatch d %d c %d G %d cut %.17g mcut %.17g mask %d direct "
+                 "%d mpass %llx mprune %llx\n", d, c, G, cut, sm->mcut[d], dec, ld, sm->mpass[d],
+                 sm->mprune[d]);
       }
-      dec = shfl(ldec, owner);
-      Sn = shfl(lS, owner);
-      Dn = shfl(lD, owner);
+      __syncwarp();
     }
+    if (prof && prof[11] == 4 && lane == 0)
+      printf("[hpk-t] check d %d c %d G %d dec %d cut %.17g S %.17g DEF %.17g\n", d, c, G, dec, cut,
+             sm->S[d], sm->DEF[d]);
     if (dec == DEC_EXACT) {
+      if (prof && lane == 0) atomicAdd(prof + 9, 1ull);
       add_unit(P, g, lane, c, P.p[d], P.m[d]);
       const int Gc = c == G ? G + 1 : G;
       dec = exact_passes(P, g, Gc, d + 1, cut) ? DEC_PASS : DEC_PRUNE;
       remove_unit(P, g, lane, c, P.p[d], P.m[d]);
+    }
+    double Sn = 0, Dn = 0;
+    if (dec == DEC_PASS) {  // (also after an exact-path PASS) the owner lane recomputes the child's level sums
+      const int owner = c & 31, k = c >> 5;
+      double lS = 0, lD = 0;
+      if (lane == owner) {
+        const double up = P.p[d], um = P.m[d];
+        const double gpk = k == 0 ? g.gp[0] : g.gp[1];
+        const double gmk = k == 0 ? g.gm[0] : g.gm[1];
+        double eff_old, eff_new, def_old, def_new;
+        if (c < G) {
+          eff_old = gpk * (k == 0 ? g.f0[0] : g.f0[1]);
+          eff_new = (gpk + up) * (k == 0 ? g.f1[0] : g.f1[1]);
+          const double d0 = P.min_mem - gmk;
+          def_old = d0 > 0.0 ? d0 : 0.0;
+          const double d1 = P.min_mem - (gmk + um);
+          def_new = d1 > 0.0 ? d1 : 0.0;
+        } else {
+          eff_old = 0;
+          eff_new = up * P.f[1];
+          def_old = 0;
+          const double d1 = P.min_mem - um;
+          def_new = d1 > 0.0 ? d1 : 0.0;
+        }
+        lS = (sm->S[d] - eff_old) + eff_new;
+        lD = (sm->DEF[d] - def_old) + def_new;
+      }
+      Sn = shfl(lS, owner);
+      Dn = shfl(lD, owner);
     }
     if (prof && lane == 0) {
       atomicAdd(prof + 3, (unsigned long long)(clock64() - pc0));
@@ -685,6 +802,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
       sm->S[d] = Sn;
       sm->DEF[d] = Dn;
       sm->nxt[d] = 0;
+      sm->mcut[d] = __longlong_as_double(0x7ff8000000000000LL);  // NaN: masks invalid
     }
     __syncwarp();
     if (prof && lane == 0) atomicAdd(prof + 5, (unsigned long long)(clock64() - pc0));
@@ -821,24 +939,55 @@ __device__ void finish_problem(const KParams& kp, GState& S) {
   atomicSub(kp.active, 1);
 }
 
-// Queue the first qmax positions (list order) that need a run at cutoff
-// version cver (block-parallel over coalesced tiles), but never a position
-// that is provably past the budget's abort point: the visits of the exact
-// runs before it (others count 1, a lower bound — a higher cutoff only prunes
-// more) already exhaust the budget.
-__device__ void push_items(const KParams& kp, int queue, int p, const int* ids, const int* pcv,
-                           const long long* pvis, const Entry* pool, int head, int len, int cver,
-                           int qmax, long long budget_left, long long* shl, int* shi) {
+// Queue the first qmax positions (list order) whose run is missing or used a
+// cutoff other than the PREDICTED entering cutoff
+//     c^_j = max(C_front, max objective found by the runs before j),
+// which equals the exact cutoff whenever those runs are exact (the commit walk
+// checks the equality exactly, so a wrong prediction only costs a re-run).
+// Positions provably past the budget's abort point are never queued: the
+// visits of the exact runs before them (others count 1, a lower bound — a
+// higher cutoff only prunes more) already exhaust the budget.
+__device__ void push_items(const KParams& kp, int queue, int p, const int* ids, const int* pran,
+                           const long long* pvis, const double* pcut, const double* pm,
+                           const Entry* pool, int head, int len, double C, int qmax,
+                           long long budget_left, long long* shl, double* shd, int* shi) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nw = blockDim.x >> 5;
   RunQueue* q = kp.queues + queue;
   RunItem* items = kp.items + (size_t)queue * kp.qcap;
   long long before = 0;  // lower bound of visits before the tile
+  double cmax = C;       // predicted cutoff entering the tile
   int pushed = 0;
   for (int base = 0; base < len; base += blockDim.x) {
     const int j = base + tid;
     const bool inl = j < len;
-    const bool exact = inl && pcv[head + j] == cver;
+    const bool ran = inl && pran[head + j] == 1;
+    const double mj = ran ? pm[head + j] : -1.0;
+    // exclusive prefix max of m within the tile -> predicted cutoff
+    double xm = mj;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double t = __shfl_up_sync(HPK_FULL_MASK, xm, o);
+      if (lane >= o) xm = t > xm ? t : xm;
+    }
+    double ex = __shfl_up_sync(HPK_FULL_MASK, xm, 1);
+    if (lane == 0) ex = -1.0;
+    if (lane == 31) shd[warp] = xm;
+    __syncthreads();
+    if (warp == 0) {
+      double w = lane < nw ? shd[lane] : -1.0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double t = __shfl_up_sync(HPK_FULL_MASK, w, o);
+        if (lane >= o) w = t > w ? t : w;
+      }
+      if (lane < nw) shd[lane] = w;
+    }
+    __syncthreads();
+    double chat = cmax;
+    if (warp > 0) chat = shd[warp - 1] > chat ? shd[warp - 1] : chat;
+    chat = ex > chat ? ex : chat;
+    const bool exact = ran && pcut[head + j] == chat;
     const long long v = inl ? (exact ? pvis[head + j] : 1) : 0;
     // exclusive visit prefix within the tile
     long long x = v;
@@ -861,7 +1010,6 @@ __device__ void push_items(const KParams& kp, int queue, int p, const int* ids, 
     __syncthreads();
     const long long excl = before + (warp == 0 ? 0 : shl[warp - 1]) + x - v;
     const bool need = inl && !exact && (budget_left < 0 || excl < budget_left);
-    // rank of the needing positions within the tile
     const unsigned bal = __ballot_sync(HPK_FULL_MASK, need);
     if (lane == 0) shi[warp] = __popc(bal);
     __syncthreads();
@@ -879,6 +1027,7 @@ __device__ void push_items(const KParams& kp, int queue, int p, const int* ids, 
     __syncthreads();
     const int take = shi[nw], slot0 = shi[nw + 1];
     const int rank = shi[warp] + __popc(bal & ((1u << lane) - 1));
+    if (need && rank < take && slot0 + rank >= kp.qcap) atomicOr(kp.err, 4);  // must not happen
     if (need && rank < take && slot0 + rank < kp.qcap) {
       RunItem& it = items[slot0 + rank];
       const int id = ids[head + j];
@@ -887,9 +1036,11 @@ __device__ void push_items(const KParams& kp, int queue, int p, const int* ids, 
       it.id = id;
       it.front = (j == 0);
       it.cap = pool[id].uncapped ? 0x3fffffffffffffffLL : kp.seg_cap;
+      it.cut = chat;
     }
     pushed += take;
     before += shl[nw - 1];
+    cmax = shd[nw - 1] > cmax ? shd[nw - 1] : cmax;
     __syncthreads();
     if (pushed >= qmax || (budget_left >= 0 && before >= budget_left)) break;
   }
@@ -912,6 +1063,10 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
   int* cnt_out = list_arr(kp, p, cur ^ 1, 2);
   long long* vis_in = list_vis(kp, p, cur);
   long long* vis_out = list_vis(kp, p, cur ^ 1);
+  double* cut_in = list_dbl(kp, p, cur, 0);
+  double* m_in = list_dbl(kp, p, cur, 1);
+  double* cut_out = list_dbl(kp, p, cur ^ 1, 0);
+  double* m_out = list_dbl(kp, p, cur ^ 1, 1);
   Entry* pool = pool_ptr(kp, p, S.pool_cur);
 
   if (S.rerun_pending) {
@@ -976,6 +1131,8 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
     ids_out[o] = ids_in[head + i];
     pcv_out[o] = pcv_in[head + i];
     vis_out[o] = vis_in[head + i];
+    cut_out[o] = cut_in[head + i];
+    m_out[o] = m_in[head + i];
     cnt_out[o] = 1;
     if (c > 1) {
       const int pf = pf_in[head + i];
@@ -983,6 +1140,8 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
         ids_out[o + k] = pf + k - 1;
         pcv_out[o + k] = -1;
         vis_out[o + k] = 0;
+        cut_out[o + k] = -1.0;
+        m_out[o + k] = -1.0;
         cnt_out[o + k] = 1;
       }
     }
@@ -1002,7 +1161,7 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
     long long rerun_cap = 0;
     while (i < total) {
       const int j = i + lane;
-      const bool ok = j < total && pcv_out[j] == cver;
+      const bool ok = j < total && pcv_out[j] == 1 && cut_out[j] == C;
       long long v = 0;
       double m = -1, bo = 0;
       int bg = 0, hb = 0, ast = -1, kind = 0;
@@ -1111,17 +1270,18 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
           aborted = i < total ? 1 : 0;
           break;
         }
-        // after an improvement the later runs used a stale cutoff: stop; after
-        // a pure deletion the cutoff is unchanged and the walk continues
-        if (shfl((int)imp, kc - 1)) break;
+        // after an improvement or a deletion the walk continues; every later
+        // position is re-checked against the updated exact cutoff C
         continue;
       }
       if (kc < 32) break;  // reached a position that still needs a run
     }
     if (lane == 0) {
-      if (kp.trace)
-        printf("[hpk] wave %d p %d len %d total %d commit %d V %lld C %.17g cver %d pool %d\n",
-               S.waves, p, len, total, i, V, C, cver, S.pool_top);
+      if (kp.trace && (kp.trace_p < 0 || kp.trace_p == p) && S.waves < 200000)
+        printf("[hpk] wave %d p %d len %d total %d commit %d V %lld C %.17g pool %d head-pcv %d "
+               "head-cut %.17g head-uncapped %d\n",
+               S.waves, p, len, total, i, V, C, S.pool_top, total > i ? pcv_out[i] : -9,
+               total > i ? cut_out[i] : -9.0, total > i ? (int)pool[ids_out[i]].uncapped : -9);
       S.C = C;
       S.cver = cver;
       S.V = V;
@@ -1159,12 +1319,16 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
       np[k] = pool[ids_out[nhead + k]];
       pcv_tmp[k] = pcv_out[nhead + k];
       vis_tmp[k] = vis_out[nhead + k];
+      cut_in[k] = cut_out[nhead + k];
+      m_in[k] = m_out[nhead + k];
     }
     __syncthreads();
     for (int k = tid; k < nlen; k += blockDim.x) {
       ids_out[k] = k;
       pcv_out[k] = pcv_tmp[k];
       vis_out[k] = vis_tmp[k];
+      cut_out[k] = cut_in[k];
+      m_out[k] = m_in[k];
       cnt_out[k] = 1;
     }
     __syncthreads();
@@ -1178,12 +1342,16 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
   }
   // ---- D. queue the next wave
   if (!(flag & 2) && (flag & 1)) {
-    const int act = max(1, *((volatile int*)kp.active));
+    // share of the run slots: from the active count SNAPSHOT taken before this
+    // schedule phase (the live count drops as problems finish mid-phase; using it
+    // let late schedulers over-push past qcap, starving problems)
+    const int act = max(1, *((volatile int*)kp.active + 6));
     const int qmax = max(32, kp.qmax / act);
     const long long bl = P.budget < 0 ? -1 : P.budget - S.V;
-    push_items(kp, next_queue, p, ids_out, pcv_out, vis_out, pool_ptr(kp, p, S.pool_cur), nhead,
-               nlen, S.cver, qmax, bl, reinterpret_cast<long long*>(smem_tmp + 64),
-               smem_tmp);
+    push_items(kp, next_queue, p, ids_out, pcv_out, vis_out, cut_out, m_out,
+               pool_ptr(kp, p, S.pool_cur), nhead, nlen, S.C, qmax, bl,
+               reinterpret_cast<long long*>(smem_tmp + 64),
+               reinterpret_cast<double*>(smem_tmp + 96), smem_tmp);
   }
   if (warp == 0) {
     if (flag & 2) {
@@ -1192,12 +1360,17 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
         e.capped = 1;
         RunQueue* q = kp.queues + next_queue;
         const int slot = atomicAdd(&q->len, 1);
+        if (slot >= kp.qcap) {
+          atomicOr(kp.err, 4);  // never: qcap covers every problem's share
+        } else {
         RunItem& it = kp.items[(size_t)next_queue * kp.qcap + slot];
         it.problem = p;
         it.pos = nhead;
         it.id = ids_out[nhead];
         it.front = 1;
         it.cap = sh_cap;
+        it.cut = S.C;
+        }
       }
     }
   }
@@ -1346,6 +1519,8 @@ __device__ void init_problem(const KParams& kp, int p) {
       e.has_best = 0;
       e.a_star = -1;
       list_vis(kp, p, 0)[0] = 0;
+      list_dbl(kp, p, 0, 0)[0] = -1.0;
+      list_dbl(kp, p, 0, 1)[0] = -1.0;
       list_arr(kp, p, 0, 0)[0] = 0;   // id
       list_arr(kp, p, 0, 1)[0] = -1;  // needs a run
       list_arr(kp, p, 0, 2)[0] = 1;
@@ -1357,6 +1532,7 @@ __device__ void init_problem(const KParams& kp, int p) {
       kp.items[slot].id = 0;
       kp.items[slot].front = 1;
       kp.items[slot].cap = kp.seg_cap;
+      kp.items[slot].cut = S.C;
     }
   }
   __syncthreads();
@@ -1405,6 +1581,7 @@ __global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
     kp.deadline_ns += now;  // relative budget -> absolute
     *kp.deadline_slot = kp.deadline_ns;
   }
+  if (kp.trace >= 4 && blockIdx.x == 0 && threadIdx.x == 0) kp.prof[11] = 4;  // per-decision trace
   for (int p = blockIdx.x; p < kp.n_problems; p += gridDim.x) init_problem(kp, p);
   gsync(kp.bar);
   kp.deadline_ns = *((volatile unsigned long long*)kp.deadline_slot);
@@ -1415,6 +1592,7 @@ __global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       kp.queues[cur ^ 1].len = 0;
       kp.queues[cur ^ 1].head = 0;
+      kp.active[6] = *((volatile int*)kp.active);  // active-count snapshot for the schedule
     }
     RunQueue* q = kp.queues + cur;
     RunItem* items = kp.items + (size_t)cur * kp.qcap;
@@ -1432,11 +1610,11 @@ __global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
       const GProb& P = kp.probs[p];
       GState& S = kp.states[p];
       Entry* E = pool_ptr(kp, p, S.pool_cur) + item.id;
-      const double C = S.C;
-      const int cver = S.cver;
+      const double C = item.cut;
+      const int cver = 1;
       const PView PV = stage_problem(P, wsm + warp, lane);
       RunOut o = run_segment(PV, E, E, C, item.cap, wsm + warp, lane, kp.err, kp.deadline_ns,
-                              kp.trace >= 2 ? kp.prof : nullptr);
+                              kp.trace >= 2 ? kp.prof : nullptr, kp.trace >= 3);
       int* pcv = list_arr(kp, p, S.cur, 1);
       int* cnt = list_arr(kp, p, S.cur, 2);
       int* pfirst = list_arr(kp, p, S.cur, 3);
@@ -1459,10 +1637,12 @@ __global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
         } else if (keep) {
           E->cver = cver;
           E->uncapped = 0;
-          pcv[item.pos] = cver;
+          pcv[item.pos] = 1;
           cnt[item.pos] = 1 + pieces;
           pfirst[item.pos] = first;
           list_vis(kp, p, S.cur)[item.pos] = o.visits;
+          list_dbl(kp, p, S.cur, 0)[item.pos] = C;
+          list_dbl(kp, p, S.cur, 1)[item.pos] = o.m;
         } else {
           E->cver = -1;
           E->finished = 0;
@@ -1490,7 +1670,7 @@ __global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
       }
     }
     gsync(kp.bar);
-    if (kp.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+    if (kp.trace && kp.trace_p < 0 && blockIdx.x == 0 && threadIdx.x == 0) {
       unsigned long long t_w2;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_w2));
       printf("[hpk] wave %d: %d runs, run %.1f us, schedule %.1f us (active %d)\n", wave, qlen,
@@ -1502,9 +1682,12 @@ __global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
   if (kp.trace >= 2 && blockIdx.x == 0 && threadIdx.x == 0) {
     const unsigned long long* q = kp.prof;
     printf("[hpk-prof] leaf batches %llu (leaves %llu): %.1f cyc/batch | child checks %llu: %.1f "
-           "cyc/check | descend %.1f cyc/check | pop total %llu cyc\n",
+           "cyc/check (to owner-done %.1f, shuffles %.1f) | descend %.1f cyc/check | pop total "
+           "%llu cyc\n",
            q[1], q[2], q[1] ? (double)q[0] / q[1] : 0.0, q[4], q[4] ? (double)q[3] / q[4] : 0.0,
+           q[4] ? (double)q[7] / q[4] : 0.0, q[4] ? (double)q[8] / q[4] : 0.0,
            q[4] ? (double)q[5] / q[4] : 0.0, q[6]);
+    printf("[hpk-prof] exact fallbacks %llu\n", q[9]);
   }
 }
 
@@ -1735,6 +1918,8 @@ struct DeviceCtx {
   int* lists = nullptr;
   long long* lvis = nullptr;
   size_t cap_lvis = 0;
+  double* ldbl = nullptr;
+  size_t cap_ldbl = 0;
   int* scratch = nullptr;
   RunQueue* queues = nullptr;
   RunItem* items = nullptr;
@@ -1853,6 +2038,27 @@ void reset() { t_timing = hpk_timing{}; }
 
 extern "C" {
 
+// Runs the device filter decision on n cases (A, D, cut triplets; rem = rm[2])
+// and writes the codes; used by the GPU tests to pin decide() (see its note).
+int hpk_selftest_decide(const double* cases, int n, const double* rm4, double mb_abs,
+                        double md_abs, int* out_codes) {
+  if (hpk_device_count() <= 0) return fail(5, "hetplan_b200: no CUDA device visible");
+  double *din, *drm;
+  int* dout;
+  HPK_CUDA(cudaMalloc(&din, sizeof(double) * 3 * (size_t)n));
+  HPK_CUDA(cudaMalloc(&drm, sizeof(double) * 4));
+  HPK_CUDA(cudaMalloc(&dout, sizeof(int) * (size_t)n));
+  HPK_CUDA(cudaMemcpy(din, cases, sizeof(double) * 3 * (size_t)n, cudaMemcpyHostToDevice));
+  HPK_CUDA(cudaMemcpy(drm, rm4, sizeof(double) * 4, cudaMemcpyHostToDevice));
+  hpk_selftest_decide_kernel<<<1, 32>>>(din, n, drm, mb_abs, md_abs, dout);
+  HPK_CUDA(cudaGetLastError());
+  HPK_CUDA(cudaMemcpy(out_codes, dout, sizeof(int) * (size_t)n, cudaMemcpyDeviceToHost));
+  cudaFree(din);
+  cudaFree(drm);
+  cudaFree(dout);
+  return 0;
+}
+
 const char* hpk_version(void) { return "hetplan-b200 0.1.0 (sm_100a)"; }
 const char* hpk_last_error(void) { return t_err.c_str(); }
 
@@ -1932,7 +2138,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     int lcap = cfg.max_list > 0 ? cfg.max_list : (1 << 16);
     int pcap = 2 * lcap;
     while (lcap > 4096 &&
-           (size_t)P * ((size_t)pcap * 2 * sizeof(Entry) + (size_t)lcap * 52) > ((size_t)4 << 30)) {
+           (size_t)P * ((size_t)pcap * 2 * sizeof(Entry) + (size_t)lcap * 84) > ((size_t)4 << 30)) {
       lcap /= 2;
       pcap /= 2;
     }
@@ -1963,6 +2169,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     if (int rc = grow(c.lists, c.cap_lists, (size_t)P * 2 * 4 * lcap)) return rc;
     if (int rc = grow(c.scratch, c.cap_scratch, (size_t)P * (lcap + 1))) return rc;
     if (int rc = grow(c.lvis, c.cap_lvis, (size_t)P * 2 * lcap)) return rc;
+    if (int rc = grow(c.ldbl, c.cap_ldbl, (size_t)P * 4 * lcap)) return rc;
     const int grid = c.sms * c.blocks_per_sm;
     const int nwarps = grid * WARPS_PER_BLOCK;
     const int qmax = 2 * nwarps;  // total run slots per wave, shared by active problems
@@ -1984,6 +2191,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     kp.pools = c.pools;
     kp.lists = c.lists;
     kp.lvis = c.lvis;
+    kp.ldbl = c.ldbl;
     kp.scratch = c.scratch;
     kp.queues = c.queues;
     kp.items = c.items;
@@ -2002,6 +2210,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     kp.bar = reinterpret_cast<unsigned int*>(c.active + 4);
     kp.prof = reinterpret_cast<unsigned long long*>(c.active + 8);
     kp.trace = getenv("HPK_TRACE") ? atoi(getenv("HPK_TRACE")) : 0;
+    kp.trace_p = getenv("HPK_TRACE_P") ? atoi(getenv("HPK_TRACE_P")) : -1;
     const size_t smem = sizeof(WarpSmem) * WARPS_PER_BLOCK + sizeof(int) * (BLOCK_THREADS + 8);
     void* args[] = {&kp};
     HPK_CUDA(cudaEventRecord(c.ev0, c.stream));
@@ -2018,6 +2227,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     HPK_CUDA(cudaStreamSynchronize(c.stream));
     if (flags_out[1] & 1) return fail(5, "hetplan_b200: segment runner watchdog tripped");
     if (flags_out[1] & 2) return fail(5, "hetplan_b200: wave engine exceeded its time budget");
+    if (flags_out[1] & 4) return fail(5, "hetplan_b200: run queue overflow (scheduler bug)");
     t_timing.d2h_bytes += sizeof(GState) * P;
     float ms = 0;
     HPK_CUDA(cudaEventElapsedTime(&ms, c.ev0, c.ev1));

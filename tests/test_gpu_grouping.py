@@ -107,3 +107,35 @@ def test_top_k_and_non_dyadic_take_the_serial_engine(engine, oracle):
     r = engine.grouping_search([pb])[0]
     o = oracle.solve_grouping(pb.power, pb.memory, 8, 6.0, pb.type_key, pb.node_key, top_k=3)
     assert r.engine == 1 and _same(r, o)
+
+
+def _host_decide(A, D, rem, cut, mb, md):
+    has_cut = cut >= 0
+    if (has_cut and A + mb < cut) or (D - md > rem):
+        return 1
+    b_pass = (not has_cut) or (A - mb >= cut)
+    return 0 if (b_pass and D + md <= rem) else 2
+
+
+def test_device_filter_decision_matches_host(engine):
+    """Pins decide(): an equivalent if/else-chain formulation was miscompiled
+    by nvcc 12.9 for sm_100a (never returned PASS) — DESIGN.md 2.3."""
+    import ctypes as C
+    rm = [0.0, 0.0, 100.0, 0.0]
+    cases = []
+    for A in (10.0, 50.0, 50.0 + 1e-12, 90.0):
+        for D in (50.0, 100.0, 100.0 + 1e-12, 150.0):
+            for cut in (-1.0, 0.0, 50.0, 60.0):
+                cases.append((A, D, cut))
+    flat = [v for c in cases for v in c]
+    lib = engine.lib
+    lib.hpk_selftest_decide.argtypes = [C.POINTER(C.c_double), C.c_int, C.POINTER(C.c_double),
+                                        C.c_double, C.c_double, C.POINTER(C.c_int)]
+    for mb in (0.0, 1e-9):
+        for md in (0.0, 1e-9):
+            out = (C.c_int * len(cases))()
+            rc = lib.hpk_selftest_decide((C.c_double * len(flat))(*flat), len(cases),
+                                         (C.c_double * 4)(*rm), mb, md, out)
+            assert rc == 0
+            want = [_host_decide(A, D, 100.0, cut, mb, md) for (A, D, cut) in cases]
+            assert list(out) == want
