@@ -898,17 +898,25 @@ __device__ int split_run(const KParams& kp, int p, GState& S, Entry* E, const Ru
   return count;
 }
 
-// Block-wide exclusive scan of a[0..len) in place over coalesced tiles of
-// blockDim.x elements (warp shuffles + one smem round per tile); returns the total.
+// Block-wide exclusive scan of src[0..len) into dst (may alias) over tiles of
+// blockDim.x * 8 elements: each thread owns 8 consecutive elements, so every
+// thread keeps 8 independent loads in flight (the scheduler's passes are
+// latency-bound on L2); warp shuffles + one smem round per tile. Returns the total.
 template <typename T>
-__device__ T block_scan_tiles(T* a, int len, T* sh) {
+__device__ T block_scan8(const T* src, T* dst, int len, T* sh) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nw = blockDim.x >> 5;
   T carry = 0;
-  for (int base = 0; base < len; base += blockDim.x) {
-    const int i = base + tid;
-    const T v = i < len ? a[i] : (T)0;
-    T x = v;
+  for (int base = 0; base < len; base += blockDim.x * 8) {
+    const int i0 = base + tid * 8;
+    T v[8];
+    T sum = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      v[k] = i0 + k < len ? src[i0 + k] : (T)0;
+      sum += v[k];
+    }
+    T x = sum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const T t = __shfl_up_sync(HPK_FULL_MASK, x, o);
@@ -926,8 +934,12 @@ __device__ T block_scan_tiles(T* a, int len, T* sh) {
       if (lane < nw) sh[lane] = w;
     }
     __syncthreads();
-    const T woff = warp == 0 ? (T)0 : sh[warp - 1];
-    if (i < len) a[i] = carry + woff + x - v;
+    T run = carry + (warp == 0 ? (T)0 : sh[warp - 1]) + x - sum;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (i0 + k < len) dst[i0 + k] = run;
+      run += v[k];
+    }
     carry += sh[nw - 1];
     __syncthreads();
   }
@@ -947,100 +959,136 @@ __device__ void finish_problem(const KParams& kp, GState& S) {
 // Positions provably past the budget's abort point are never queued: the
 // visits of the exact runs before them (others count 1, a lower bound — a
 // higher cutoff only prunes more) already exhaust the budget.
+template <typename T, typename Op>
+__device__ __forceinline__ T block_excl_scan_1(T x, T ident, T* sh, Op op, T* total) {
+  // exclusive scan of one value per thread (thread order), returns the prefix
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nw = blockDim.x >> 5;
+  T inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const T t = __shfl_up_sync(HPK_FULL_MASK, inc, o);
+    if (lane >= o) inc = op(inc, t);
+  }
+  if (lane == 31) sh[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    T w = lane < nw ? sh[lane] : ident;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const T t = __shfl_up_sync(HPK_FULL_MASK, w, o);
+      if (lane >= o) w = op(w, t);
+    }
+    if (lane < nw) sh[lane] = w;
+  }
+  __syncthreads();
+  T ex = __shfl_up_sync(HPK_FULL_MASK, inc, 1);
+  if (lane == 0) ex = ident;
+  if (warp > 0) ex = op(sh[warp - 1], ex);
+  *total = sh[nw - 1];
+  __syncthreads();
+  return ex;
+}
+
+struct OpMax {
+  __device__ double operator()(double a, double b) const { return a > b ? a : b; }
+};
+struct OpAddL {
+  __device__ long long operator()(long long a, long long b) const { return a + b; }
+};
+struct OpAddI {
+  __device__ int operator()(int a, int b) const { return a + b; }
+};
+
 __device__ void push_items(const KParams& kp, int queue, int p, const int* ids, const int* pran,
                            const long long* pvis, const double* pcut, const double* pm,
                            const Entry* pool, int head, int len, double C, int qmax,
                            long long budget_left, long long* shl, double* shd, int* shi) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nw = blockDim.x >> 5;
+  const int tid = threadIdx.x;
   RunQueue* q = kp.queues + queue;
   RunItem* items = kp.items + (size_t)queue * kp.qcap;
   long long before = 0;  // lower bound of visits before the tile
   double cmax = C;       // predicted cutoff entering the tile
   int pushed = 0;
-  for (int base = 0; base < len; base += blockDim.x) {
-    const int j = base + tid;
-    const bool inl = j < len;
-    const bool ran = inl && pran[head + j] == 1;
-    const double mj = ran ? pm[head + j] : -1.0;
-    // exclusive prefix max of m within the tile -> predicted cutoff
-    double xm = mj;
+  for (int base = 0; base < len; base += blockDim.x * 8) {
+    const int j0 = base + tid * 8;  // this thread's 8 consecutive positions
+    bool ran[8];
+    double mj[8], cj[8];
+    long long vj[8];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const double t = __shfl_up_sync(HPK_FULL_MASK, xm, o);
-      if (lane >= o) xm = t > xm ? t : xm;
+    for (int k = 0; k < 8; ++k) {
+      const int j = j0 + k;
+      ran[k] = j < len && pran[head + j] == 1;
+      mj[k] = ran[k] ? pm[head + j] : -1.0;
+      cj[k] = ran[k] ? pcut[head + j] : -2.0;
+      vj[k] = ran[k] ? pvis[head + j] : 0;
     }
-    double ex = __shfl_up_sync(HPK_FULL_MASK, xm, 1);
-    if (lane == 0) ex = -1.0;
-    if (lane == 31) shd[warp] = xm;
-    __syncthreads();
-    if (warp == 0) {
-      double w = lane < nw ? shd[lane] : -1.0;
+    double tmax = -1.0;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const double t = __shfl_up_sync(HPK_FULL_MASK, w, o);
-        if (lane >= o) w = t > w ? t : w;
+    for (int k = 0; k < 8; ++k) tmax = mj[k] > tmax ? mj[k] : tmax;
+    double tile_max;
+    const double exm = block_excl_scan_1<double>(tmax, -1.0, shd, OpMax(), &tile_max);
+    double chat[8];
+    bool need[8];
+    long long vsum = 0;
+    {
+      double run = cmax > exm ? cmax : exm;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        chat[k] = run;
+        run = mj[k] > run ? mj[k] : run;
+        const bool exact = ran[k] && cj[k] == chat[k];
+        vj[k] = (j0 + k < len) ? (exact ? vj[k] : 1) : 0;
+        need[k] = (j0 + k < len) && !exact;
+        vsum += vj[k];
       }
-      if (lane < nw) shd[lane] = w;
     }
-    __syncthreads();
-    double chat = cmax;
-    if (warp > 0) chat = shd[warp - 1] > chat ? shd[warp - 1] : chat;
-    chat = ex > chat ? ex : chat;
-    const bool exact = ran && pcut[head + j] == chat;
-    const long long v = inl ? (exact ? pvis[head + j] : 1) : 0;
-    // exclusive visit prefix within the tile
-    long long x = v;
+    long long tile_vis;
+    const long long exv = block_excl_scan_1<long long>(vsum, 0, shl, OpAddL(), &tile_vis);
+    int nneed = 0;
+    {
+      long long run = before + exv;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const long long t = __shfl_up_sync(HPK_FULL_MASK, x, o);
-      if (lane >= o) x += t;
-    }
-    if (lane == 31) shl[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-      long long w = lane < nw ? shl[lane] : 0;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const long long t = __shfl_up_sync(HPK_FULL_MASK, w, o);
-        if (lane >= o) w += t;
+      for (int k = 0; k < 8; ++k) {
+        need[k] = need[k] && (budget_left < 0 || run < budget_left);
+        run += vj[k];
+        nneed += need[k] ? 1 : 0;
       }
-      if (lane < nw) shl[lane] = w;
     }
-    __syncthreads();
-    const long long excl = before + (warp == 0 ? 0 : shl[warp - 1]) + x - v;
-    const bool need = inl && !exact && (budget_left < 0 || excl < budget_left);
-    const unsigned bal = __ballot_sync(HPK_FULL_MASK, need);
-    if (lane == 0) shi[warp] = __popc(bal);
-    __syncthreads();
+    int tile_need;
+    const int exn = block_excl_scan_1<int>(nneed, 0, shi, OpAddI(), &tile_need);
     if (tid == 0) {
-      int run = 0;
-      for (int w = 0; w < nw; ++w) {
-        const int c = shi[w];
-        shi[w] = run;
-        run += c;
-      }
-      int take = min(run, qmax - pushed);
-      shi[nw] = take;
-      shi[nw + 1] = take > 0 ? atomicAdd(&q->len, take) : 0;
+      const int take = min(tile_need, qmax - pushed);
+      shi[40] = take;
+      shi[41] = take > 0 ? atomicAdd(&q->len, take) : 0;
     }
     __syncthreads();
-    const int take = shi[nw], slot0 = shi[nw + 1];
-    const int rank = shi[warp] + __popc(bal & ((1u << lane) - 1));
-    if (need && rank < take && slot0 + rank >= kp.qcap) atomicOr(kp.err, 4);  // must not happen
-    if (need && rank < take && slot0 + rank < kp.qcap) {
-      RunItem& it = items[slot0 + rank];
-      const int id = ids[head + j];
-      it.problem = p;
-      it.pos = head + j;
-      it.id = id;
-      it.front = (j == 0);
-      it.cap = pool[id].uncapped ? 0x3fffffffffffffffLL : kp.seg_cap;
-      it.cut = chat;
+    const int take = shi[40], slot0 = shi[41];
+    int rank = exn;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (need[k]) {
+        if (rank < take) {
+          if (slot0 + rank >= kp.qcap) {
+            atomicOr(kp.err, 4);  // must not happen
+          } else {
+            const int j = j0 + k;
+            RunItem& it = items[slot0 + rank];
+            const int id = ids[head + j];
+            it.problem = p;
+            it.pos = head + j;
+            it.id = id;
+            it.front = (j == 0);
+            it.cap = pool[id].uncapped ? 0x3fffffffffffffffLL : kp.seg_cap;
+            it.cut = chat[k];
+          }
+        }
+        ++rank;
+      }
     }
     pushed += take;
-    before += shl[nw - 1];
-    cmax = shd[nw - 1] > cmax ? shd[nw - 1] : cmax;
+    before += tile_vis;
+    cmax = tile_max > cmax ? tile_max : cmax;
     __syncthreads();
     if (pushed >= qmax || (budget_left >= 0 && before >= budget_left)) break;
   }
@@ -1089,11 +1137,11 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
     return;
   }
 
+  unsigned long long _tprev = 0;
+  if (kp.trace >= 5 && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_tprev));
   // ---- A. expand the splits made by this wave's runs (cnt = 1 + pieces)
   int* off = kp.scratch + (size_t)p * (kp.lcap + 1);
-  for (int i = tid; i < len; i += blockDim.x) off[i] = cnt_in[head + i];
-  __syncthreads();
-  int total = block_scan_tiles<int>(off, len, smem_tmp);
+  int total = block_scan8<int>(cnt_in + head, off, len, smem_tmp);
   if (total > kp.lcap - kp.reserve) {
     // List nearly full: keep expansions in list order while they leave the
     // head's reserve free; the others are reverted to unrun FULL segments
@@ -1121,11 +1169,12 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
       }
     }
     __syncthreads();
-    total = block_scan_tiles<int>(off, len, smem_tmp);
+    total = block_scan8<int>(off, off, len, smem_tmp);
   }
   if (tid == 0) off[len] = total;
   __syncthreads();
-  for (int i = tid; i < len; i += blockDim.x) {  // scatter from the input side
+  for (int i0 = tid * 8; i0 < len; i0 += blockDim.x * 8)  // scatter from the input side,
+  for (int i = i0; i < i0 + 8 && i < len; ++i) {            // 8 consecutive inputs per thread
     const int o = off[i];
     const int c = off[i + 1] - o;
     ids_out[o] = ids_in[head + i];
@@ -1148,6 +1197,12 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
   }
   __syncthreads();
 
+  if (kp.trace >= 5 && tid == 0) {
+    unsigned long long _t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));
+    atomicAdd(kp.prof + 12, _t - _tprev);
+    _tprev = _t;
+  }
   // ---- B. ordered commit walk (warp 0)
   __shared__ int sh_head, sh_flag;
   __shared__ long long sh_cap;
@@ -1277,7 +1332,7 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
       if (kc < 32) break;  // reached a position that still needs a run
     }
     if (lane == 0) {
-      if (kp.trace && (kp.trace_p < 0 || kp.trace_p == p) && S.waves < 200000)
+      if (kp.trace && kp.trace < 5 && (kp.trace_p < 0 || kp.trace_p == p) && S.waves < 200000)
         printf("[hpk] wave %d p %d len %d total %d commit %d V %lld C %.17g pool %d head-pcv %d "
                "head-cut %.17g head-uncapped %d\n",
                S.waves, p, len, total, i, V, C, S.pool_top, total > i ? pcv_out[i] : -9,
@@ -1307,6 +1362,12 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
     }
   }
   __syncthreads();
+  if (kp.trace >= 5 && tid == 0) {
+    unsigned long long _t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));
+    atomicAdd(kp.prof + 13, _t - _tprev);
+    _tprev = _t;
+  }
   const int flag = sh_flag;
   int nhead = sh_head;
   const int nlen = total - nhead;
@@ -1339,6 +1400,12 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
     }
     nhead = 0;
     __syncthreads();
+  }
+  if (kp.trace >= 5 && tid == 0) {
+    unsigned long long _t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));
+    atomicAdd(kp.prof + 14, _t - _tprev);
+    _tprev = _t;
   }
   // ---- D. queue the next wave
   if (!(flag & 2) && (flag & 1)) {
@@ -1375,6 +1442,12 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
     }
   }
   __syncthreads();
+  if (kp.trace >= 5 && tid == 0) {
+    unsigned long long _t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));
+    atomicAdd(kp.prof + 15, _t - _tprev);
+    _tprev = _t;
+  }
 }
 
 // ---------------------------------------------------------------- init
@@ -1614,7 +1687,8 @@ __global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
       const int cver = 1;
       const PView PV = stage_problem(P, wsm + warp, lane);
       RunOut o = run_segment(PV, E, E, C, item.cap, wsm + warp, lane, kp.err, kp.deadline_ns,
-                              kp.trace >= 2 ? kp.prof : nullptr, kp.trace >= 3);
+                              (kp.trace >= 2 && kp.trace < 5) ? kp.prof : nullptr,
+                              kp.trace == 3);
       int* pcv = list_arr(kp, p, S.cur, 1);
       int* cnt = list_arr(kp, p, S.cur, 2);
       int* pfirst = list_arr(kp, p, S.cur, 3);
@@ -1670,7 +1744,13 @@ __global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
       }
     }
     gsync(kp.bar);
-    if (kp.trace && kp.trace_p < 0 && blockIdx.x == 0 && threadIdx.x == 0) {
+    if (kp.trace >= 5 && blockIdx.x == 0 && threadIdx.x == 0) {
+      unsigned long long t_w2;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_w2));
+      atomicAdd(kp.prof + 16, t_w1 - t_w0);
+      atomicAdd(kp.prof + 17, t_w2 - t_w1);
+    }
+    if (kp.trace && kp.trace < 5 && kp.trace_p < 0 && blockIdx.x == 0 && threadIdx.x == 0) {
       unsigned long long t_w2;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_w2));
       printf("[hpk] wave %d: %d runs, run %.1f us, schedule %.1f us (active %d)\n", wave, qlen,
@@ -1679,7 +1759,13 @@ __global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
     if (*((volatile int*)kp.active) <= 0) break;
     cur ^= 1;
   }
-  if (kp.trace >= 2 && blockIdx.x == 0 && threadIdx.x == 0) {
+  if (kp.trace >= 5 && blockIdx.x == 0 && threadIdx.x == 0) {
+    const unsigned long long* q = kp.prof;
+    printf("[hpk-sched] totals over all waves/problems (us): expand+scatter %.1f commit %.1f "
+           "compaction %.1f push %.1f | run phases %.1f schedule phases %.1f\n", q[12] * 1e-3,
+           q[13] * 1e-3, q[14] * 1e-3, q[15] * 1e-3, q[16] * 1e-3, q[17] * 1e-3);
+  }
+  if (kp.trace >= 2 && kp.trace < 5 && blockIdx.x == 0 && threadIdx.x == 0) {
     const unsigned long long* q = kp.prof;
     printf("[hpk-prof] leaf batches %llu (leaves %llu): %.1f cyc/batch | child checks %llu: %.1f "
            "cyc/check (to owner-done %.1f, shuffles %.1f) | descend %.1f cyc/check | pop total "
@@ -2131,7 +2217,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
   // ---------------- wave engine
   if (!wave_ix.empty()) {
     const int P = (int)wave_ix.size();
-    const long long seg_cap = cfg.segment_cap > 0 ? cfg.segment_cap : 2048;
+    const long long seg_cap = cfg.segment_cap > 0 ? cfg.segment_cap : 1024;
     // list capacity (ids) and entry-pool capacity per problem; large by default
     // (the list must hold the whole speculative frontier), scaled down so that
     // big batches (cfg5 sweeps) stay within ~4 GB of HBM.
