@@ -160,6 +160,7 @@ typedef struct hpk_grouping_result {
   long long segment_runs;
   long long segment_visits;          /* visits executed incl. speculation */
   int max_list;
+  long long exact_checks;            /* child checks inside the filter margin (exact path) */
 } hpk_grouping_result;
 
 typedef struct hpk_search_config {

@@ -44,6 +44,7 @@ namespace hpk {
 constexpr int MAXN = HPK_MAX_UNITS;  // 64 units -> lanes own groups g and g+32
 constexpr int WARPS_PER_BLOCK = 8;
 constexpr int BLOCK_THREADS = WARPS_PER_BLOCK * 32;
+constexpr int TILE = BLOCK_THREADS * 8;  // list positions per expansion / commit tile
 constexpr uint8_t KIND_FULL = 0;
 constexpr uint8_t KIND_PREFIX = 1;
 
@@ -91,7 +92,7 @@ struct GState {
   long long rerun_cap;
   double seed_obj, seed_z;
   int seed_ix, waves;
-  long long runs, run_visits;
+  long long runs, run_visits, exact_checks;
   int max_list, error;
   uint8_t best_rgs[MAXN];
   uint8_t seed_rgs[MAXN];
@@ -112,14 +113,21 @@ struct KParams {
   GProb* probs;
   GState* states;
   Entry* pools;       // [P][2][pcap]
-  int* lists;         // [P][2][4][lcap]: ids, pcver, cnt, pfirst
+  int* lists;         // [P][2][5][lcap]: ids, pcver, cnt, pfirst, info
   long long* lvis;    // [P][2][lcap]: visits of the finished run at each position
-  double* ldbl;       // [P][2][2][lcap]: cutoff the run at each position used, its max objective
+  double* ldbl;       // [P][2][3][lcap]: cutoff the run at each position used, its max
+                      // objective, its best objective
   int* scratch;       // [P][lcap + 1]
+  int* xt;            // [P][xtn]: pieces added by this wave's splits, per list tile
+  int2* work;         // [2][wcap]: expansion work items (problem, tile) per wave parity
+  int* wcount;        // [2]
+  int xtn, wcap;
   RunQueue* queues;   // [2]
   RunItem* items;     // [2][qcap]
   int* active;        // problems still running
   int* err;           // watchdog flags
+  int* stop;          // run phase: the queue has drained (capped runs stop early)
+  long long minq;     // ... after at least this many visits (0: never stop early)
   int n_problems;
   int lcap, pcap, qcap, qmax, reserve;
   long long seg_cap;
@@ -135,18 +143,32 @@ struct KParams {
 __device__ __forceinline__ Entry* pool_ptr(const KParams& kp, int p, int which) {
   return kp.pools + ((size_t)p * 2 + which) * kp.pcap;
 }
-// list arrays of buffer `buf`: 0 ids, 1 pcver (cutoff version of a finished
-// run at this position, -1 = needs a run), 2 cnt (expansion count), 3 pfirst
+// list arrays of buffer `buf`: 0 ids, 1 pcver (1 = a finished run at this
+// position, -1 = needs a run), 2 cnt (expansion count), 3 pfirst, 4 info (the
+// run's best_G | 256 has_best | 512 PREFIX re-run that pruned an ancestor)
 __device__ __forceinline__ int* list_arr(const KParams& kp, int p, int buf, int which) {
-  return kp.lists + (((size_t)p * 2 + buf) * 4 + which) * kp.lcap;
+  return kp.lists + (((size_t)p * 2 + buf) * 5 + which) * kp.lcap;
 }
 __device__ __forceinline__ long long* list_vis(const KParams& kp, int p, int buf) {
   return kp.lvis + ((size_t)p * 2 + buf) * kp.lcap;
 }
-// which: 0 = cutoff used by the run at the position, 1 = its max leaf objective
+// which: 0 = cutoff used by the run at the position, 1 = its max leaf
+// objective, 2 = its best objective
 __device__ __forceinline__ double* list_dbl(const KParams& kp, int p, int buf, int which) {
-  return kp.ldbl + (((size_t)p * 2 + buf) * 2 + which) * kp.lcap;
+  return kp.ldbl + (((size_t)p * 2 + buf) * 3 + which) * kp.lcap;
 }
+
+// scheduler CTA scratch (dynamic smem after the warps' DFS stacks)
+struct SchedSmem {
+  long long l[32];
+  double d[32];
+  int i[64];
+  double bo[32];
+  int bg[32], bi[32];
+  long long v_after, v_before, cap;
+  double c_after, c_before;
+  int fb, fs, sp_del, ndel, head, flag;
+};
 
 // --------------------------------------------------------------- warp DFS
 
@@ -158,9 +180,8 @@ struct WarpSmem {
   unsigned long long mpass[MAXN + 1];   // per level: children that pass the check
   unsigned long long mprune[MAXN + 1];  // per level: children that are pruned
   double mcut[MAXN + 1];                // cutoff the masks were computed with
+  unsigned lvl[MAXN + 1];  // per level: path | next child << 8 | G << 16
   uint8_t path[MAXN];
-  uint8_t nxt[MAXN + 1];
-  uint8_t Gat[MAXN + 1];
   uint8_t endp[MAXN];
   uint8_t best[MAXN];
 };
@@ -208,6 +229,10 @@ constexpr double kEps52 = 2.220446049250313e-16;  // 2^-52
 
 // Per-lane group registers: lane owns groups lane and lane+32; f0/f1 cache the
 // Eq. (2) factors for the current member count and for one more member.
+// Updates are branch-free: every lane executes them, the owner's select is
+// taken. Under the wave engine's contract every sum is exact, so x + 0.0,
+// 0.0 + up (push_back) and up - up (pop_back) equal the reference's values
+// (grouping.cpp:180-198) bit for bit.
 struct Groups {
   double gp[2], gm[2], f0[2], f1[2];
   int gc[2];
@@ -215,47 +240,29 @@ struct Groups {
 
 __device__ __forceinline__ void add_unit(const PView& P, Groups& g, int lane, int grp, double up,
                                          double um) {
-  if ((grp & 31) == lane) {
-    const int s = grp >> 5;
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      if (k == s) {
-        if (g.gc[k] == 0) {  // new group: push_back (grouping.cpp:180-182)
-          g.gp[k] = up;
-          g.gm[k] = um;
-          g.gc[k] = 1;
-        } else {             // += (grouping.cpp:184-186)
-          g.gp[k] += up;
-          g.gm[k] += um;
-          g.gc[k] += 1;
-        }
-        g.f0[k] = g.f1[k];
-        g.f1[k] = P.f[g.gc[k] + 1];
-      }
-    }
+  for (int k = 0; k < 2; ++k) {
+    const bool o = grp == lane + 32 * k;
+    g.gp[k] += o ? up : 0.0;
+    g.gm[k] += o ? um : 0.0;
+    g.gc[k] += o ? 1 : 0;
+    const double fn = P.f[g.gc[k] + 1];
+    g.f0[k] = o ? g.f1[k] : g.f0[k];
+    g.f1[k] = o ? fn : g.f1[k];
   }
 }
 
 __device__ __forceinline__ void remove_unit(const PView& P, Groups& g, int lane, int grp,
                                             double up, double um) {
-  if ((grp & 31) == lane) {
-    const int s = grp >> 5;
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      if (k == s) {
-        if (g.gc[k] == 1) {  // pop_back (grouping.cpp:192-194)
-          g.gp[k] = 0;
-          g.gm[k] = 0;
-          g.gc[k] = 0;
-        } else {             // -= (grouping.cpp:196-198); exact under the contract
-          g.gp[k] -= up;
-          g.gm[k] -= um;
-          g.gc[k] -= 1;
-        }
-        g.f1[k] = g.f0[k];
-        g.f0[k] = P.f[g.gc[k]];
-      }
-    }
+  for (int k = 0; k < 2; ++k) {
+    const bool o = grp == lane + 32 * k;
+    g.gp[k] -= o ? up : 0.0;
+    g.gm[k] -= o ? um : 0.0;
+    g.gc[k] -= o ? 1 : 0;
+    const double fp = P.f[g.gc[k]];
+    g.f1[k] = o ? g.f0[k] : g.f1[k];
+    g.f0[k] = o ? fp : g.f0[k];
   }
 }
 
@@ -270,16 +277,15 @@ __device__ __forceinline__ void groups_init(const PView& P, Groups& g) {
   }
 }
 
-// eff of this lane's slot k (0 if the group does not exist); f0 = f[gc] is the
-// reference's (1 - rho) for the group (grouping.cpp:103-108)
+// eff of this lane's slot k: f0 = f[gc] is the reference's (1 - rho) for the
+// group (grouping.cpp:103-108); an empty slot has gp = 0 and f[0] = 0.
 __device__ __forceinline__ double slot_eff(const PView& P, const Groups& g, int k) {
   (void)P;
-  return g.gc[k] > 0 ? g.gp[k] * g.f0[k] : 0.0;
+  return g.gp[k] * g.f0[k];
 }
 __device__ __forceinline__ double slot_def(const PView& P, const Groups& g, int k) {
-  if (g.gc[k] == 0) return 0.0;
   const double d = P.min_mem - g.gm[k];
-  return d > 0.0 ? d : 0.0;  // std::max(0.0, d)
+  return (g.gc[k] > 0 && d > 0.0) ? d : 0.0;  // std::max(0.0, d) over existing groups
 }
 
 // Exact node check in the reference's serial order (grouping.cpp:154-169) for
@@ -349,50 +355,49 @@ struct RunOut {
   double best_obj;
   int best_G, a_star;
   int dstop;   // unfinished: the stop node is path[0..dstop-1) + [stop_c]
+  int exact;   // child checks resolved by the exact serial check
   int stop_c;
 };
 
 // DFS of subtree(E.u) in preorder (PREFIX: stopping before E.end), cap visits.
+//
+// The current level's state — next child c, group count G, the approximate
+// level sums Sd/Dd, the unit (up, um) its children assign, the children's
+// pass/prune bitmasks and the cutoff they were computed with — is held in
+// warp-uniform registers. A level is spilled to the per-warp smem stack only
+// when the DFS descends below it and reloaded when it pops back, so a child
+// check is register-only. A run of children the masks prune is consumed in
+// O(1): each still counts one visit (grouping.cpp:178, the check happens on
+// entry :161-169) and none is entered.
+//
+// stopf (optional): set once the wave's run queue has drained; a capped run
+// then stops at its next check after >= minq visits and is split like a run
+// that hit its cap, so no warp idles behind the wave's longest run.
 __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, double C,
                               long long cap, WarpSmem* sm, int lane, int* err,
                               unsigned long long deadline, unsigned long long* prof,
-                              bool dbg) {
-  // prof (trace >= 2): [0] leaf-batch cycles [1] batches [2] leaves
-  //                    [3] child-check cycles [4] checks [5] descend cycles [6] pop cycles
+                              const int* stopf, long long minq) {
+  // prof (trace >= 2): [0] run cycles [1] leaf batches [2] leaves [3] loop iterations
+  //   [4] single checks [5] descends [6] pops [7] prune skips [8] children skipped
+  //   [9] exact fallbacks [10] mask computations
   long long pc0 = 0;
+  unsigned long long pcnt[11];  // per-warp counters, flushed once per run (no atomics in the loop)
+#pragma unroll
+  for (int k = 0; k < 11; ++k) pcnt[k] = 0;
+#ifdef HPK_RUNNER_PROF  // per-warp counters (trace >= 2), compiled out by default
+#define HPK_PC(k, v) \
+  do {               \
+    if (prof) pcnt[k] += (v); \
+  } while (0)
+#else
+#define HPK_PC(k, v) \
+  do {               \
+  } while (0)
+#endif
+  if (prof) pc0 = clock64();
   const int n = P.n;
   const int du = E->du;
   const bool prefix = E->kind == KIND_PREFIX;
-  if (cap <= 0) {  // budget already exhausted: the reference aborts before entering u
-    RunOut z;
-    z.visits = 0;
-    z.m = -1.0;
-    z.finished = false;
-    z.has_best = false;
-    z.best_obj = 0;
-    z.best_G = 0;
-    z.a_star = -1;
-    z.dstop = 0;
-    z.stop_c = 0;
-    return z;
-  }
-  const int dend = prefix ? E->dend : 0;
-  for (int i = lane; i < du; i += 32) sm->path[i] = E->u[i];
-  if (prefix)
-    for (int i = lane; i < dend; i += 32) sm->endp[i] = E->end[i];
-  __syncwarp();
-
-  Groups g;
-  groups_init(P, g);
-  int G = 0;
-  if (lane == 0) sm->Gat[0] = 0;
-  for (int i = 0; i + 1 < du; ++i) {
-    const int grp = sm->path[i];
-    add_unit(P, g, lane, grp, P.p[i], P.m[i]);
-    if (grp == G) ++G;
-    if (lane == 0) sm->Gat[i + 1] = (uint8_t)G;
-  }
-  __syncwarp();
   RunOut o;
   o.visits = 0;
   o.m = -1.0;
@@ -403,23 +408,36 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
   o.a_star = -1;
   o.dstop = 0;
   o.stop_c = 0;
-  double cut = C;
-  int match = prefix ? du : -1;
-  long long iters = 0;
-  // watchdog (never hit when correct): each iteration visits, pops or batches
-  const long long max_iters = cap > (1LL << 40) ? (1LL << 62) : 4 * cap + 4 * MAXN + 64;
+  o.exact = 0;
+  if (cap <= 0) return o;  // budget already exhausted: the reference aborts before entering u
+  const int dend = prefix ? E->dend : 0;
+  for (int i = lane; i < du; i += 32) sm->path[i] = E->u[i];
+  if (prefix)
+    for (int i = lane; i < dend; i += 32) sm->endp[i] = E->end[i];
+  __syncwarp();
 
-  // Enter the segment root u.
-  {
+  Groups g;
+  groups_init(P, g);
+  int G = 0;
+  if (lane == 0) sm->lvl[0] = 0;
+  for (int i = 0; i + 1 < du; ++i) {
+    const int grp = sm->path[i];
+    add_unit(P, g, lane, grp, P.p[i], P.m[i]);
+    if (grp == G) ++G;
+    if (lane == 0) sm->lvl[i + 1] = (unsigned)G << 16;
+  }
+  {  // enter the segment root u
     const int i = du - 1;
     const int grp = sm->path[i];
     add_unit(P, g, lane, grp, P.p[i], P.m[i]);
     if (grp == G) ++G;
-    if (lane == 0) sm->Gat[du] = (uint8_t)G;
-    __syncwarp();
+    if (lane == 0) sm->lvl[du] = (unsigned)G << 16;
     o.visits = 1;
   }
+  __syncwarp();
   int d = du;
+  double cut = C;
+  double Sd, Dd;
   if (d == n) {  // the root is a leaf (grouping.cpp:138-149)
     bool infeas = false;
     double z = INFINITY;
@@ -447,371 +465,329 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
   {  // node check of u itself
     double le = slot_eff(P, g, 0) + slot_eff(P, g, 1);
     double ld = slot_def(P, g, 0) + slot_def(P, g, 1);
-    const double S = warp_sum_approx(le);
-    const double DEF = warp_sum_approx(ld);
-    const double A = S + P.R[d];
-    int dec = decide(P, A, DEF, d, cut);
+    Sd = warp_sum_approx(le);
+    Dd = warp_sum_approx(ld);
+    int dec = decide(P, Sd + P.R[d], Dd, d, cut);
     if (dec == DEC_EXACT) dec = exact_passes(P, g, G, d, cut) ? DEC_PASS : DEC_PRUNE;
     if (dec == DEC_PRUNE) {
       if (prefix) o.a_star = du;
       o.finished = true;
       goto done;
     }
-    if (lane == 0) {
-      sm->S[d] = S;
-      sm->DEF[d] = DEF;
-      sm->nxt[d] = 0;
-      sm->mcut[d] = __longlong_as_double(0x7ff8000000000000LL);  // NaN: masks invalid
-    }
-    __syncwarp();
   }
+  {
+    const double kNaN = __longlong_as_double(0x7ff8000000000000LL);
+    const double mm_ = P.min_mem, mb = P.mb_abs, md = P.md_abs;
+    int c = 0;                        // next child of the current node
+    double up = P.p[d], um = P.m[d];  // unit d: assigned by the children
+    unsigned long long mp = 0, mr = 0;
+    double mc = kNaN;                 // cutoff of mp/mr (NaN: not computed)
+    double lS[2] = {0, 0}, lD[2] = {0, 0};  // this lane's children's level sums
+    bool sums_ok = false;             // lS/lD belong to the current node
+    int match = prefix ? du : -1;     // path == end marker on levels < match
+    int ec = (prefix && du < dend) ? sm->endp[du] : -1;  // end child at level `match`
+    unsigned it = 0;
+    int stop_pending = 0;  // stop flag loaded 32 iterations ago (latency off the chain)
 
-  while (true) {
-    if (++iters > max_iters) {
-      if (lane == 0) atomicOr(err, 1);
-      o.finished = true;
-      break;
-    }
-    if ((iters & 1023) == 0) {  // wall-clock watchdog (uniform: lane 0's clock)
-      unsigned long long now;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-      now = __shfl_sync(HPK_FULL_MASK, now, 0);
-      if (now > deadline) {
-        if (lane == 0) atomicOr(err, 2);
-        o.finished = true;
-        break;
-      }
-    }
-    if (d == n - 1) {
-      // ---- leaf batch: children c = c0..G are leaves (unit n-1) ----
-      if (prof) pc0 = clock64();
-      const int c0 = sm->nxt[d];
-      int count = G + 1 - c0;
-      bool end_hit = false;
-      if (prefix && match == d) {
-        const int ec = sm->endp[d];  // dend == n here
-        if (ec - c0 < count) {
-          count = ec - c0 > 0 ? ec - c0 : 0;
-          end_hit = true;
-        }
-      }
-      bool cap_hit = false;
-      if ((long long)count > cap - o.visits) {
-        count = (int)(cap - o.visits);
-        cap_hit = true;
-        end_hit = false;
-      }
-      if (count > 0) {
-        const double up = P.p[n - 1], um = P.m[n - 1];
-        bool inf_k[2];
-        double eff_k[2];
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          const bool valid = g.gc[k] > 0;
-          inf_k[k] = valid && g.gm[k] < P.min_mem;
-          eff_k[k] = valid ? slot_eff(P, g, k) : INFINITY;
-        }
-        const int n_inf = __popc(__ballot_sync(HPK_FULL_MASK, inf_k[0])) +
-                          __popc(__ballot_sync(HPK_FULL_MASK, inf_k[1]));
-        // min1 / idx1 / min2 over existing groups
-        double m1, m2;
-        int i1;
-        if (eff_k[0] <= eff_k[1]) {
-          m1 = eff_k[0];
-          i1 = lane;
-          m2 = eff_k[1];
-        } else {
-          m1 = eff_k[1];
-          i1 = lane + 32;
-          m2 = eff_k[0];
-        }
-        // reductions only span the lanes that own groups/children: width W =
-        // next power of two >= G+1 (the full warp once slot 1 is in use)
-        const int W = G + 1 > 32 ? 32 : (G + 1 <= 1 ? 1 : 1 << (32 - __clz(G)));
-        for (int off = W >> 1; off > 0; off >>= 1) {
-          const double om1 = __shfl_xor_sync(HPK_FULL_MASK, m1, off);
-          const int oi1 = __shfl_xor_sync(HPK_FULL_MASK, i1, off);
-          const double om2 = __shfl_xor_sync(HPK_FULL_MASK, m2, off);
-          if (om1 < m1 || (om1 == m1 && oi1 < i1)) {
-            m2 = m1 < om2 ? m1 : om2;
-            m1 = om1;
-            i1 = oi1;
-          } else {
-            m2 = om1 < m2 ? om1 : m2;
+    while (true) {
+      HPK_PC(3, 1);
+      if ((++it & 31) == 0) {
+        if ((it & 1023) == 0) {  // wall-clock watchdog (uniform: lane 0's clock)
+          unsigned long long now;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+          now = __shfl_sync(HPK_FULL_MASK, now, 0);
+          if (now > deadline) {
+            if (lane == 0) atomicOr(err, 2);
+            o.finished = true;
+            break;
           }
         }
-        // each lane evaluates the children it owns (c = lane, lane+32)
-        double best_o = -1.0;
-        int best_Gc = 0, best_c = 1 << 30;
-        double mx = -1.0;
+        if (stopf != nullptr) {
+          const int s = shfl(stop_pending, 0);
+          if (lane == 0) stop_pending = *((volatile const int*)stopf);
+          if (s) {
+            const long long lim = o.visits > minq ? o.visits : minq;
+            if (lim < cap) cap = lim;
+          }
+        }
+      }
+      if (d == n - 1) {
+        // ---- leaf batch: children c0..G are leaves (unit n-1) ----
+        const int c0 = c;
+        int count = G + 1 - c0;
+        bool end_hit = false;
+        if (prefix && match == d) {  // dend == n here
+          if (ec - c0 < count) {
+            count = ec - c0 > 0 ? ec - c0 : 0;
+            end_hit = true;
+          }
+        }
+        bool cap_hit = false;
+        if ((long long)count > cap - o.visits) {
+          count = (int)(cap - o.visits);
+          cap_hit = true;
+          end_hit = false;
+        }
+        if (count > 0) {
+          bool inf_k[2];
+          double eff_k[2];
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          const int c = lane + 32 * k;
-          if (c >= c0 && c < c0 + count) {
-            double eff_new, mem_new, other_min;
-            int others_inf, Gc;
-            if (c < G) {
-              eff_new = (g.gp[k] + up) * g.f1[k];
-              mem_new = g.gm[k] + um;
-              others_inf = n_inf - (inf_k[k] ? 1 : 0);
-              other_min = (c == i1) ? m2 : m1;
-              Gc = G;
-            } else {  // c == G: new singleton group
-              eff_new = up * P.f[1];
-              mem_new = um;
-              others_inf = n_inf;
-              other_min = m1;
-              Gc = G + 1;
-            }
-            if (others_inf == 0 && !(mem_new < P.min_mem)) {
+          for (int k = 0; k < 2; ++k) {
+            const bool valid = g.gc[k] > 0;
+            inf_k[k] = valid && g.gm[k] < mm_;
+            eff_k[k] = valid ? slot_eff(P, g, k) : INFINITY;
+          }
+          const int n_inf = __popc(__ballot_sync(HPK_FULL_MASK, inf_k[0])) +
+                            __popc(__ballot_sync(HPK_FULL_MASK, inf_k[1]));
+          // min1 / idx1 / min2 over existing groups
+          const bool s0 = eff_k[0] <= eff_k[1];
+          double m1 = s0 ? eff_k[0] : eff_k[1];
+          double m2 = s0 ? eff_k[1] : eff_k[0];
+          int i1 = s0 ? lane : lane + 32;
+          // reductions only span the lanes that own groups/children: width W =
+          // next power of two >= G+1 (the full warp once slot 1 is in use)
+          const int W = G + 1 > 32 ? 32 : (G + 1 <= 1 ? 1 : 1 << (32 - __clz(G)));
+          for (int off = W >> 1; off > 0; off >>= 1) {
+            const double om1 = __shfl_xor_sync(HPK_FULL_MASK, m1, off);
+            const int oi1 = __shfl_xor_sync(HPK_FULL_MASK, i1, off);
+            const double om2 = __shfl_xor_sync(HPK_FULL_MASK, m2, off);
+            const bool take = om1 < m1 || (om1 == m1 && oi1 < i1);
+            const double lo2 = take ? m1 : om1;
+            m2 = lo2 < (take ? om2 : m2) ? lo2 : (take ? om2 : m2);
+            m1 = take ? om1 : m1;
+            i1 = take ? oi1 : i1;
+          }
+          // each lane evaluates the children it owns (c = lane, lane+32)
+          double best_o = -1.0;
+          int best_Gc = 0, best_c = 1 << 30;
+          double mx = -1.0;
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const int ch = lane + 32 * k;
+            const bool isnew = ch == G;  // new singleton group (the slot is empty)
+            const double eff_new = (g.gp[k] + up) * g.f1[k];
+            const double mem_new = g.gm[k] + um;
+            const int others_inf = n_inf - (inf_k[k] ? 1 : 0);
+            const double other_min = (!isnew && ch == i1) ? m2 : m1;
+            const int Gc = isnew ? G + 1 : G;
+            if (ch >= c0 && ch < c0 + count && others_inf == 0 && !(mem_new < mm_)) {
               const double z = eff_new < other_min ? eff_new : other_min;
               const double obj = (double)Gc * z;
               mx = obj > mx ? obj : mx;
-              if (best_o < 0 || key_better(obj, Gc, c, best_o, best_Gc, best_c)) {
+              if (best_o < 0 || key_better(obj, Gc, ch, best_o, best_Gc, best_c)) {
                 best_o = obj;
                 best_Gc = Gc;
-                best_c = c;
+                best_c = ch;
               }
             }
           }
-        }
-        for (int off = W >> 1; off > 0; off >>= 1) {
-          const double oo = __shfl_xor_sync(HPK_FULL_MASK, best_o, off);
-          const int og = __shfl_xor_sync(HPK_FULL_MASK, best_Gc, off);
-          const int oc = __shfl_xor_sync(HPK_FULL_MASK, best_c, off);
-          if (oo >= 0 && (best_o < 0 || key_better(oo, og, oc, best_o, best_Gc, best_c))) {
-            best_o = oo;
-            best_Gc = og;
-            best_c = oc;
+          for (int off = W >> 1; off > 0; off >>= 1) {
+            const double oo = __shfl_xor_sync(HPK_FULL_MASK, best_o, off);
+            const int og = __shfl_xor_sync(HPK_FULL_MASK, best_Gc, off);
+            const int oc = __shfl_xor_sync(HPK_FULL_MASK, best_c, off);
+            const double om = __shfl_xor_sync(HPK_FULL_MASK, mx, off);
+            const bool take = oo >= 0 && (best_o < 0 || key_better(oo, og, oc, best_o, best_Gc, best_c));
+            best_o = take ? oo : best_o;
+            best_Gc = take ? og : best_Gc;
+            best_c = take ? oc : best_c;
+            mx = om > mx ? om : mx;
           }
-          const double om = __shfl_xor_sync(HPK_FULL_MASK, mx, off);
-          mx = om > mx ? om : mx;
-        }
-        if (W < 32) {  // make the block-[0,W) result warp-uniform
-          best_o = shfl(best_o, 0);
-          best_Gc = shfl(best_Gc, 0);
-          best_c = shfl(best_c, 0);
-          mx = shfl(mx, 0);
-        }
-        o.visits += count;
-        if (best_o >= 0) {
-          if (!o.has_best || best_o > o.best_obj ||
-              (best_o == o.best_obj && best_Gc < o.best_G)) {
-            o.has_best = true;
-            o.best_obj = best_o;
-            o.best_G = best_Gc;
-            for (int i = lane; i < n - 1; i += 32) sm->best[i] = sm->path[i];
-            if (lane == 0) sm->best[n - 1] = (uint8_t)best_c;
-            __syncwarp();
+          if (W < 32) {  // make the block-[0,W) result warp-uniform
+            best_o = shfl(best_o, 0);
+            best_Gc = shfl(best_Gc, 0);
+            best_c = shfl(best_c, 0);
+            mx = shfl(mx, 0);
           }
-          o.m = mx > o.m ? mx : o.m;
-          cut = mx > cut ? mx : cut;
+          o.visits += count;
+          if (best_o >= 0) {
+            if (!o.has_best || best_o > o.best_obj ||
+                (best_o == o.best_obj && best_Gc < o.best_G)) {
+              o.has_best = true;
+              o.best_obj = best_o;
+              o.best_G = best_Gc;
+              __syncwarp();  // lane 0's path spills are visible
+              for (int i = lane; i < n - 1; i += 32) sm->best[i] = sm->path[i];
+              if (lane == 0) sm->best[n - 1] = (uint8_t)best_c;
+              __syncwarp();
+            }
+            o.m = mx > o.m ? mx : o.m;
+            cut = mx > cut ? mx : cut;
+          }
+        }
+        HPK_PC(1, 1);
+        HPK_PC(2, count > 0 ? count : 0);
+        if (cap_hit) {
+          if (lane == 0) sm->lvl[d] = (unsigned)G << 16;
+          o.dstop = d + 1;
+          o.stop_c = c0 + count;
+          o.finished = false;
+          break;
+        }
+        if (end_hit) {
+          o.finished = true;
+          break;
+        }
+        c = G + 1;
+      }
+      if (c > G) {  // node exhausted: pop unit d-1
+        if (d == du) {
+          o.finished = true;
+          break;
+        }
+        __syncwarp();  // lane 0's spills of this level are visible
+        --d;
+        const unsigned w0 = sm->lvl[d];  // path | next child << 8 | G << 16
+        up = P.p[d];
+        um = P.m[d];
+        Sd = sm->S[d];
+        Dd = sm->DEF[d];
+        mp = sm->mpass[d];
+        mr = sm->mprune[d];
+        mc = sm->mcut[d];
+        const int grp = w0 & 255;
+        c = (w0 >> 8) & 255;
+        G = (w0 >> 16) & 255;
+        remove_unit(P, g, lane, grp, up, um);
+        sums_ok = false;
+        if (match > d) match = d;
+        if (prefix && match == d) ec = sm->endp[d];
+        HPK_PC(6, 1);
+        continue;
+      }
+      if (prefix && match == d) {
+        if (c > ec || (c == ec && d + 1 == dend)) {
+          o.finished = true;
+          break;
         }
       }
-      if (prof && lane == 0) {
-        atomicAdd(prof + 0, (unsigned long long)(clock64() - pc0));
-        atomicAdd(prof + 1, 1ull);
-        atomicAdd(prof + 2, (unsigned long long)(count > 0 ? count : 0));
-        if (prof[11] == 4)
-          printf("[hpk-t] leaves d %d G %d count %d cut %.17g\n", d, G, count, cut);
-      }
-      if (cap_hit) {
+      if (o.visits >= cap) {
+        if (lane == 0) sm->lvl[d] = (unsigned)G << 16;
         o.dstop = d + 1;
-        o.stop_c = c0 + count;
+        o.stop_c = c;
         o.finished = false;
         break;
       }
-      if (end_hit) {
-        o.finished = true;
-        break;
-      }
-      if (lane == 0) sm->nxt[d] = (uint8_t)(G + 1);
-      __syncwarp();
-    }
-    const int c = sm->nxt[d];
-    if (c > G) {  // node exhausted: pop unit d-1
-      if (d == du) {
-        o.finished = true;
-        break;
-      }
-      if (prof) pc0 = clock64();
-      const int grp = sm->path[d - 1];
-      remove_unit(P, g, lane, grp, P.p[d - 1], P.m[d - 1]);
-      G = sm->Gat[d - 1];
-      --d;
-      if (prof && lane == 0) atomicAdd(prof + 6, (unsigned long long)(clock64() - pc0));
-      if (match > d) match = d;
-      continue;
-    }
-    if (prefix && match == d) {
-      const int ec = sm->endp[d];
-      if (c > ec || (c == ec && d + 1 == dend)) {
-        o.finished = true;
-        break;
-      }
-    }
-    if (o.visits >= cap) {
-      o.dstop = d + 1;
-      o.stop_c = c;
-      o.finished = false;
-      break;
-    }
-    if (prof) pc0 = clock64();
-    o.visits += 1;
-    if (lane == 0) sm->nxt[d] = (uint8_t)(c + 1);
-    __syncwarp();  // every lane re-reads nxt[d] at the next iteration
-    // ---- check child c (internal node at depth d+1) ----
-    // All children of the node at depth d are checked in ONE lane-parallel
-    // round (lane ci decides child ci); the outcome is kept as pass/prune
-    // bitmasks per level and reused until the cutoff changes. The child's
-    // level sums follow from the parent's in O(1):
-    //   S' = S - eff(ci) + eff'(ci),  DEF' = DEF - def(ci) + def'(ci)
-    if (sm->mcut[d] != cut) {
-      int ldec[2] = {DEC_PRUNE, DEC_PRUNE};
-      const double up = P.p[d], um = P.m[d];
-      const double Sd = sm->S[d], Dd = sm->DEF[d], Rn = P.R[d + 1];
+      // ---- child decisions of this node, lane-parallel (lane ci decides
+      // children ci and ci+32), recomputed only when the cutoff moved. The
+      // child's level sums follow from the parent's in O(1):
+      //   S' = S - eff(ci) + eff'(ci),  DEF' = DEF - def(ci) + def'(ci)
+      // (an empty slot ci == G gives eff = 0, eff' = up * f[1]). A child is
+      // PRUNE / PASS when the approximate bound and deficit clear the cutoff by
+      // more than the error margins mb / md; else it is checked exactly.
+      if (mc != cut) {
+        const double Rn = P.R[d + 1], RMn = P.RM[d + 1];
+        const bool hc = cut >= 0;
+        bool pr[2], ps[2];
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const int ci = lane + 32 * k;
-        if (ci <= G) {
-          double eff_old, eff_new, def_old, def_new;
-          if (ci < G) {
-            eff_old = g.gp[k] * g.f0[k];
-            eff_new = (g.gp[k] + up) * g.f1[k];
-            const double d0 = P.min_mem - g.gm[k];
-            def_old = d0 > 0.0 ? d0 : 0.0;
-            const double d1 = P.min_mem - (g.gm[k] + um);
-            def_new = d1 > 0.0 ? d1 : 0.0;
-          } else {
-            eff_old = 0;
-            eff_new = up * P.f[1];
-            def_old = 0;
-            const double d1 = P.min_mem - um;
-            def_new = d1 > 0.0 ? d1 : 0.0;
-          }
-          const double lS = (Sd - eff_old) + eff_new;
-          const double lD = (Dd - def_old) + def_new;
-          ldec[k] = decide(P, lS + Rn, lD, d + 1, cut);
+        for (int k = 0; k < 2; ++k) {
+          const int ci = lane + 32 * k;
+          const double eff_old = g.gp[k] * g.f0[k];
+          const double eff_new = (g.gp[k] + up) * g.f1[k];
+          const double d0 = mm_ - g.gm[k];
+          const double def_old = (g.gc[k] > 0 && d0 > 0.0) ? d0 : 0.0;
+          const double d1 = mm_ - (g.gm[k] + um);
+          const double def_new = d1 > 0.0 ? d1 : 0.0;
+          lS[k] = (Sd - eff_old) + eff_new;
+          lD[k] = (Dd - def_old) + def_new;
+          const double A = lS[k] + Rn;
+          const bool valid = ci <= G;
+          pr[k] = !valid || (hc && A + mb < cut) || (lD[k] - md > RMn);
+          ps[k] = !pr[k] && (!hc || A - mb >= cut) && (lD[k] + md <= RMn);
         }
+        mp = (unsigned long long)__ballot_sync(HPK_FULL_MASK, ps[0]) |
+             ((unsigned long long)__ballot_sync(HPK_FULL_MASK, ps[1]) << 32);
+        mr = (unsigned long long)__ballot_sync(HPK_FULL_MASK, pr[0]) |
+             ((unsigned long long)__ballot_sync(HPK_FULL_MASK, pr[1]) << 32);
+        mc = cut;
+        sums_ok = true;
+        HPK_PC(10, 1);
       }
-      const unsigned p0 = __ballot_sync(HPK_FULL_MASK, ldec[0] == DEC_PASS);
-      const unsigned p1 = __ballot_sync(HPK_FULL_MASK, ldec[1] == DEC_PASS);
-      const unsigned r0 = __ballot_sync(HPK_FULL_MASK, ldec[0] == DEC_PRUNE);
-      const unsigned r1 = __ballot_sync(HPK_FULL_MASK, ldec[1] == DEC_PRUNE);
-      if (lane == 0) {
-        sm->mpass[d] = (unsigned long long)p0 | ((unsigned long long)p1 << 32);
-        sm->mprune[d] = (unsigned long long)r0 | ((unsigned long long)r1 << 32);
-        sm->mcut[d] = cut;
-      }
-      __syncwarp();
-    }
-    int dec;
-    {
       const unsigned long long bit = 1ull << c;
-      dec = (sm->mpass[d] & bit) ? DEC_PASS : ((sm->mprune[d] & bit) ? DEC_PRUNE : DEC_EXACT);
-    }
-    if (dbg) {  // HPK_TRACE=3: cross-check the mask against a direct owner-lane decision
-      const int owner = c & 31, k = c >> 5;
-      int ld = 0;
-      if (lane == owner) {
-        const double up = P.p[d], um = P.m[d];
-        const double gpk = k == 0 ? g.gp[0] : g.gp[1];
-        const double gmk = k == 0 ? g.gm[0] : g.gm[1];
-        double eff_old, eff_new, def_old, def_new;
-        if (c < G) {
-          eff_old = gpk * (k == 0 ? g.f0[0] : g.f0[1]);
-          eff_new = (gpk + up) * (k == 0 ? g.f1[0] : g.f1[1]);
-          const double d0 = P.min_mem - gmk;
-          def_old = d0 > 0.0 ? d0 : 0.0;
-          const double d1 = P.min_mem - (gmk + um);
-          def_new = d1 > 0.0 ? d1 : 0.0;
-        } else {
-          eff_old = 0;
-          eff_new = up * P.f[1];
-          def_old = 0;
-          const double d1 = P.min_mem - um;
-          def_new = d1 > 0.0 ? d1 : 0.0;
+      if (mr & bit) {
+        // children c .. c+k-1 are all pruned: k visits, nothing entered
+        const unsigned long long rest = ~(mr >> c);
+        int k = rest ? __ffsll((long long)rest) - 1 : 64 - c;
+        if (k > G + 1 - c) k = G + 1 - c;
+        if ((long long)k > cap - o.visits) k = (int)(cap - o.visits);
+        if (prefix && match == d) {
+          // the end node (d+1 == dend) is not visited; the end path's child is,
+          // and its prune is the ancestor prune a* (grouping.cpp:162,169)
+          const int kl = (d + 1 == dend) ? ec - c : ec - c + 1;
+          if (k > kl) k = kl;
+          if (d + 1 < dend && c + k - 1 == ec && o.a_star < 0) o.a_star = d + 1;
         }
-        const double lS = (sm->S[d] - eff_old) + eff_new;
-        const double lD = (sm->DEF[d] - def_old) + def_new;
-        ld = decide(P, lS + P.R[d + 1], lD, d + 1, cut);
-        if (ld != dec)
-          printf("[hpk-dbg] mask/direct mismatch d %d c %d G %d cut %.17g mcut %.17g mask %d direct "
-                 "%d mpass %llx mprune %llx\n", d, c, G, cut, sm->mcut[d], dec, ld, sm->mpass[d],
-                 sm->mprune[d]);
+        o.visits += k;
+        c += k;
+        HPK_PC(7, 1);
+        HPK_PC(8, k);
+        continue;
       }
-      __syncwarp();
-    }
-    if (prof && prof[11] == 4 && lane == 0)
-      printf("[hpk-t] check d %d c %d G %d dec %d cut %.17g S %.17g DEF %.17g\n", d, c, G, dec, cut,
-             sm->S[d], sm->DEF[d]);
-    if (dec == DEC_EXACT) {
-      if (prof && lane == 0) atomicAdd(prof + 9, 1ull);
-      add_unit(P, g, lane, c, P.p[d], P.m[d]);
-      const int Gc = c == G ? G + 1 : G;
-      dec = exact_passes(P, g, Gc, d + 1, cut) ? DEC_PASS : DEC_PRUNE;
-      remove_unit(P, g, lane, c, P.p[d], P.m[d]);
-    }
-    double Sn = 0, Dn = 0;
-    if (dec == DEC_PASS) {  // (also after an exact-path PASS) the owner lane recomputes the child's level sums
-      const int owner = c & 31, k = c >> 5;
-      double lS = 0, lD = 0;
-      if (lane == owner) {
-        const double up = P.p[d], um = P.m[d];
-        const double gpk = k == 0 ? g.gp[0] : g.gp[1];
-        const double gmk = k == 0 ? g.gm[0] : g.gm[1];
-        double eff_old, eff_new, def_old, def_new;
-        if (c < G) {
-          eff_old = gpk * (k == 0 ? g.f0[0] : g.f0[1]);
-          eff_new = (gpk + up) * (k == 0 ? g.f1[0] : g.f1[1]);
-          const double d0 = P.min_mem - gmk;
-          def_old = d0 > 0.0 ? d0 : 0.0;
-          const double d1 = P.min_mem - (gmk + um);
-          def_new = d1 > 0.0 ? d1 : 0.0;
-        } else {
-          eff_old = 0;
-          eff_new = up * P.f[1];
-          def_old = 0;
-          const double d1 = P.min_mem - um;
-          def_new = d1 > 0.0 ? d1 : 0.0;
+      o.visits += 1;
+      HPK_PC(4, 1);
+      if (!(mp & bit)) {  // inside the error margin: the exact serial check
+        o.exact += 1;
+        add_unit(P, g, lane, c, up, um);
+        const int Gc = c == G ? G + 1 : G;
+        const bool pass = exact_passes(P, g, Gc, d + 1, cut);
+        remove_unit(P, g, lane, c, up, um);
+        if (!pass) {
+          if (prefix && match == d && c == ec && o.a_star < 0) o.a_star = d + 1;
+          ++c;
+          continue;
         }
-        lS = (sm->S[d] - eff_old) + eff_new;
-        lD = (sm->DEF[d] - def_old) + def_new;
       }
-      Sn = shfl(lS, owner);
-      Dn = shfl(lD, owner);
+      // ---- PASS: descend into child c
+      if (!sums_ok) {  // (after a pop) the lanes recompute their children's sums
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const double eff_old = g.gp[k] * g.f0[k];
+          const double eff_new = (g.gp[k] + up) * g.f1[k];
+          const double d0 = mm_ - g.gm[k];
+          const double def_old = (g.gc[k] > 0 && d0 > 0.0) ? d0 : 0.0;
+          const double d1 = mm_ - (g.gm[k] + um);
+          const double def_new = d1 > 0.0 ? d1 : 0.0;
+          lS[k] = (Sd - eff_old) + eff_new;
+          lD[k] = (Dd - def_old) + def_new;
+        }
+        sums_ok = true;
+      }
+      const double Sn = shfl(c < 32 ? lS[0] : lS[1], c & 31);
+      const double Dn = shfl(c < 32 ? lD[0] : lD[1], c & 31);
+      if (lane == 0) {  // spill this level
+        sm->lvl[d] = (unsigned)c | ((unsigned)(c + 1) << 8) | ((unsigned)G << 16);
+        sm->path[d] = (uint8_t)c;
+        sm->S[d] = Sd;
+        sm->DEF[d] = Dd;
+        sm->mpass[d] = mp;
+        sm->mprune[d] = mr;
+        sm->mcut[d] = mc;
+      }
+      add_unit(P, g, lane, c, up, um);
+      if (c == G) ++G;
+      if (prefix && match == d && c == ec) match = d + 1;
+      ++d;
+      Sd = Sn;
+      Dd = Dn;
+      c = 0;
+      mc = kNaN;
+      sums_ok = false;
+      up = P.p[d];
+      um = P.m[d];
+      if (prefix && match == d) ec = sm->endp[d];
+      HPK_PC(5, 1);
     }
-    if (prof && lane == 0) {
-      atomicAdd(prof + 3, (unsigned long long)(clock64() - pc0));
-      atomicAdd(prof + 4, 1ull);
-    }
-    if (dec == DEC_PRUNE) {
-      if (prefix && match == d && c == sm->endp[d] && o.a_star < 0) o.a_star = d + 1;
-      continue;
-    }
-    if (prof) pc0 = clock64();
-    // ---- descend into child c ----
-    if (lane == 0) sm->path[d] = (uint8_t)c;
-    __syncwarp();
-    add_unit(P, g, lane, c, P.p[d], P.m[d]);
-    if (c == G) ++G;
-    if (prefix && match == d && c == sm->endp[d]) match = d + 1;
-    ++d;
-    if (lane == 0) {
-      sm->Gat[d] = (uint8_t)G;
-      sm->S[d] = Sn;
-      sm->DEF[d] = Dn;
-      sm->nxt[d] = 0;
-      sm->mcut[d] = __longlong_as_double(0x7ff8000000000000LL);  // NaN: masks invalid
-    }
-    __syncwarp();
-    if (prof && lane == 0) atomicAdd(prof + 5, (unsigned long long)(clock64() - pc0));
   }
 done:
   __syncwarp();
   if (o.has_best)
     for (int i = lane; i < n; i += 32) Eout->best_rgs[i] = sm->best[i];
   __syncwarp();
+  if (prof && lane == 0) {
+    pcnt[0] = (unsigned long long)(clock64() - pc0);
+#pragma unroll
+    for (int k = 0; k < 11; ++k) atomicAdd(prof + k, pcnt[k]);
+  }
+#undef HPK_PC
   return o;
 }
 
@@ -834,8 +810,9 @@ __device__ int split_run(const KParams& kp, int p, GState& S, Entry* E, const Ru
   const int du = E->du;
   const int d = o.dstop - 1;  // the stop node is child stop_c of path[0..d)
   // level table: lev = d (siblings after stop_c), then lev = d-1 .. du
-  int count = 1 + ((int)sm->Gat[d] - o.stop_c);
-  for (int lev = d - 1; lev >= du; --lev) count += (int)sm->Gat[lev] - (int)sm->path[lev];
+  const auto gat = [&](int lev) { return (int)((sm->lvl[lev] >> 16) & 255); };
+  int count = 1 + (gat(d) - o.stop_c);
+  for (int lev = d - 1; lev >= du; --lev) count += gat(lev) - (int)sm->path[lev];
   int first = 0;
   if (lane == 0) {  // CAS bump allocation: a failed attempt leaves no hole, and the
     // list head alone may use the last `reserve` slots (progress guarantee)
@@ -866,12 +843,12 @@ __device__ int split_run(const KParams& kp, int p, GState& S, Entry* E, const Ru
       int idx = k - 1;
       lev = d;
       int base = o.stop_c;
-      int cnt = (int)sm->Gat[d] - base;
+      int cnt = gat(d) - base;
       while (idx >= cnt) {
         idx -= cnt;
         --lev;
         base = sm->path[lev];
-        cnt = (int)sm->Gat[lev] - base;
+        cnt = gat(lev) - base;
       }
       child = base + 1 + idx;
     }
@@ -1094,9 +1071,135 @@ __device__ void push_items(const KParams& kp, int queue, int p, const int* ids, 
   }
 }
 
+// ---- list expansion, spread over every CTA (schedule step S2). The list of a
+// problem is cut into tiles of TILE positions; the runners added the piece
+// counts of their splits to xt[tile] (atomic), so a tile's output offset is
+// known from the tile counts alone: tiles without splits are shifted copies,
+// the others scan their expansion counts. A nearly full list (the revert rule
+// needs the whole list in order) is left to the problem's own CTA (S3).
+__device__ __forceinline__ int xt_sums(const int* xt, int ntile, int t, SchedSmem* sh, int* before) {
+  const int tid = threadIdx.x;
+  if (tid < 32) {
+    int b = 0, a = 0;
+    for (int k = tid; k < ntile; k += 32) {
+      const int x = xt[k];
+      a += x;
+      if (k < t) b += x;
+    }
+    b = warp_sum_int(b);
+    a = warp_sum_int(a);
+    if (tid == 0) {
+      sh->i[60] = b;
+      sh->i[61] = a;
+    }
+  }
+  __syncthreads();
+  *before = sh->i[60];
+  const int all = sh->i[61];
+  __syncthreads();
+  return all;
+}
+
+__device__ void expand_tile(const KParams& kp, int p, int t, SchedSmem* sh) {
+  const GState& S = kp.states[p];
+  const int tid = threadIdx.x;
+  if (S.done || S.rerun_pending) return;
+  const int cur = S.cur, head = S.head, len = S.len;
+  const int ntile = (len + TILE - 1) / TILE;
+  const int* xt = kp.xt + (size_t)p * kp.xtn;
+  int ebase = 0;
+  const int etot = xt_sums(xt, ntile, t, sh, &ebase);
+  if (len + etot > kp.lcap - kp.reserve) return;
+  const int lo = t * TILE, n = min(TILE, len - lo);
+  const int* __restrict__ ids_i = list_arr(kp, p, cur, 0) + head + lo;
+  const int* __restrict__ pcv_i = list_arr(kp, p, cur, 1) + head + lo;
+  const int* __restrict__ cnt_i = list_arr(kp, p, cur, 2) + head + lo;
+  const int* __restrict__ pf_i = list_arr(kp, p, cur, 3) + head + lo;
+  const int* __restrict__ inf_i = list_arr(kp, p, cur, 4) + head + lo;
+  const long long* __restrict__ vis_i = list_vis(kp, p, cur) + head + lo;
+  const double* __restrict__ cut_i = list_dbl(kp, p, cur, 0) + head + lo;
+  const double* __restrict__ m_i = list_dbl(kp, p, cur, 1) + head + lo;
+  const double* __restrict__ bo_i = list_dbl(kp, p, cur, 2) + head + lo;
+  const int ob = lo + ebase;  // output position of the tile's first entry
+  int* __restrict__ ids_o = list_arr(kp, p, cur ^ 1, 0) + ob;
+  int* __restrict__ pcv_o = list_arr(kp, p, cur ^ 1, 1) + ob;
+  int* __restrict__ cnt_o = list_arr(kp, p, cur ^ 1, 2) + ob;
+  int* __restrict__ inf_o = list_arr(kp, p, cur ^ 1, 4) + ob;
+  long long* __restrict__ vis_o = list_vis(kp, p, cur ^ 1) + ob;
+  double* __restrict__ cut_o = list_dbl(kp, p, cur ^ 1, 0) + ob;
+  double* __restrict__ m_o = list_dbl(kp, p, cur ^ 1, 1) + ob;
+  double* __restrict__ bo_o = list_dbl(kp, p, cur ^ 1, 2) + ob;
+  if (xt[t] == 0) {  // no split in this tile: shifted copy
+#pragma unroll 4
+    for (int i = tid; i < n; i += blockDim.x) {
+      ids_o[i] = ids_i[i];
+      pcv_o[i] = pcv_i[i];
+      inf_o[i] = inf_i[i];
+      vis_o[i] = vis_i[i];
+      cut_o[i] = cut_i[i];
+      m_o[i] = m_i[i];
+      bo_o[i] = bo_i[i];
+      cnt_o[i] = 1;
+    }
+    return;
+  }
+  int* off = kp.scratch + (size_t)p * (kp.lcap + 1) + lo;
+  const int tsum = block_scan8<int>(cnt_i, off, n, sh->i);
+  __syncthreads();
+  const int* __restrict__ o_ = off;
+  // 4 consecutive inputs per thread, all loads issued before the stores
+  for (int i0 = tid * 4; i0 < n; i0 += blockDim.x * 4) {
+    int o[5], id[4], pc[4], inf[4];
+    long long vv[4];
+    double cu[4], mm[4], bb[4];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) o[k] = i0 + k < n ? o_[i0 + k] : tsum;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = i0 + k < n ? i0 + k : i0;
+      id[k] = ids_i[i];
+      pc[k] = pcv_i[i];
+      inf[k] = inf_i[i];
+      vv[k] = vis_i[i];
+      cu[k] = cut_i[i];
+      mm[k] = m_i[i];
+      bb[k] = bo_i[i];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (i0 + k < n) {
+        const int q = o[k];
+        ids_o[q] = id[k];
+        pcv_o[q] = pc[k];
+        inf_o[q] = inf[k];
+        vis_o[q] = vv[k];
+        cut_o[q] = cu[k];
+        m_o[q] = mm[k];
+        bo_o[q] = bb[k];
+        cnt_o[q] = 1;
+        const int c = o[k + 1] - q;
+        if (c > 1) {
+          const int pf = pf_i[i0 + k];
+          for (int tt = 1; tt < c; ++tt) {
+            ids_o[q + tt] = pf + tt - 1;
+            pcv_o[q + tt] = -1;
+            inf_o[q + tt] = 0;
+            vis_o[q + tt] = 0;
+            cut_o[q + tt] = -1.0;
+            m_o[q + tt] = -1.0;
+            bo_o[q + tt] = -1.0;
+            cnt_o[q + tt] = 1;
+          }
+        }
+      }
+    }
+  }
+}
+
 // Per-problem scheduler (one CTA): expand splits, ordered commit, compaction,
 // queue the next wave.
-__device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* smem_tmp) {
+__device__ void schedule_problem(const KParams& kp, int p, int next_queue, void* smem_tmp,
+                                 int wnext) {
   GState& S = kp.states[p];
   const GProb& P = kp.probs[p];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1115,6 +1218,10 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
   double* m_in = list_dbl(kp, p, cur, 1);
   double* cut_out = list_dbl(kp, p, cur ^ 1, 0);
   double* m_out = list_dbl(kp, p, cur ^ 1, 1);
+  int* inf_in = list_arr(kp, p, cur, 4);
+  int* inf_out = list_arr(kp, p, cur ^ 1, 4);
+  double* bo_in = list_dbl(kp, p, cur, 2);
+  double* bo_out = list_dbl(kp, p, cur ^ 1, 2);
   Entry* pool = pool_ptr(kp, p, S.pool_cur);
 
   if (S.rerun_pending) {
@@ -1139,25 +1246,36 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
 
   unsigned long long _tprev = 0;
   if (kp.trace >= 5 && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_tprev));
-  // ---- A. expand the splits made by this wave's runs (cnt = 1 + pieces)
-  int* off = kp.scratch + (size_t)p * (kp.lcap + 1);
-  int total = block_scan8<int>(cnt_in + head, off, len, smem_tmp);
-  if (total > kp.lcap - kp.reserve) {
-    // List nearly full: keep expansions in list order while they leave the
-    // head's reserve free; the others are reverted to unrun FULL segments
-    // (their pieces become garbage). If even the head cannot expand it re-runs
-    // uncapped (finishes in one run) — progress is guaranteed.
-    if (tid == 0) {
-      int used = len;
-      for (int i = 0; i < len; ++i) {
-        const int c = (i + 1 < len ? off[i + 1] : total) - off[i];
-        off[i] = c;
+  // ---- A. expand the splits made by this wave's runs (cnt = 1 + pieces).
+  // Normally done by expand_tile() over every CTA (S2); a nearly full list is
+  // expanded here, in order, with the revert rule.
+  SchedSmem* sh = reinterpret_cast<SchedSmem*>(smem_tmp);
+  int* xt = kp.xt + (size_t)p * kp.xtn;
+  const int ntile = (len + TILE - 1) / TILE;
+  int xt_before;
+  const int etot = xt_sums(xt, ntile, 0, sh, &xt_before);
+  for (int k = tid; k < ntile; k += blockDim.x) xt[k] = 0;  // re-armed for the next wave
+  int total;
+  if (len + etot <= kp.lcap - kp.reserve) {
+    total = len + etot;  // expanded by expand_tile()
+  } else {
+    const int mr = len;
+    int* off = kp.scratch + (size_t)p * (kp.lcap + 1);
+    int total_run = block_scan8<int>(cnt_in + head, off, mr, sh->i);
+    if (total_run + (len - mr) > kp.lcap - kp.reserve) {
+      // List nearly full: expansions are kept in list order while the list still
+      // leaves the head's reserve free (the inclusive count of extra entries is
+      // monotone, so the kept ones form a prefix); the others are reverted to
+      // unrun FULL segments (their pieces become garbage). If even the head cannot
+      // expand it re-runs uncapped (finishes in one run) — progress is guaranteed.
+      for (int i = tid; i < mr; i += blockDim.x) {
+        const int nx = i + 1 < mr ? off[i + 1] : total_run;
+        int c = nx - off[i];
         if (c > 1) {
-          const int limit = i == 0 ? kp.lcap : kp.lcap - kp.reserve;
-          if (used + c - 1 <= limit) {
-            used += c - 1;
-          } else {
-            off[i] = 1;
+          const int incl_extra = nx - (i + 1);
+          const int limit = (i == 0 ? kp.lcap : kp.lcap - kp.reserve) - len;
+          if (incl_extra > limit) {
+            c = 1;
             Entry& e = pool[ids_in[head + i]];
             e.kind = KIND_FULL;
             e.cver = -1;
@@ -1166,102 +1284,211 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
             pcv_in[head + i] = -1;
           }
         }
+        cnt_in[head + i] = c;
+      }
+      __syncthreads();
+      total_run = block_scan8<int>(cnt_in + head, off, mr, sh->i);
+    }
+    total = total_run + (len - mr);
+    if (tid == 0) off[mr] = total_run;
+    __syncthreads();
+    {
+      const int* __restrict__ o_ = off;
+      const int* __restrict__ ids_i = ids_in + head;
+      const int* __restrict__ pcv_i = pcv_in + head;
+      const int* __restrict__ inf_i = inf_in + head;
+      const int* __restrict__ pf_i = pf_in + head;
+      const long long* __restrict__ vis_i = vis_in + head;
+      const double* __restrict__ cut_i = cut_in + head;
+      const double* __restrict__ m_i = m_in + head;
+      const double* __restrict__ bo_i = bo_in + head;
+      int* __restrict__ ids_o = ids_out;
+      int* __restrict__ pcv_o = pcv_out;
+      int* __restrict__ inf_o = inf_out;
+      int* __restrict__ cnt_o = cnt_out;
+      long long* __restrict__ vis_o = vis_out;
+      double* __restrict__ cut_o = cut_out;
+      double* __restrict__ m_o = m_out;
+      double* __restrict__ bo_o = bo_out;
+      // run region: 4 consecutive inputs per thread, all loads issued before the stores
+      for (int i0 = tid * 4; i0 < mr; i0 += blockDim.x * 4) {
+        int o[5], id[4], pc[4], inf[4];
+        long long vv[4];
+        double cu[4], mm[4], bb[4];
+  #pragma unroll
+        for (int k = 0; k < 5; ++k) o[k] = i0 + k <= mr ? o_[i0 + k] : 0;
+  #pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int i = i0 + k < mr ? i0 + k : i0;
+          id[k] = ids_i[i];
+          pc[k] = pcv_i[i];
+          inf[k] = inf_i[i];
+          vv[k] = vis_i[i];
+          cu[k] = cut_i[i];
+          mm[k] = m_i[i];
+          bb[k] = bo_i[i];
+        }
+  #pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (i0 + k < mr) {
+            const int q = o[k];
+            ids_o[q] = id[k];
+            pcv_o[q] = pc[k];
+            inf_o[q] = inf[k];
+            vis_o[q] = vv[k];
+            cut_o[q] = cu[k];
+            m_o[q] = mm[k];
+            bo_o[q] = bb[k];
+            cnt_o[q] = 1;
+            const int c = o[k + 1] - q;
+            if (c > 1) {
+              const int pf = pf_i[i0 + k];
+              for (int t = 1; t < c; ++t) {
+                ids_o[q + t] = pf + t - 1;
+                pcv_o[q + t] = -1;
+                inf_o[q + t] = 0;
+                vis_o[q + t] = 0;
+                cut_o[q + t] = -1.0;
+                m_o[q + t] = -1.0;
+                bo_o[q + t] = -1.0;
+                cnt_o[q + t] = 1;
+              }
+            }
+          }
+        }
+      }
+      // tail: shifted copy
+      const int delta = total_run - mr;
+  #pragma unroll 4
+      for (int i = mr + tid; i < len; i += blockDim.x) {
+        const int q = i + delta;
+        ids_o[q] = ids_i[i];
+        pcv_o[q] = pcv_i[i];
+        inf_o[q] = inf_i[i];
+        vis_o[q] = vis_i[i];
+        cut_o[q] = cut_i[i];
+        m_o[q] = m_i[i];
+        bo_o[q] = bo_i[i];
+        cnt_o[q] = 1;
       }
     }
     __syncthreads();
-    total = block_scan8<int>(off, off, len, smem_tmp);
   }
-  if (tid == 0) off[len] = total;
-  __syncthreads();
-  for (int i0 = tid * 8; i0 < len; i0 += blockDim.x * 8)  // scatter from the input side,
-  for (int i = i0; i < i0 + 8 && i < len; ++i) {            // 8 consecutive inputs per thread
-    const int o = off[i];
-    const int c = off[i + 1] - o;
-    ids_out[o] = ids_in[head + i];
-    pcv_out[o] = pcv_in[head + i];
-    vis_out[o] = vis_in[head + i];
-    cut_out[o] = cut_in[head + i];
-    m_out[o] = m_in[head + i];
-    cnt_out[o] = 1;
-    if (c > 1) {
-      const int pf = pf_in[head + i];
-      for (int k = 1; k < c; ++k) {
-        ids_out[o + k] = pf + k - 1;
-        pcv_out[o + k] = -1;
-        vis_out[o + k] = 0;
-        cut_out[o + k] = -1.0;
-        m_out[o + k] = -1.0;
-        cnt_out[o + k] = 1;
-      }
-    }
-  }
-  __syncthreads();
-
   if (kp.trace >= 5 && tid == 0) {
     unsigned long long _t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));
     atomicAdd(kp.prof + 12, _t - _tprev);
     _tprev = _t;
   }
-  // ---- B. ordered commit walk (warp 0)
-  __shared__ int sh_head, sh_flag;
-  __shared__ long long sh_cap;
-  if (warp == 0) {
-    double C = S.C;
-    int cver = S.cver;
-    long long V = S.V;
-    const long long B = P.budget;
-    int i = 0;
-    int done = 0, aborted = 0, rerun = 0;
-    long long rerun_cap = 0;
-    while (i < total) {
-      const int j = i + lane;
-      const bool ok = j < total && pcv_out[j] == 1 && cut_out[j] == C;
-      long long v = 0;
-      double m = -1, bo = 0;
-      int bg = 0, hb = 0, ast = -1, kind = 0;
-      if (ok) {
-        const Entry& e = pool[ids_out[j]];
-        v = e.visits;
-        m = e.m;
-        hb = e.has_best;
-        bo = e.best_obj;
-        bg = e.best_G;
-        ast = e.a_star;
-        kind = e.kind;
-      }
-      const unsigned bad = __ballot_sync(HPK_FULL_MASK, !ok);
-      const int first_bad = bad ? __ffs(bad) - 1 : 32;
-      long long cum = v;  // inclusive scan of visits
+  // ---- B. ordered commit walk, block-parallel over tiles of 8 positions per
+  // thread. Walking the list in order, position j commits iff its run is
+  // exact: it ran with the cutoff the serial DFS has on entering it,
+  //     C_j = max(C_front, max m over the committed positions before j)
+  // (a prefix max — improvements need no stop). A tile stops at the first
+  // position that is not exact, or right after a PREFIX whose re-run pruned an
+  // ancestor (it deletes the pieces under that ancestor) or the position where
+  // the budget runs out (grouping.cpp:174-177).
+  double C = S.C;
+  int cver = S.cver;
+  long long V = S.V;
+  const long long B = P.budget;
+  int i = 0;
+  int done = 0, aborted = 0, rerun = 0;
+  long long rerun_cap = 0;
+  while (i < total) {
+    const int tile = min(total - i, (int)blockDim.x * 8);
+    const int r0 = tid * 8;  // this thread's positions, relative to i
+    int pc[8], inf[8];
+    double cu[8], mm[8];
+    long long vv[8];
 #pragma unroll
-      for (int o2 = 1; o2 < 32; o2 <<= 1) {
-        const long long t = __shfl_up_sync(HPK_FULL_MASK, cum, o2);
-        if (lane >= o2) cum += t;
+    for (int k = 0; k < 8; ++k) {
+      const int r = r0 + k;
+      const int j = i + (r < tile ? r : 0);
+      pc[k] = r < tile ? pcv_out[j] : 0;
+      cu[k] = cut_out[j];
+      mm[k] = m_out[j];
+      vv[k] = vis_out[j];
+      inf[k] = inf_out[j];
+    }
+    double tmax = -1.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (pc[k] == 1) tmax = mm[k] > tmax ? mm[k] : tmax;
+    double dummy_d;
+    const double exm = block_excl_scan_1<double>(tmax, -1.0, sh->d, OpMax(), &dummy_d);
+    bool ok[8];
+    double cafter[8];
+    long long vsum = 0;
+    {
+      double run = C > exm ? C : exm;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        ok[k] = pc[k] == 1 && cu[k] == run;
+        if (pc[k] == 1) run = mm[k] > run ? mm[k] : run;
+        cafter[k] = run;
+        vsum += ok[k] ? vv[k] : 0;
       }
-      const bool imp = ok && m > C;
-      const bool del = ok && kind == KIND_PREFIX && ast >= 0;
-      const bool over = ok && B >= 0 && V + cum >= B;
-      const unsigned special = __ballot_sync(HPK_FULL_MASK, (imp || del || over) && lane < first_bad);
-      const int first_sp = special ? __ffs(special) - 1 : 32;
-      int kc = first_bad;  // lanes [0, kc) are processed this chunk
-      if (first_sp < kc) kc = first_sp + 1;
-      const bool special_last = kc > 0 && first_sp == kc - 1;
-      bool overflow = false;  // budget runs out INSIDE the special lane: re-run it capped
-      if (special_last) {
-        const long long cum_l = shfl(cum, kc - 1);
-        const int over_l = shfl((int)over, kc - 1);
-        if (over_l && V + cum_l > B) overflow = true;
+    }
+    long long dummy_l;
+    const long long exv = block_excl_scan_1<long long>(vsum, 0, sh->l, OpAddL(), &dummy_l);
+    int fb = 1 << 30, fs = 1 << 30;
+    long long cum[8];
+    {
+      long long run = V + exv;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        run += ok[k] ? vv[k] : 0;
+        cum[k] = run;
+        const int r = r0 + k;
+        if (!ok[k] && r < fb) fb = r;
+        const bool del = (inf[k] & 512) != 0;
+        const bool over = B >= 0 && run >= B;
+        if (ok[k] && (del || over) && r < fs) fs = r;
       }
-      const int kcommit = overflow ? kc - 1 : kc;
-      // merge bests of [0, kcommit): (obj desc, G asc, index asc)
+    }
+    if (fb > tile) fb = tile;
+    if (tid == 0) {
+      sh->fb = 1 << 30;
+      sh->fs = 1 << 30;
+    }
+    __syncthreads();
+    atomicMin(&sh->fb, fb);
+    atomicMin(&sh->fs, fs);
+    __syncthreads();
+    const int FB = sh->fb, FS = sh->fs;
+    const bool special_last = FS < FB;
+    const int kc = special_last ? FS + 1 : FB;  // relative positions [0, kc) are processed
+    // the thread owning position kc-1 publishes the state after it
+    if (kc > 0 && (kc - 1) >> 3 == tid) {
+      const int k = (kc - 1) & 7;
+      sh->v_after = cum[k];
+      sh->c_after = cafter[k];
+      sh->v_before = cum[k] - vv[k];
+      sh->c_before = k > 0 ? cafter[k - 1] : (C > exm ? C : exm);
+      sh->sp_del = (inf[k] & 512) != 0;
+    }
+    __syncthreads();
+    bool overflow = false;  // budget runs out INSIDE the special position: re-run it capped
+    if (special_last && B >= 0 && sh->v_after > B) overflow = true;
+    const int kcommit = overflow ? kc - 1 : kc;
+    // best over the committed positions: (obj desc, G asc, position asc)
+    {
       double ko = -1;
       int kg = 0, ki = 1 << 30;
-      if (lane < kcommit && hb) {
-        ko = bo;
-        kg = bg;
-        ki = lane;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int r = r0 + k;
+        if (r < kcommit && (inf[k] & 256)) {
+          const double bo = bo_out[i + r];
+          const int bg = inf[k] & 255;
+          if (ko < 0 || key_better(bo, bg, r, ko, kg, ki)) {
+            ko = bo;
+            kg = bg;
+            ki = r;
+          }
+        }
       }
-      double mm = (lane < kcommit) ? m : -1.0;
 #pragma unroll
       for (int o2 = 16; o2 > 0; o2 >>= 1) {
         const double oo = __shfl_xor_sync(HPK_FULL_MASK, ko, o2);
@@ -1272,37 +1499,62 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
           kg = og;
           ki = oi;
         }
-        const double om = __shfl_xor_sync(HPK_FULL_MASK, mm, o2);
-        mm = om > mm ? om : mm;
       }
-      const int gh = *((volatile int*)&S.has_best);
-      const double gbo = *((volatile double*)&S.best_obj);
-      const int gbg = *((volatile int*)&S.best_G);
-      if (ko >= 0 && (!gh || ko > gbo || (ko == gbo && kg < gbg))) {
-        const Entry& w = pool[ids_out[i + ki]];
-        for (int t = lane; t < P.n; t += 32) S.best_rgs[t] = w.best_rgs[t];
-        if (lane == 0) {
-          S.has_best = 1;
-          S.best_obj = ko;
-          S.best_G = kg;
+      if (lane == 0) {
+        sh->bo[warp] = ko;
+        sh->bg[warp] = kg;
+        sh->bi[warp] = ki;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        const int nw = blockDim.x >> 5;
+        ko = lane < nw ? sh->bo[lane] : -1.0;
+        kg = lane < nw ? sh->bg[lane] : 0;
+        ki = lane < nw ? sh->bi[lane] : (1 << 30);
+#pragma unroll
+        for (int o2 = 16; o2 > 0; o2 >>= 1) {
+          const double oo = __shfl_xor_sync(HPK_FULL_MASK, ko, o2);
+          const int og = __shfl_xor_sync(HPK_FULL_MASK, kg, o2);
+          const int oi = __shfl_xor_sync(HPK_FULL_MASK, ki, o2);
+          if (oo >= 0 && (ko < 0 || key_better(oo, og, oi, ko, kg, ki))) {
+            ko = oo;
+            kg = og;
+            ki = oi;
+          }
+        }
+        const int gh = S.has_best;
+        const double gbo = S.best_obj;
+        const int gbg = S.best_G;
+        if (ko >= 0 && (!gh || ko > gbo || (ko == gbo && kg < gbg))) {
+          const Entry& w = pool[ids_out[i + ki]];
+          for (int t = lane; t < P.n; t += 32) S.best_rgs[t] = w.best_rgs[t];
+          if (lane == 0) {
+            S.has_best = 1;
+            S.best_obj = ko;
+            S.best_G = kg;
+          }
         }
       }
-      __syncwarp();
-      if (kcommit > 0) V += shfl(cum, kcommit - 1);
-      if (mm > C) {
-        C = mm;
+    }
+    if (kcommit > 0) {
+      const double cn = (kcommit == kc) ? sh->c_after : sh->c_before;
+      V = (kcommit == kc) ? sh->v_after : sh->v_before;
+      if (cn > C) {
+        C = cn;
         ++cver;
       }
-      i += kcommit;
-      if (overflow) {
-        rerun = 1;
-        rerun_cap = B - V;
-        break;
-      }
-      if (special_last) {
-        const int jl = i - 1;  // the special entry, now committed
-        const int del_l = shfl((int)del, kc - 1);
-        if (del_l) {
+    }
+    i += kcommit;
+    if (overflow) {
+      rerun = 1;
+      rerun_cap = B - V;
+      __syncthreads();
+      break;
+    }
+    if (special_last) {
+      const int jl = i - 1;  // the special entry, now committed
+      if (sh->sp_del) {
+        if (warp == 0) {
           const Entry& e = pool[ids_out[jl]];
           const int la = e.a_star;
           int ndel = 0;
@@ -1318,48 +1570,50 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
             ndel += firstout;
             if (firstout < 32) break;
           }
-          i += ndel;
+          if (lane == 0) sh->ndel = ndel;
         }
-        if (B >= 0 && V == B) {
-          done = 1;
-          aborted = i < total ? 1 : 0;
-          break;
-        }
-        // after an improvement or a deletion the walk continues; every later
-        // position is re-checked against the updated exact cutoff C
-        continue;
+        __syncthreads();
+        i += sh->ndel;
       }
-      if (kc < 32) break;  // reached a position that still needs a run
+      __syncthreads();
+      if (B >= 0 && V == B) {
+        done = 1;
+        aborted = i < total ? 1 : 0;
+        break;
+      }
+      continue;  // every later position is re-checked against the updated C
     }
-    if (lane == 0) {
-      if (kp.trace && kp.trace < 5 && (kp.trace_p < 0 || kp.trace_p == p) && S.waves < 200000)
-        printf("[hpk] wave %d p %d len %d total %d commit %d V %lld C %.17g pool %d head-pcv %d "
-               "head-cut %.17g head-uncapped %d\n",
-               S.waves, p, len, total, i, V, C, S.pool_top, total > i ? pcv_out[i] : -9,
-               total > i ? cut_out[i] : -9.0, total > i ? (int)pool[ids_out[i]].uncapped : -9);
-      S.C = C;
-      S.cver = cver;
-      S.V = V;
-      S.cur = cur ^ 1;
-      S.head = i;
-      S.len = total - i;
-      S.waves += 1;
-      S.max_list = max(S.max_list, total);
-      if (rerun) {
-        S.rerun_pending = 1;
-        S.rerun_cap = rerun_cap;
-      }
-      if (done) {
-        S.aborted = aborted;
-        finish_problem(kp, S);
-      } else if (!rerun && S.len == 0) {
-        S.aborted = 0;
-        finish_problem(kp, S);
-      }
-      sh_head = i;
-      sh_flag = (S.done ? 0 : 1) | (rerun ? 2 : 0);
-      sh_cap = rerun_cap;
+    __syncthreads();
+    if (kc < tile) break;  // reached a position that still needs a run
+  }
+  if (tid == 0) {
+    if (kp.trace && kp.trace < 5 && (kp.trace_p < 0 || kp.trace_p == p) && S.waves < 200000)
+      printf("[hpk] wave %d p %d len %d total %d extra %d commit %d V %lld C %.17g pool %d "
+             "head-pcv %d head-cut %.17g head-uncapped %d\n",
+             S.waves, p, len, total, etot, i, V, C, S.pool_top, total > i ? pcv_out[i] : -9,
+             total > i ? cut_out[i] : -9.0, total > i ? (int)pool[ids_out[i]].uncapped : -9);
+    S.C = C;
+    S.cver = cver;
+    S.V = V;
+    S.cur = cur ^ 1;
+    S.head = i;
+    S.len = total - i;
+    S.waves += 1;
+    S.max_list = max(S.max_list, total);
+    if (rerun) {
+      S.rerun_pending = 1;
+      S.rerun_cap = rerun_cap;
     }
+    if (done) {
+      S.aborted = aborted;
+      finish_problem(kp, S);
+    } else if (!rerun && S.len == 0) {
+      S.aborted = 0;
+      finish_problem(kp, S);
+    }
+    sh->head = i;
+    sh->flag = (S.done ? 0 : 1) | (rerun ? 2 : 0);
+    sh->cap = rerun_cap;
   }
   __syncthreads();
   if (kp.trace >= 5 && tid == 0) {
@@ -1368,8 +1622,8 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
     atomicAdd(kp.prof + 13, _t - _tprev);
     _tprev = _t;
   }
-  const int flag = sh_flag;
-  int nhead = sh_head;
+  const int flag = sh->flag;
+  int nhead = sh->head;
   const int nlen = total - nhead;
   // ---- C. pool compaction when the bump allocator is nearly exhausted
   if ((flag & 1) && S.pool_top > kp.pcap - 2 * kp.reserve - 64 * 32) {
@@ -1382,6 +1636,8 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
       vis_tmp[k] = vis_out[nhead + k];
       cut_in[k] = cut_out[nhead + k];
       m_in[k] = m_out[nhead + k];
+      inf_in[k] = inf_out[nhead + k];
+      bo_in[k] = bo_out[nhead + k];
     }
     __syncthreads();
     for (int k = tid; k < nlen; k += blockDim.x) {
@@ -1390,6 +1646,8 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
       vis_out[k] = vis_tmp[k];
       cut_out[k] = cut_in[k];
       m_out[k] = m_in[k];
+      inf_out[k] = inf_in[k];
+      bo_out[k] = bo_in[k];
       cnt_out[k] = 1;
     }
     __syncthreads();
@@ -1416,9 +1674,7 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
     const int qmax = max(32, kp.qmax / act);
     const long long bl = P.budget < 0 ? -1 : P.budget - S.V;
     push_items(kp, next_queue, p, ids_out, pcv_out, vis_out, cut_out, m_out,
-               pool_ptr(kp, p, S.pool_cur), nhead, nlen, S.C, qmax, bl,
-               reinterpret_cast<long long*>(smem_tmp + 64),
-               reinterpret_cast<double*>(smem_tmp + 96), smem_tmp);
+               pool_ptr(kp, p, S.pool_cur), nhead, nlen, S.C, qmax, bl, sh->l, sh->d, sh->i);
   }
   if (warp == 0) {
     if (flag & 2) {
@@ -1435,7 +1691,7 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
         it.pos = nhead;
         it.id = ids_out[nhead];
         it.front = 1;
-        it.cap = sh_cap;
+        it.cap = sh->cap;
         it.cut = S.C;
         }
       }
@@ -1447,6 +1703,12 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, int* 
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));
     atomicAdd(kp.prof + 15, _t - _tprev);
     _tprev = _t;
+  }
+  // expansion work items of the next wave: one per list tile
+  if (tid == 0 && !S.done && !(flag & 2)) {
+    const int nt = (S.len + TILE - 1) / TILE;
+    const int base = atomicAdd(kp.wcount + wnext, nt);
+    for (int t = 0; t < nt; ++t) kp.work[(size_t)wnext * kp.wcap + base + t] = make_int2(p, t);
   }
 }
 
@@ -1567,6 +1829,7 @@ __device__ void init_problem(const KParams& kp, int p) {
     S.waves = 0;
     S.runs = 0;
     S.run_visits = 0;
+    S.exact_checks = 0;
     S.max_list = 1;
     S.error = 0;
     // root node (not a visit): bound = sum of all powers, serially (:154-160)
@@ -1594,10 +1857,14 @@ __device__ void init_problem(const KParams& kp, int p) {
       list_vis(kp, p, 0)[0] = 0;
       list_dbl(kp, p, 0, 0)[0] = -1.0;
       list_dbl(kp, p, 0, 1)[0] = -1.0;
+      list_dbl(kp, p, 0, 2)[0] = -1.0;
+      list_arr(kp, p, 0, 4)[0] = 0;
       list_arr(kp, p, 0, 0)[0] = 0;   // id
       list_arr(kp, p, 0, 1)[0] = -1;  // needs a run
       list_arr(kp, p, 0, 2)[0] = 1;
       S.len = 1;
+      const int wi = atomicAdd(kp.wcount + 0, 1);
+      kp.work[wi] = make_int2(p, 0);
       RunQueue* q = kp.queues + 0;
       const int slot = atomicAdd(&q->len, 1);
       kp.items[slot].problem = p;
@@ -1642,10 +1909,17 @@ __device__ __forceinline__ void gsync(unsigned int* bar) {
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
+// 2 CTAs (16 warps) per SM: <= 128 registers per thread (HPK_REG_FREE=1 lifts the
+// bound: ~200 registers, 1 CTA per SM — an experiment knob)
+#ifdef HPK_REG_FREE
+#define HPK_WAVE_BOUNDS __launch_bounds__(BLOCK_THREADS)
+#else
+#define HPK_WAVE_BOUNDS __launch_bounds__(BLOCK_THREADS, 2)
+#endif
+__global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WarpSmem* wsm = reinterpret_cast<WarpSmem*>(smem_raw);
-  int* smem_tmp = reinterpret_cast<int*>(smem_raw + sizeof(WarpSmem) * WARPS_PER_BLOCK);
+  void* smem_tmp = smem_raw + sizeof(WarpSmem) * WARPS_PER_BLOCK;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1677,7 +1951,10 @@ __global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
       int it = 0;
       if (lane == 0) it = atomicAdd(&q->head, 1);
       it = shfl(it, 0);
-      if (it >= qlen) break;
+      if (it >= qlen) {  // queue drained: tell the runs still going to wrap up
+        if (lane == 0 && kp.minq > 0) *((volatile int*)kp.stop) = 1;
+        break;
+      }
       const RunItem item = items[it];
       const int p = item.problem;
       const GProb& P = kp.probs[p];
@@ -1686,9 +1963,12 @@ __global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
       const double C = item.cut;
       const int cver = 1;
       const PView PV = stage_problem(P, wsm + warp, lane);
+      // (a PREFIX re-run must end at its end marker: it is never split)
+      const bool stoppable =
+          kp.minq > 0 && !E->capped && !E->uncapped && E->kind != KIND_PREFIX;
       RunOut o = run_segment(PV, E, E, C, item.cap, wsm + warp, lane, kp.err, kp.deadline_ns,
                               (kp.trace >= 2 && kp.trace < 5) ? kp.prof : nullptr,
-                              kp.trace == 3);
+                              stoppable ? kp.stop : nullptr, kp.minq);
       int* pcv = list_arr(kp, p, S.cur, 1);
       int* cnt = list_arr(kp, p, S.cur, 2);
       int* pfirst = list_arr(kp, p, S.cur, 3);
@@ -1717,6 +1997,12 @@ __global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
           list_vis(kp, p, S.cur)[item.pos] = o.visits;
           list_dbl(kp, p, S.cur, 0)[item.pos] = C;
           list_dbl(kp, p, S.cur, 1)[item.pos] = o.m;
+          list_dbl(kp, p, S.cur, 2)[item.pos] = o.best_obj;
+          list_arr(kp, p, S.cur, 4)[item.pos] =
+              o.best_G | (o.has_best ? 256 : 0) |
+              ((E->kind == KIND_PREFIX && o.a_star >= 0) ? 512 : 0);
+          if (pieces > 0)
+            atomicAdd(kp.xt + (size_t)p * kp.xtn + (item.pos - S.head) / TILE, pieces);
         } else {
           E->cver = -1;
           E->finished = 0;
@@ -1725,6 +2011,7 @@ __global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
         }
         atomicAdd((unsigned long long*)&S.runs, 1ull);
         atomicAdd((unsigned long long*)&S.run_visits, (unsigned long long)o.visits);
+        if (o.exact) atomicAdd((unsigned long long*)&S.exact_checks, (unsigned long long)o.exact);
       }
       __syncwarp();
     }
@@ -1732,10 +2019,29 @@ __global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
     unsigned long long t_w1 = 0;
     if (kp.trace && blockIdx.x == 0 && threadIdx.x == 0)
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_w1));
-    // ---- schedule phase
+    // ---- schedule phase. S2: list expansion, every CTA takes tiles
+    {
+      const int wb = wave & 1;
+      if (blockIdx.x == 0 && threadIdx.x == 0) kp.wcount[wb ^ 1] = 0;
+      const int nwk = *((volatile int*)(kp.wcount + wb));
+      SchedSmem* sh = reinterpret_cast<SchedSmem*>(smem_tmp);
+      for (int w = blockIdx.x; w < nwk; w += gridDim.x) {
+        const int2 wk = kp.work[(size_t)wb * kp.wcap + w];
+        expand_tile(kp, wk.x, wk.y, sh);
+        __syncthreads();
+      }
+    }
+    gsync(kp.bar);
+    if (kp.trace >= 5 && blockIdx.x == 0 && threadIdx.x == 0) {
+      unsigned long long t_x;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_x));
+      atomicAdd(kp.prof + 18, t_x - t_w1);
+    }
+    // S3: commit, compaction, queue the next wave (one CTA per problem)
     for (int p = blockIdx.x; p < kp.n_problems; p += gridDim.x)
-      schedule_problem(kp, p, cur ^ 1, smem_tmp);
+      schedule_problem(kp, p, cur ^ 1, smem_tmp, (wave & 1) ^ 1);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
+      *((volatile int*)kp.stop) = 0;  // re-armed for the next run phase
       unsigned long long now;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
       if (now > kp.deadline_ns) {  // wall-clock watchdog: stop every block
@@ -1762,18 +2068,18 @@ __global__ void __launch_bounds__(BLOCK_THREADS) hpk_wave_kernel(KParams kp) {
   if (kp.trace >= 5 && blockIdx.x == 0 && threadIdx.x == 0) {
     const unsigned long long* q = kp.prof;
     printf("[hpk-sched] totals over all waves/problems (us): expand+scatter %.1f commit %.1f "
-           "compaction %.1f push %.1f | run phases %.1f schedule phases %.1f\n", q[12] * 1e-3,
-           q[13] * 1e-3, q[14] * 1e-3, q[15] * 1e-3, q[16] * 1e-3, q[17] * 1e-3);
+           "compaction %.1f push %.1f | run phases %.1f schedule phases %.1f (S2 expansion %.1f)\n",
+           q[12] * 1e-3, q[13] * 1e-3, q[14] * 1e-3, q[15] * 1e-3, q[16] * 1e-3, q[17] * 1e-3,
+           q[18] * 1e-3);
   }
   if (kp.trace >= 2 && kp.trace < 5 && blockIdx.x == 0 && threadIdx.x == 0) {
     const unsigned long long* q = kp.prof;
-    printf("[hpk-prof] leaf batches %llu (leaves %llu): %.1f cyc/batch | child checks %llu: %.1f "
-           "cyc/check (to owner-done %.1f, shuffles %.1f) | descend %.1f cyc/check | pop total "
-           "%llu cyc\n",
-           q[1], q[2], q[1] ? (double)q[0] / q[1] : 0.0, q[4], q[4] ? (double)q[3] / q[4] : 0.0,
-           q[4] ? (double)q[7] / q[4] : 0.0, q[4] ? (double)q[8] / q[4] : 0.0,
-           q[4] ? (double)q[5] / q[4] : 0.0, q[6]);
-    printf("[hpk-prof] exact fallbacks %llu\n", q[9]);
+    const unsigned long long vis = q[2] + q[4] + q[8];
+    printf("[hpk-prof] run cycles %llu, iterations %llu (%.1f cyc/iter), visits %llu (%.1f "
+           "cyc/visit) | leaf batches %llu (leaves %llu) | single checks %llu | prune skips %llu "
+           "(children %llu) | descends %llu pops %llu masks %llu exact %llu\n",
+           q[0], q[3], q[3] ? (double)q[0] / q[3] : 0.0, vis, vis ? (double)q[0] / vis : 0.0,
+           q[1], q[2], q[4], q[7], q[8], q[5], q[6], q[10], q[9]);
   }
 }
 
@@ -2007,6 +2313,10 @@ struct DeviceCtx {
   double* ldbl = nullptr;
   size_t cap_ldbl = 0;
   int* scratch = nullptr;
+  int* xt = nullptr;
+  size_t cap_xt = 0;
+  int2* work = nullptr;
+  size_t cap_work = 0;
   RunQueue* queues = nullptr;
   RunItem* items = nullptr;
   int* active = nullptr;
@@ -2039,7 +2349,7 @@ int ensure_ctx(DeviceCtx& c, int device) {
   cudaDeviceProp prop;
   HPK_CUDA(cudaGetDeviceProperties(&prop, device));
   c.sms = prop.multiProcessorCount;
-  const size_t smem = sizeof(WarpSmem) * WARPS_PER_BLOCK + sizeof(int) * (BLOCK_THREADS + 8);
+  const size_t smem = sizeof(WarpSmem) * WARPS_PER_BLOCK + sizeof(SchedSmem);
   HPK_CUDA(cudaFuncSetAttribute(hpk_wave_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
   int bps = 0;
@@ -2050,7 +2360,7 @@ int ensure_ctx(DeviceCtx& c, int device) {
   HPK_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
   HPK_CUDA(cudaEventCreate(&c.ev0));
   HPK_CUDA(cudaEventCreate(&c.ev1));
-  HPK_CUDA(cudaMalloc(&c.active, sizeof(int) * 32));
+  HPK_CUDA(cudaMalloc(&c.active, sizeof(int) * 64));
   HPK_CUDA(cudaMalloc(&c.queues, sizeof(RunQueue) * 2));
   c.device = device;
   return 0;
@@ -2206,6 +2516,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     results[i].segment_runs = 0;
     results[i].segment_visits = 0;
     results[i].max_list = 0;
+    results[i].exact_checks = 0;
     if (pr.n < 1) return fail(6, "grouping: no devices");
     if (pr.top_k > HPK_MAX_TOPK) return fail(6, "hetplan_b200: top_k above 16 unsupported");
     const bool contract = exact_sums(pr.power, pr.n, 0, false) &&
@@ -2217,14 +2528,14 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
   // ---------------- wave engine
   if (!wave_ix.empty()) {
     const int P = (int)wave_ix.size();
-    const long long seg_cap = cfg.segment_cap > 0 ? cfg.segment_cap : 1024;
+    const long long seg_cap = cfg.segment_cap > 0 ? cfg.segment_cap : 512;
     // list capacity (ids) and entry-pool capacity per problem; large by default
     // (the list must hold the whole speculative frontier), scaled down so that
     // big batches (cfg5 sweeps) stay within ~4 GB of HBM.
     int lcap = cfg.max_list > 0 ? cfg.max_list : (1 << 16);
     int pcap = 2 * lcap;
     while (lcap > 4096 &&
-           (size_t)P * ((size_t)pcap * 2 * sizeof(Entry) + (size_t)lcap * 84) > ((size_t)4 << 30)) {
+           (size_t)P * ((size_t)pcap * 2 * sizeof(Entry) + (size_t)lcap * 100) > ((size_t)4 << 30)) {
       lcap /= 2;
       pcap /= 2;
     }
@@ -2252,10 +2563,14 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     if (int rc = grow(c.probs, c.cap_probs, (size_t)P)) return rc;
     if (int rc = grow(c.states, c.cap_states, (size_t)P)) return rc;
     if (int rc = grow(c.pools, c.cap_pools, (size_t)P * 2 * pcap)) return rc;
-    if (int rc = grow(c.lists, c.cap_lists, (size_t)P * 2 * 4 * lcap)) return rc;
+    if (int rc = grow(c.lists, c.cap_lists, (size_t)P * 2 * 5 * lcap)) return rc;
     if (int rc = grow(c.scratch, c.cap_scratch, (size_t)P * (lcap + 1))) return rc;
     if (int rc = grow(c.lvis, c.cap_lvis, (size_t)P * 2 * lcap)) return rc;
-    if (int rc = grow(c.ldbl, c.cap_ldbl, (size_t)P * 4 * lcap)) return rc;
+    if (int rc = grow(c.ldbl, c.cap_ldbl, (size_t)P * 6 * lcap)) return rc;
+    const int xtn = lcap / TILE + 2;
+    if (int rc = grow(c.xt, c.cap_xt, (size_t)P * xtn)) return rc;
+    if (int rc = grow(c.work, c.cap_work, (size_t)2 * P * xtn)) return rc;
+    HPK_CUDA(cudaMemsetAsync(c.xt, 0, sizeof(int) * P * xtn, c.stream));
     const int grid = c.sms * c.blocks_per_sm;
     const int nwarps = grid * WARPS_PER_BLOCK;
     const int qmax = 2 * nwarps;  // total run slots per wave, shared by active problems
@@ -2265,9 +2580,10 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     HPK_CUDA(cudaMemcpyAsync(c.probs, hp.data(), sizeof(GProb) * P, cudaMemcpyHostToDevice,
                              c.stream));
     HPK_CUDA(cudaMemsetAsync(c.queues, 0, sizeof(RunQueue) * 2, c.stream));
-    int init_flags[32] = {0};
-    init_flags[0] = P;
-    HPK_CUDA(cudaMemcpyAsync(c.active, init_flags, sizeof(int) * 32, cudaMemcpyHostToDevice,
+    int init_flags[64] = {0};  // [0] active [1] err [2:4) deadline [4:6) barrier
+    init_flags[0] = P;         // [6] active snapshot [7] stop [8:60) trace counters
+                               // [60:62) expansion work counts
+    HPK_CUDA(cudaMemcpyAsync(c.active, init_flags, sizeof(int) * 64, cudaMemcpyHostToDevice,
                              c.stream));
     t_timing.h2d_bytes += sizeof(GProb) * P + sizeof(int);
 
@@ -2279,10 +2595,17 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     kp.lvis = c.lvis;
     kp.ldbl = c.ldbl;
     kp.scratch = c.scratch;
+    kp.xt = c.xt;
+    kp.xtn = xtn;
+    kp.work = c.work;
+    kp.wcap = P * xtn;
+    kp.wcount = c.active + 60;
     kp.queues = c.queues;
     kp.items = c.items;
     kp.active = c.active;
     kp.err = c.active + 1;
+    kp.stop = c.active + 7;
+    kp.minq = getenv("HPK_MINQ") ? atoll(getenv("HPK_MINQ")) : 0;
     kp.n_problems = P;
     kp.lcap = lcap;
     kp.pcap = pcap;
@@ -2297,7 +2620,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     kp.prof = reinterpret_cast<unsigned long long*>(c.active + 8);
     kp.trace = getenv("HPK_TRACE") ? atoi(getenv("HPK_TRACE")) : 0;
     kp.trace_p = getenv("HPK_TRACE_P") ? atoi(getenv("HPK_TRACE_P")) : -1;
-    const size_t smem = sizeof(WarpSmem) * WARPS_PER_BLOCK + sizeof(int) * (BLOCK_THREADS + 8);
+    const size_t smem = sizeof(WarpSmem) * WARPS_PER_BLOCK + sizeof(SchedSmem);
     void* args[] = {&kp};
     HPK_CUDA(cudaEventRecord(c.ev0, c.stream));
     HPK_CUDA(cudaLaunchCooperativeKernel((void*)hpk_wave_kernel, dim3(grid),
@@ -2328,6 +2651,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
       r.segment_runs = s.runs;
       r.segment_visits = s.run_visits;
       r.max_list = s.max_list;
+      r.exact_checks = s.exact_checks;
       r.visited = s.V;
       if (!s.done)
         return fail(5, "hetplan_b200: wave engine did not converge within " +

@@ -16,7 +16,7 @@ HPK_MAX_UNITS = 64
 HPK_MAX_TOPK = 16
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libhetplan_b200.so")
+LIB_PATH = os.environ.get("HPK_LIB") or os.path.join(PKG_DIR, "libhetplan_b200.so")
 
 
 class hpk_grouping_problem(C.Structure):
@@ -48,6 +48,7 @@ class hpk_grouping_result(C.Structure):
         ("segment_runs", C.c_longlong),
         ("segment_visits", C.c_longlong),
         ("max_list", C.c_int),
+        ("exact_checks", C.c_longlong),
     ]
 
 
@@ -108,6 +109,7 @@ class GroupingResult:
     segment_runs: int
     segment_visits: int
     max_list: int
+    exact_checks: int = 0
 
 
 class EngineError(RuntimeError):
@@ -186,5 +188,6 @@ class Engine:
             rgs = [[r.rgs[k * m + u] for u in range(m)] for k in range(r.count)]
             out.append(GroupingResult(r.status, r.count, bool(r.optimal), r.engine, r.visited,
                                       list(r.objective[:r.count]), list(r.z[:r.count]), rgs,
-                                      r.waves, r.segment_runs, r.segment_visits, r.max_list))
+                                      r.waves, r.segment_runs, r.segment_visits, r.max_list,
+                                      r.exact_checks))
         return out
