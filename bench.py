@@ -337,6 +337,166 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
+def _snapshot_inputs(lib, snaps):
+    cl = [lib.cluster_parse(w.cluster_json()) for w in snaps]
+    md = lib.model_parse(snaps[0].model_json())
+    pr = [lib.profile_synth(c, w.base_seconds, w.max_layers) for c, w in zip(cl, snaps)]
+    return cl, md, pr
+
+
+def _ref_plan_one(i):
+    """Worker of the cfg5 reference arm: one snapshot through the reference C ABI."""
+    from oracle.binding import REF_LIB
+    from paper_2512_20953_b200 import configs
+    from paper_2512_20953_b200.capi import HetplanLib
+    w = configs.cfg5_snapshots(i + 1)[i]
+    ref = HetplanLib(REF_LIB)
+    cl = ref.cluster_parse(w.cluster_json())
+    md = ref.model_parse(w.model_json())
+    pr = ref.profile_synth(cl, w.base_seconds, w.max_layers)
+    t0 = time.perf_counter()
+    ref.plan_compute(cl, md, pr).close()
+    return time.perf_counter() - t0
+
+
+def _cfg5_sample_visits():
+    with open(os.path.join(ROOT, "tests", "golden", "cfg5_visits.json")) as f:
+        return [r["visits"] for r in json.load(f)]
+
+
+def run_reference_cfg5(args):
+    """Reference planner over a bounded sample of the sweep on ALL host cores
+    (independent snapshots, one process each: the reference is single-threaded)."""
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    import multiprocessing as mp
+    vis = _cfg5_sample_visits()
+    cores = os.cpu_count() or 1
+    sample = min(len(vis), max(cores, 2 * cores))
+    times = []
+    with mp.get_context("spawn").Pool(cores) as pool:
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            pool.map(_ref_plan_one, range(sample))
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                times.append(dt)
+    ms = statistics.mean(times) * 1e3
+    value = sum(vis[:sample]) / (ms * 1e-3)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"cfg5 replanning sweep (sample of {sample} snapshots per step)",
+                   "parallelism": f"{cores} host processes", "options": "reference defaults"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"snapshots 0..{sample - 1} of the seed-2512 sweep per step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200_cfg5(args):
+    """The replanning sweep: every snapshot's plan search batched into one
+    hp_plan_compute_batch call per rank (snapshots sharded round-robin over ranks)."""
+    import torch
+    from paper_2512_20953_b200 import configs
+    from paper_2512_20953_b200.capi import HetplanLib
+    from paper_2512_20953_b200.engine import LIB_PATH, Engine
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    eng = Engine()
+    snaps = configs.cfg5_snapshots(args.snapshots)
+    mine = snaps[rank::world]
+    probs = [pb for w in mine for _, pb in tp_problems(w)]
+    lib = HetplanLib(LIB_PATH)
+    cl, md, pr = _snapshot_inputs(lib, mine)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    dev_ms, e2e_ms, launches, visits, h2d, d2h = [], [], 0, 0, 0, 0
+    for i in range(args.warmup + args.steps):
+        flush.zero_()
+        barrier()
+        eng.reset_timing()
+        res = eng.grouping_search(probs, device=local)
+        t = eng.timing()
+        flush.zero_()
+        barrier()
+        t0 = time.perf_counter()
+        out = lib.plan_compute_batch(cl, md, pr)
+        dt = time.perf_counter() - t0
+        te = eng.timing()
+        bad = [st for st, _, _ in out if st != 0]
+        if bad:
+            raise SystemExit(f"cfg5: {len(bad)} snapshots failed to plan")
+        barrier()
+        if i >= args.warmup:
+            dev_ms.append(t.search_ms + t.serial_ms)
+            e2e_ms.append(dt * 1e3)
+            launches += t.kernel_launches + te.kernel_launches
+            visits = sum(r.visited for r in res)
+            h2d += te.h2d_bytes
+            d2h += te.d2h_bytes
+    local_vals = [statistics.mean(dev_ms), statistics.mean(e2e_ms), float(visits)]
+    vals = [local_vals]
+    if dist is not None:
+        tt = torch.tensor(local_vals, dtype=torch.float64, device="cuda")
+        g = [torch.zeros_like(tt) for _ in range(world)]
+        dist.all_gather(g, tt)
+        vals = [[float(x) for x in v] for v in g]
+    if rank != 0:
+        dist.barrier()
+        dist.destroy_process_group()
+        return
+    dev_max = max(v[0] for v in vals)
+    e2e_max = max(v[1] for v in vals)
+    total_visits = sum(v[2] for v in vals)
+    with ClockSampler(local) as cs:
+        t_end = time.time() + 1.0
+        while time.time() < t_end:
+            eng.grouping_search(probs[: max(1, len(probs) // 8)], device=local)
+    # CPU baseline: the reference on 1 core over a small sample (scaled per visit)
+    svis = _cfg5_sample_visits()
+    k = min(4, len(svis))
+    ct = [_ref_plan_one(i) for i in range(k)]
+    cpu_value = sum(svis[:k]) / sum(ct)
+    line = {
+        "metric": METRIC, "value": total_visits / (dev_max * 1e-3), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": e2e_max,
+        "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"cfg5 replanning sweep: {args.snapshots} snapshots of the cfg3 "
+                   "cluster (seed 2512)", "parallelism": f"snapshots sharded over {world} GPU(s)",
+                   "options": "reference defaults", "l2": "flushed between timed iterations"},
+        "device_ms_per_step": dev_max,
+        "visits_per_step": total_visits,
+        "e2e": {"value": total_visits / (e2e_max * 1e-3), "unit": UNIT,
+                "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
+                "latency_ms": e2e_max},
+        "cpu_baseline": {"value": cpu_value, "unit": UNIT, "cores": 1, "kind": "reference",
+                         "sample": f"snapshots 0..{k - 1}, hp_plan_compute on 1 host core",
+                         "host_cores": os.cpu_count()},
+        "clocks": cs.summary(),
+        "gpu_launches": launches,
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def _cpu_model():
     try:
         with open("/proc/cpuinfo") as f:
@@ -354,9 +514,13 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4"])
+    ap.add_argument("--workload", default="cfg4",
+                    choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--snapshots", type=int, default=1000, help="cfg5 sweep size")
     args = ap.parse_args()
-    if args.impl == "reference":
+    if args.workload == "cfg5":
+        (run_reference_cfg5 if args.impl == "reference" else run_b200_cfg5)(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_b200(args)

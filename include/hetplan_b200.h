@@ -92,6 +92,19 @@ void hp_plan_options_init(hp_plan_options* options);                  /* c_api.h
 hp_status hp_plan_compute(const hp_cluster* cluster, const hp_model* model,
                           const hp_profile* profile, const hp_plan_options* options,
                           hp_plan** out);
+/* Extension (not in the reference ABI): hp_plan_compute over n clusters that
+ * share a model — e.g. the snapshots of a spot-preemption replanning sweep
+ * (SURVEY.md 8(d) cfg5). Every cluster's TP-dimension searches go into ONE
+ * grouping-search launch and every candidate into ONE partition/cost launch;
+ * the host phases (unit formation, stage mapping, selection) run on
+ * host_threads threads (<= 0: all cores). out_plans[i] / out_status[i] are
+ * what hp_plan_compute returns for cluster i; out_errors[i] (optional) is its
+ * error message or NULL (free with hp_string_free). Returns HP_OK unless an
+ * argument is invalid. Results equal n hp_plan_compute calls byte for byte. */
+hp_status hp_plan_compute_batch(int n, const hp_cluster* const* clusters, const hp_model* model,
+                                const hp_profile* const* profiles,
+                                const hp_plan_options* options, int host_threads,
+                                hp_plan** out_plans, hp_status* out_status, char** out_errors);
 hp_status hp_plan_load_file(const char* path, hp_plan** out);         /* c_api.h:94 */
 hp_status hp_plan_write_file(const hp_plan* plan, const char* path);  /* c_api.h:95 */
 hp_status hp_plan_to_json(const hp_plan* plan, char** out);           /* c_api.h:96 */

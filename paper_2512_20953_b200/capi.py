@@ -13,7 +13,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 from dataclasses import dataclass
-from typing import Optional, Sequence
+from typing import List, Optional, Sequence, Tuple
 
 HP_OK = 0
 HP_PARSE_ERROR = 2
@@ -98,6 +98,12 @@ class HetplanLib:
         L.hp_plan_options_init.argtypes = [C.POINTER(hp_plan_options)]
         L.hp_plan_compute.argtypes = [_VP, _VP, _VP, C.POINTER(hp_plan_options), C.POINTER(_VP)]
         L.hp_plan_compute.restype = C.c_int
+        if hasattr(L, "hp_plan_compute_batch"):  # product library only
+            L.hp_plan_compute_batch.argtypes = [C.c_int, C.POINTER(_VP), _VP, C.POINTER(_VP),
+                                                C.POINTER(hp_plan_options), C.c_int,
+                                                C.POINTER(_VP), C.POINTER(C.c_int),
+                                                C.POINTER(C.c_void_p)]
+            L.hp_plan_compute_batch.restype = C.c_int
         for name in ("hp_plan_to_json", "hp_plan_explain"):
             getattr(L, name).argtypes = [_VP, C.POINTER(C.c_void_p)]
             getattr(L, name).restype = C.c_int
@@ -144,6 +150,51 @@ class HetplanLib:
         h = _VP()
         self._check(self.lib.hp_profile_synth(cluster.ptr, base_seconds, max_layers, C.byref(h)))
         return Handle(self, h, "hp_profile_free")
+
+    def _options(self, options: Optional[PlanOptions], keep: list) -> hp_plan_options:
+        o = hp_plan_options()
+        self.lib.hp_plan_options_init(C.byref(o))
+        if options is not None:
+            if options.tp_dims is not None:
+                arr = (C.c_int * len(options.tp_dims))(*options.tp_dims)
+                keep.append(arr)
+                o.tp_dims = C.cast(arr, C.POINTER(C.c_int))
+                o.n_tp_dims = len(options.tp_dims)
+            o.min_mem_override = options.min_mem_override
+            o.exact_threshold = options.exact_threshold
+            o.node_budget = options.node_budget
+            o.top_k = options.top_k
+            o.sync_overlap_max = int(options.sync_overlap_max)
+            o.validate_with_sim = int(options.validate_with_sim)
+            o.derive_power = int(options.derive_power)
+            if options.power_reference is not None:
+                b = options.power_reference.encode()
+                keep.append(b)
+                o.power_reference = b
+        return o
+
+    def plan_compute_batch(self, clusters: List["Handle"], model: "Handle",
+                           profiles: List["Handle"], options: Optional[PlanOptions] = None,
+                           host_threads: int = 0) -> List[Tuple[int, Optional["Handle"], str]]:
+        """hp_plan_compute_batch: [(status, plan handle or None, error message)]."""
+        n = len(clusters)
+        keep: list = []
+        o = self._options(options, keep)
+        cl = (_VP * n)(*[c.ptr for c in clusters])
+        pr = (_VP * n)(*[p.ptr for p in profiles])
+        plans = (_VP * n)()
+        status = (C.c_int * n)()
+        errs = (C.c_void_p * n)()
+        rc = self.lib.hp_plan_compute_batch(n, cl, model.ptr, pr, C.byref(o), host_threads,
+                                            plans, status, errs)
+        if rc != HP_OK:
+            raise HetplanError(rc, "hp_plan_compute_batch: invalid arguments")
+        out = []
+        for i in range(n):
+            msg = self._take_string(errs[i]) if errs[i] else ""
+            h = Handle(self, _VP(plans[i]), "hp_plan_free") if plans[i] else None
+            out.append((status[i], h, msg))
+        return out
 
     def plan_compute(self, cluster: "Handle", model: "Handle", profile: "Handle",
                      options: Optional[PlanOptions] = None) -> "Handle":

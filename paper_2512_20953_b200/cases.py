@@ -66,7 +66,7 @@ def _case(name, cluster, model, max_layers, options=None, heavy=False):
                     heavy=heavy)
 
 
-def plan_cases(include_heavy: bool = True, n_snapshots: int = 6) -> list[PlanCase]:
+def plan_cases(include_heavy: bool = True, n_snapshots: int = 24) -> list[PlanCase]:
     out = []
     for name in ("cfg1", "cfg2", "cfg3", "cfg4"):
         w = configs.get(name)

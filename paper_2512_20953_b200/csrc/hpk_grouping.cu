@@ -88,14 +88,28 @@ struct GState {
   int cur, head, len;
   int done, aborted, rerun_pending, pool_cur;
   int pool_top;      // bump allocator of the active pool (atomic)
-  int pad0;
+  int nagg;          // expansion tiles summarised in agg (0: none valid)
   long long rerun_cap;
   double seed_obj, seed_z;
   int seed_ix, waves;
   long long runs, run_visits, exact_checks;
+  long long runs_prev;  // runs at the previous schedule (pieces-per-run estimate)
   int max_list, error;
   uint8_t best_rgs[MAXN];
   uint8_t seed_rgs[MAXN];
+};
+
+// Summary of one expansion tile's output range [ob, ob + n) of the new list,
+// written by expand_tile(): lets the commit walk and the queue scan pass a
+// fully run, cutoff-consistent tile in O(1) instead of re-reading it.
+struct TileAgg {
+  int ob, n;        // output range
+  int nrun, ndel;   // positions with a finished run; PREFIX re-runs that pruned an ancestor
+  double mmax;      // max objective over the runs (-1: none)
+  double cutc;      // the cutoff every run used (NaN: not all the same / none)
+  long long sumvis; // visits of the runs
+  double bobj;      // best candidate of the tile: (obj desc, G asc, position asc); -1: none
+  int bG, bidx;
 };
 
 struct RunItem {
@@ -122,12 +136,14 @@ struct KParams {
   int2* work;         // [2][wcap]: expansion work items (problem, tile) per wave parity
   int* wcount;        // [2]
   int xtn, wcap;
+  TileAgg* agg;       // [P][xtn]
   RunQueue* queues;   // [2]
   RunItem* items;     // [2][qcap]
   int* active;        // problems still running
   int* err;           // watchdog flags
   int* stop;          // run phase: the queue has drained (capped runs stop early)
   long long minq;     // ... after at least this many visits (0: never stop early)
+  unsigned long long wave_ns;  // run-phase time slice (0: none): later runs stop and split
   int n_problems;
   int lcap, pcap, qcap, qmax, reserve;
   long long seg_cap;
@@ -168,6 +184,7 @@ struct SchedSmem {
   long long v_after, v_before, cap;
   double c_after, c_before;
   int fb, fs, sp_del, ndel, head, flag;
+  double part[8 * 8];  // AggAcc partials (8 warps x 64 B)
 };
 
 // --------------------------------------------------------------- warp DFS
@@ -376,7 +393,7 @@ struct RunOut {
 __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, double C,
                               long long cap, WarpSmem* sm, int lane, int* err,
                               unsigned long long deadline, unsigned long long* prof,
-                              const int* stopf, long long minq) {
+                              const int* stopf, long long minq, unsigned long long wave_end) {
   // prof (trace >= 2): [0] run cycles [1] leaf batches [2] leaves [3] loop iterations
   //   [4] single checks [5] descends [6] pops [7] prune skips [8] children skipped
   //   [9] exact fallbacks [10] mask computations
@@ -501,6 +518,12 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
             o.finished = true;
             break;
           }
+        }
+        if (wave_end != 0) {  // the wave's time slice is over: stop at the next check
+          unsigned long long now;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+          now = __shfl_sync(HPK_FULL_MASK, now, 0);
+          if (now > wave_end && o.visits < cap) cap = o.visits;
         }
         if (stopf != nullptr) {
           const int s = shfl(stop_pending, 0);
@@ -980,22 +1003,48 @@ struct OpAddI {
 __device__ void push_items(const KParams& kp, int queue, int p, const int* ids, const int* pran,
                            const long long* pvis, const double* pcut, const double* pm,
                            const Entry* pool, int head, int len, double C, int qmax,
-                           long long budget_left, long long* shl, double* shd, int* shi) {
+                           long long budget_left, long long* shl, double* shd, int* shi,
+                           const TileAgg* ag, int nagg, int ashift) {
   const int tid = threadIdx.x;
   RunQueue* q = kp.queues + queue;
   RunItem* items = kp.items + (size_t)queue * kp.qcap;
   long long before = 0;  // lower bound of visits before the tile
   double cmax = C;       // predicted cutoff entering the tile
   int pushed = 0;
-  for (int base = 0; base < len; base += blockDim.x * 8) {
+  int ta = 0;  // tile-summary cursor (summaries are at buffer offset -ashift)
+  int base = 0;
+  while (base < len) {
+    if (nagg) {
+      // a summarised tile whose runs are all exact under the predicted cutoff
+      // queues nothing: pass it in O(1)
+      const int at = head + base;
+      while (ta < nagg && ag[ta].ob - ashift + ag[ta].n <= at) ++ta;
+      if (ta < nagg && ag[ta].ob - ashift == at) {
+        const TileAgg a = ag[ta];
+        if (a.nrun == a.n && a.mmax <= cmax && a.cutc == cmax) {
+          before += a.sumvis;
+          base += a.n;
+          ++ta;
+          if (kp.trace >= 5 && tid == 0) atomicAdd(kp.prof + 19, 1ull);
+          if (budget_left >= 0 && before >= budget_left) break;
+          continue;
+        }
+      }
+    }
+    const int lim = (nagg && ta < nagg) ? min(len, ag[ta].ob - ashift + ag[ta].n - head) : len;
+    const int jend = base + min(lim - base, (int)blockDim.x * 8);
     const int j0 = base + tid * 8;  // this thread's 8 consecutive positions
+    if (kp.trace >= 5 && tid == 0) {
+      atomicAdd(kp.prof + 20, 1ull);
+      atomicAdd(kp.prof + 21, (unsigned long long)(jend - base));
+    }
     bool ran[8];
     double mj[8], cj[8];
     long long vj[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int j = j0 + k;
-      ran[k] = j < len && pran[head + j] == 1;
+      ran[k] = j < jend && pran[head + j] == 1;
       mj[k] = ran[k] ? pm[head + j] : -1.0;
       cj[k] = ran[k] ? pcut[head + j] : -2.0;
       vj[k] = ran[k] ? pvis[head + j] : 0;
@@ -1015,8 +1064,8 @@ __device__ void push_items(const KParams& kp, int queue, int p, const int* ids, 
         chat[k] = run;
         run = mj[k] > run ? mj[k] : run;
         const bool exact = ran[k] && cj[k] == chat[k];
-        vj[k] = (j0 + k < len) ? (exact ? vj[k] : 1) : 0;
-        need[k] = (j0 + k < len) && !exact;
+        vj[k] = (j0 + k < jend) ? (exact ? vj[k] : 1) : 0;
+        need[k] = (j0 + k < jend) && !exact;
         vsum += vj[k];
       }
     }
@@ -1056,7 +1105,11 @@ __device__ void push_items(const KParams& kp, int queue, int p, const int* ids, 
             it.pos = head + j;
             it.id = id;
             it.front = (j == 0);
-            it.cap = pool[id].uncapped ? 0x3fffffffffffffffLL : kp.seg_cap;
+            // an uncapped (list-full) run is the head's: under a budget it
+            // needs at most budget_left + 1 visits to show the overflow
+            it.cap = !pool[id].uncapped ? kp.seg_cap
+                     : budget_left < 0  ? 0x3fffffffffffffffLL
+                                        : budget_left + 1;
             it.cut = chat[k];
           }
         }
@@ -1066,6 +1119,7 @@ __device__ void push_items(const KParams& kp, int queue, int p, const int* ids, 
     pushed += take;
     before += tile_vis;
     cmax = tile_max > cmax ? tile_max : cmax;
+    base = jend;
     __syncthreads();
     if (pushed >= qmax || (budget_left >= 0 && before >= budget_left)) break;
   }
@@ -1100,6 +1154,95 @@ __device__ __forceinline__ int xt_sums(const int* xt, int ntile, int t, SchedSme
   return all;
 }
 
+// Per-thread accumulator of a TileAgg, reduced over the CTA.
+struct AggAcc {
+  int nrun, ndel;
+  long long sumvis;
+  double mmax, cmin, cmax, bo;
+  int bg, bi;
+  __device__ void init() {
+    nrun = 0;
+    ndel = 0;
+    sumvis = 0;
+    mmax = -1.0;
+    cmin = INFINITY;
+    cmax = -INFINITY;
+    bo = -1.0;
+    bg = 0;
+    bi = 0x7fffffff;
+  }
+  __device__ void add(int pc, int inf, long long vis, double cut, double m, double bobj, int pos) {
+    if (pc != 1) return;
+    ++nrun;
+    ndel += (inf & 512) ? 1 : 0;
+    sumvis += vis;
+    mmax = m > mmax ? m : mmax;
+    cmin = cut < cmin ? cut : cmin;
+    cmax = cut > cmax ? cut : cmax;
+    if (inf & 256) {
+      const int g = inf & 255;
+      if (bo < 0 || key_better(bobj, g, pos, bo, bg, bi)) {
+        bo = bobj;
+        bg = g;
+        bi = pos;
+      }
+    }
+  }
+  __device__ void merge(const AggAcc& o) {
+    nrun += o.nrun;
+    ndel += o.ndel;
+    sumvis += o.sumvis;
+    mmax = o.mmax > mmax ? o.mmax : mmax;
+    cmin = o.cmin < cmin ? o.cmin : cmin;
+    cmax = o.cmax > cmax ? o.cmax : cmax;
+    if (o.bo >= 0 && (bo < 0 || key_better(o.bo, o.bg, o.bi, bo, bg, bi))) {
+      bo = o.bo;
+      bg = o.bg;
+      bi = o.bi;
+    }
+  }
+  __device__ void shfl_merge(int off) {
+    AggAcc o;
+    o.nrun = __shfl_xor_sync(HPK_FULL_MASK, nrun, off);
+    o.ndel = __shfl_xor_sync(HPK_FULL_MASK, ndel, off);
+    o.sumvis = __shfl_xor_sync(HPK_FULL_MASK, sumvis, off);
+    o.mmax = __shfl_xor_sync(HPK_FULL_MASK, mmax, off);
+    o.cmin = __shfl_xor_sync(HPK_FULL_MASK, cmin, off);
+    o.cmax = __shfl_xor_sync(HPK_FULL_MASK, cmax, off);
+    o.bo = __shfl_xor_sync(HPK_FULL_MASK, bo, off);
+    o.bg = __shfl_xor_sync(HPK_FULL_MASK, bg, off);
+    o.bi = __shfl_xor_sync(HPK_FULL_MASK, bi, off);
+    merge(o);
+  }
+};
+
+// CTA reduction of the accumulators; thread 0 writes the tile summary.
+__device__ void write_tile_agg(AggAcc acc, TileAgg* out, int ob, int n, SchedSmem* sh) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc.shfl_merge(off);
+  AggAcc* part = reinterpret_cast<AggAcc*>(sh->part);
+  if (lane == 0) part[warp] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) acc.merge(part[w]);
+    TileAgg a;
+    a.ob = ob;
+    a.n = n;
+    a.nrun = acc.nrun;
+    a.ndel = acc.ndel;
+    a.mmax = acc.mmax;
+    a.cutc = (acc.nrun > 0 && acc.cmin == acc.cmax) ? acc.cmin
+                                                     : __longlong_as_double(0x7ff8000000000000LL);
+    a.sumvis = acc.sumvis;
+    a.bobj = acc.bo;
+    a.bG = acc.bg;
+    a.bidx = acc.bi;
+    *out = a;
+  }
+  __syncthreads();
+}
+
 __device__ void expand_tile(const KParams& kp, int p, int t, SchedSmem* sh) {
   const GState& S = kp.states[p];
   const int tid = threadIdx.x;
@@ -1129,18 +1272,26 @@ __device__ void expand_tile(const KParams& kp, int p, int t, SchedSmem* sh) {
   double* __restrict__ cut_o = list_dbl(kp, p, cur ^ 1, 0) + ob;
   double* __restrict__ m_o = list_dbl(kp, p, cur ^ 1, 1) + ob;
   double* __restrict__ bo_o = list_dbl(kp, p, cur ^ 1, 2) + ob;
-  if (xt[t] == 0) {  // no split in this tile: shifted copy
+  AggAcc acc;
+  acc.init();
+  const int xtt = xt[t];
+  if (xtt == 0) {  // no split in this tile: shifted copy
 #pragma unroll 4
     for (int i = tid; i < n; i += blockDim.x) {
-      ids_o[i] = ids_i[i];
-      pcv_o[i] = pcv_i[i];
-      inf_o[i] = inf_i[i];
-      vis_o[i] = vis_i[i];
-      cut_o[i] = cut_i[i];
-      m_o[i] = m_i[i];
-      bo_o[i] = bo_i[i];
+      const int id = ids_i[i], pc = pcv_i[i], inf = inf_i[i];
+      const long long vv = vis_i[i];
+      const double cu = cut_i[i], mm = m_i[i], bb = bo_i[i];
+      ids_o[i] = id;
+      pcv_o[i] = pc;
+      inf_o[i] = inf;
+      vis_o[i] = vv;
+      cut_o[i] = cu;
+      m_o[i] = mm;
+      bo_o[i] = bb;
       cnt_o[i] = 1;
+      acc.add(pc, inf, vv, cu, mm, bb, ob + i);
     }
+    write_tile_agg(acc, kp.agg + (size_t)p * kp.xtn + t, ob, n, sh);
     return;
   }
   int* off = kp.scratch + (size_t)p * (kp.lcap + 1) + lo;
@@ -1177,6 +1328,7 @@ __device__ void expand_tile(const KParams& kp, int p, int t, SchedSmem* sh) {
         m_o[q] = mm[k];
         bo_o[q] = bb[k];
         cnt_o[q] = 1;
+        acc.add(pc[k], inf[k], vv[k], cu[k], mm[k], bb[k], ob + q);
         const int c = o[k + 1] - q;
         if (c > 1) {
           const int pf = pf_i[i0 + k];
@@ -1194,6 +1346,7 @@ __device__ void expand_tile(const KParams& kp, int p, int t, SchedSmem* sh) {
       }
     }
   }
+  write_tile_agg(acc, kp.agg + (size_t)p * kp.xtn + t, ob, tsum, sh);
 }
 
 // Per-problem scheduler (one CTA): expand splits, ordered commit, compaction,
@@ -1256,8 +1409,11 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
   const int etot = xt_sums(xt, ntile, 0, sh, &xt_before);
   for (int k = tid; k < ntile; k += blockDim.x) xt[k] = 0;  // re-armed for the next wave
   int total;
+  int nagg = 0;  // tile summaries of the new list (valid when expand_tile() expanded it)
+  const TileAgg* ag = kp.agg + (size_t)p * kp.xtn;
   if (len + etot <= kp.lcap - kp.reserve) {
     total = len + etot;  // expanded by expand_tile()
+    nagg = ntile;
   } else {
     const int mr = len;
     int* off = kp.scratch + (size_t)p * (kp.lcap + 1);
@@ -1395,8 +1551,42 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
   int i = 0;
   int done = 0, aborted = 0, rerun = 0;
   long long rerun_cap = 0;
+  int ta = 0;  // tile-summary cursor
   while (i < total) {
-    const int tile = min(total - i, (int)blockDim.x * 8);
+    if (nagg) {
+      // whole summarised tiles commit in O(1) when every position ran with the
+      // cutoff C, none improves on it, none deletes and the budget is not reached
+      while (ta < nagg && ag[ta].ob + ag[ta].n <= i) ++ta;
+      if (ta < nagg && ag[ta].ob == i) {
+        const TileAgg a = ag[ta];
+        if (a.nrun == a.n && a.ndel == 0 && a.mmax <= C && a.cutc == C &&
+            (B < 0 || V + a.sumvis < B)) {
+          if (a.bobj >= 0 && tid < 32) {
+            const int gh = S.has_best;
+            const double gbo = S.best_obj;
+            const int gbg = S.best_G;
+            if (!gh || a.bobj > gbo || (a.bobj == gbo && a.bG < gbg)) {
+              const Entry& w = pool[ids_out[a.bidx]];
+              for (int t = lane; t < P.n; t += 32) S.best_rgs[t] = w.best_rgs[t];
+              if (lane == 0) {
+                S.has_best = 1;
+                S.best_obj = a.bobj;
+                S.best_G = a.bG;
+              }
+            }
+          }
+          V += a.sumvis;
+          i += a.n;
+          ++ta;
+          if (kp.trace >= 5 && tid == 0) atomicAdd(kp.prof + 22, 1ull);
+          __syncthreads();
+          continue;
+        }
+      }
+    }
+    const int lim = (nagg && ta < nagg) ? ag[ta].ob + ag[ta].n : total;
+    const int tile = min(lim - i, (int)blockDim.x * 8);
+    if (kp.trace >= 5 && tid == 0) atomicAdd(kp.prof + 23, 1ull);
     const int r0 = tid * 8;  // this thread's positions, relative to i
     int pc[8], inf[8];
     double cu[8], mm[8];
@@ -1626,7 +1816,9 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
   int nhead = sh->head;
   const int nlen = total - nhead;
   // ---- C. pool compaction when the bump allocator is nearly exhausted
+  int ashift = 0;  // the list moves from [nhead, total) to [0, nlen)
   if ((flag & 1) && S.pool_top > kp.pcap - 2 * kp.reserve - 64 * 32) {
+    ashift = nhead;
     Entry* np = pool_ptr(kp, p, S.pool_cur ^ 1);
     int* pcv_tmp = list_arr(kp, p, cur, 1);  // the input buffer is free now
     long long* vis_tmp = vis_in;
@@ -1671,10 +1863,19 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
     // schedule phase (the live count drops as problems finish mid-phase; using it
     // let late schedulers over-push past qcap, starving problems)
     const int act = max(1, *((volatile int*)kp.active + 6));
-    const int qmax = max(32, kp.qmax / act);
+    // ... throttled by the list's headroom: each queued run may split, adding
+    // about as many pieces as this wave's runs did on average; a full list
+    // would revert splits (wasted runs) every wave
+    const long long runs_now = S.runs;
+    const long long dr = runs_now - S.runs_prev;
+    const int est = (int)min((long long)kp.reserve, max(1LL, (etot + dr - 1) / max(1LL, dr)));
+    const int headroom = kp.lcap - kp.reserve - nlen;
+    const int qmax = max(1, min(max(32, kp.qmax / act), headroom / est));
     const long long bl = P.budget < 0 ? -1 : P.budget - S.V;
     push_items(kp, next_queue, p, ids_out, pcv_out, vis_out, cut_out, m_out,
-               pool_ptr(kp, p, S.pool_cur), nhead, nlen, S.C, qmax, bl, sh->l, sh->d, sh->i);
+               pool_ptr(kp, p, S.pool_cur), nhead, nlen, S.C, qmax, bl, sh->l, sh->d, sh->i, ag,
+               nagg, ashift);
+    if (tid == 0) S.runs_prev = runs_now;
   }
   if (warp == 0) {
     if (flag & 2) {
@@ -1828,6 +2029,7 @@ __device__ void init_problem(const KParams& kp, int p) {
     S.rerun_pending = 0;
     S.waves = 0;
     S.runs = 0;
+    S.runs_prev = 0;
     S.run_visits = 0;
     S.exact_checks = 0;
     S.max_list = 1;
@@ -1944,6 +2146,11 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
     RunQueue* q = kp.queues + cur;
     RunItem* items = kp.items + (size_t)cur * kp.qcap;
     const int qlen = min(*((volatile int*)&q->len), kp.qcap);
+    unsigned long long wave_t0 = 0;  // this warp's view of the run phase start
+    if (kp.wave_ns) {
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(wave_t0));
+      wave_t0 = __shfl_sync(HPK_FULL_MASK, wave_t0, 0);
+    }
     unsigned long long t_w0 = 0;
     if (kp.trace && blockIdx.x == 0 && threadIdx.x == 0)
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_w0));
@@ -1964,17 +2171,21 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
       const int cver = 1;
       const PView PV = stage_problem(P, wsm + warp, lane);
       // (a PREFIX re-run must end at its end marker: it is never split)
-      const bool stoppable =
-          kp.minq > 0 && !E->capped && !E->uncapped && E->kind != KIND_PREFIX;
+      const bool stoppable = !E->capped && !E->uncapped && E->kind != KIND_PREFIX;
       RunOut o = run_segment(PV, E, E, C, item.cap, wsm + warp, lane, kp.err, kp.deadline_ns,
                               (kp.trace >= 2 && kp.trace < 5) ? kp.prof : nullptr,
-                              stoppable ? kp.stop : nullptr, kp.minq);
+                              stoppable && kp.minq > 0 ? kp.stop : nullptr, kp.minq,
+                              stoppable && kp.wave_ns ? wave_t0 + kp.wave_ns : 0ull);
       int* pcv = list_arr(kp, p, S.cur, 1);
       int* cnt = list_arr(kp, p, S.cur, 2);
       int* pfirst = list_arr(kp, p, S.cur, 3);
       int pieces = 0, first = 0;
       bool keep = true;
-      if (!o.finished && !E->capped) {
+      if (!o.finished && E->uncapped) {
+        // the head ran past the remaining budget: keep it as a finished run
+        // with budget_left + 1 visits; the commit walk re-runs it capped
+        o.finished = true;
+      } else if (!o.finished && !E->capped) {
         pieces = split_run(kp, p, S, E, o, wsm + warp, lane, item.front != 0, &first);
         keep = pieces > 0;  // pool full: drop the run, it re-runs later
       }
@@ -2071,6 +2282,8 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
            "compaction %.1f push %.1f | run phases %.1f schedule phases %.1f (S2 expansion %.1f)\n",
            q[12] * 1e-3, q[13] * 1e-3, q[14] * 1e-3, q[15] * 1e-3, q[16] * 1e-3, q[17] * 1e-3,
            q[18] * 1e-3);
+    printf("[hpk-sched] push: %llu tiles skipped, %llu chunks scanned (%llu positions) | commit: "
+           "%llu tiles skipped, %llu chunks\n", q[19], q[20], q[21], q[22], q[23]);
   }
   if (kp.trace >= 2 && kp.trace < 5 && blockIdx.x == 0 && threadIdx.x == 0) {
     const unsigned long long* q = kp.prof;
@@ -2317,6 +2530,8 @@ struct DeviceCtx {
   size_t cap_xt = 0;
   int2* work = nullptr;
   size_t cap_work = 0;
+  TileAgg* agg = nullptr;
+  size_t cap_agg = 0;
   RunQueue* queues = nullptr;
   RunItem* items = nullptr;
   int* active = nullptr;
@@ -2532,7 +2747,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     // list capacity (ids) and entry-pool capacity per problem; large by default
     // (the list must hold the whole speculative frontier), scaled down so that
     // big batches (cfg5 sweeps) stay within ~4 GB of HBM.
-    int lcap = cfg.max_list > 0 ? cfg.max_list : (1 << 16);
+    int lcap = cfg.max_list > 0 ? cfg.max_list : (1 << 17);
     int pcap = 2 * lcap;
     while (lcap > 4096 &&
            (size_t)P * ((size_t)pcap * 2 * sizeof(Entry) + (size_t)lcap * 100) > ((size_t)4 << 30)) {
@@ -2570,10 +2785,13 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     const int xtn = lcap / TILE + 2;
     if (int rc = grow(c.xt, c.cap_xt, (size_t)P * xtn)) return rc;
     if (int rc = grow(c.work, c.cap_work, (size_t)2 * P * xtn)) return rc;
+    if (int rc = grow(c.agg, c.cap_agg, (size_t)P * xtn)) return rc;
     HPK_CUDA(cudaMemsetAsync(c.xt, 0, sizeof(int) * P * xtn, c.stream));
     const int grid = c.sms * c.blocks_per_sm;
     const int nwarps = grid * WARPS_PER_BLOCK;
-    const int qmax = 2 * nwarps;  // total run slots per wave, shared by active problems
+    // total run slots per wave, shared by the active problems (most segments are
+    // small: several per warp keep the warps busy through the time slice)
+    const int qmax = (getenv("HPK_QMUL") ? atoi(getenv("HPK_QMUL")) : 2) * nwarps;
     const int qcap = qmax + 33 * P + 64;
     if (int rc = grow(c.items, c.cap_items, (size_t)2 * qcap)) return rc;
 
@@ -2597,6 +2815,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     kp.scratch = c.scratch;
     kp.xt = c.xt;
     kp.xtn = xtn;
+    kp.agg = c.agg;
     kp.work = c.work;
     kp.wcap = P * xtn;
     kp.wcount = c.active + 60;
@@ -2606,6 +2825,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     kp.err = c.active + 1;
     kp.stop = c.active + 7;
     kp.minq = getenv("HPK_MINQ") ? atoll(getenv("HPK_MINQ")) : 0;
+    kp.wave_ns = getenv("HPK_WAVE_US") ? (unsigned long long)(atof(getenv("HPK_WAVE_US")) * 1000.0) : 0ull;
     kp.n_problems = P;
     kp.lcap = lcap;
     kp.pcap = pcap;

@@ -15,6 +15,12 @@
 // stage_map.cpp:63-216) and plan assembly/validation. There is no CPU
 // fallback: without a CUDA device plan_cluster throws InternalError.
 #include <algorithm>
+#include <atomic>
+#include <cstdlib>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <thread>
 #include <cmath>
 #include <iostream>
 #include <map>
@@ -131,15 +137,55 @@ struct TpWork {
   throw InternalError(m);
 }
 
-}  // namespace
+// One plan_cluster call, split at its two GPU launches so that many calls
+// (a replanning sweep) share one grouping-search launch and one
+// partition/cost launch (hp_plan_compute_batch).
+struct PlanJob {
+  const ClusterSpec& spec;
+  const ModelConfig& cfg;
+  const ProfileTable& profile;
+  const MemoryModel& memmodel;
+  const PlannerOptions& options;
+  std::vector<int> tp_dims, valid;
+  std::optional<std::map<std::string, double>> derived;
+  std::map<std::string, int> type_key;
+  std::vector<TpWork> work;
+  std::vector<hpk_grouping_problem> problems;
+  std::vector<std::vector<double>> pw, pm;
+  std::vector<std::vector<int>> tk, nk;
+  std::vector<hpk_grouping_result> gres;
+  std::vector<std::vector<int>> rgs_buf;
+  std::vector<Candidate> cands;
+  std::vector<hpk_plan_candidate> pin;
+  std::vector<int> pin_of;
+  std::vector<hpk_plan_result> pres;
+  std::exception_ptr error;  // raised by a phase; the job is finished
+  std::optional<ParallelPlan> plan;
+  PlanJob(const ClusterSpec& s, const ModelConfig& c, const ProfileTable& p, const MemoryModel& m,
+          const PlannerOptions& o)
+      : spec(s), cfg(c), profile(p), memmodel(m), options(o) {}
+};
 
-ParallelPlan plan_cluster(const ClusterSpec& spec, const ModelConfig& cfg,
-                          const ProfileTable& profile, const MemoryModel& memmodel,
-                          const PlannerOptions& options) {
-  hpk_reset_timing();
+// planner.cpp:116-133 and phase 1: per-TP prechecks in the reference's order
+void job_prepare(PlanJob& J) {
+  const ClusterSpec& spec = J.spec;
+  const ModelConfig& cfg = J.cfg;
+  const ProfileTable& profile = J.profile;
+  const MemoryModel& memmodel = J.memmodel;
+  const PlannerOptions& options = J.options;
+  auto& tp_dims = J.tp_dims;
+  auto& valid = J.valid;
+  auto& derived = J.derived;
+  auto& type_key = J.type_key;
+  auto& work = J.work;
+  auto& problems = J.problems;
+  auto& pw = J.pw;
+  auto& pm = J.pm;
+  auto& tk = J.tk;
+  auto& nk = J.nk;
   // planner.cpp:119-126
-  std::vector<int> tp_dims = options.tp_dims;
-  const std::vector<int> valid = enumerate_tp_dims(spec);
+  tp_dims = options.tp_dims;
+  valid = enumerate_tp_dims(spec);
   if (tp_dims.empty()) {
     tp_dims = valid;
   } else {
@@ -147,23 +193,18 @@ ParallelPlan plan_cluster(const ClusterSpec& spec, const ModelConfig& cfg,
     tp_dims.erase(std::unique(tp_dims.begin(), tp_dims.end()), tp_dims.end());
   }
   // planner.cpp:128-133
-  std::optional<std::map<std::string, double>> derived;
   if (options.derive_power) {
     std::string ref = options.power_reference;
     if (ref.empty()) ref = spec.gpu_types.begin()->first;
     derived = derive_power(profile, ref, 1);
   }
-  std::map<std::string, int> type_key;
   for (const auto& [name, t] : spec.gpu_types) {
     (void)t;
     type_key.emplace(name, (int)type_key.size());
   }
 
   // ---- phase 1: per-TP prechecks in the reference's order (grouping.cpp:270-289)
-  std::vector<TpWork> work(tp_dims.size());
-  std::vector<hpk_grouping_problem> problems;
-  std::vector<std::vector<double>> pw, pm;
-  std::vector<std::vector<int>> tk, nk;
+  work.assign(tp_dims.size(), TpWork{});
   problems.reserve(tp_dims.size());
   for (size_t w = 0; w < tp_dims.size(); ++w) {
     TpWork& tw = work[w];
@@ -236,25 +277,27 @@ ParallelPlan plan_cluster(const ClusterSpec& spec, const ModelConfig& cfg,
     problems[k].node_key = nk[k].data();
   }
 
-  // ---- phase 2: one batched GPU search over every TP dimension
-  std::vector<hpk_grouping_result> gres(problems.size());
-  std::vector<std::vector<int>> rgs_buf(problems.size());
+  J.gres.assign(problems.size(), hpk_grouping_result{});
+  J.rgs_buf.assign(problems.size(), {});
   for (size_t k = 0; k < problems.size(); ++k) {
-    rgs_buf[k].assign((size_t)problems[k].top_k * problems[k].n, 0);
-    gres[k].rgs = rgs_buf[k].data();
+    J.rgs_buf[k].assign((size_t)problems[k].top_k * problems[k].n, 0);
+    J.gres[k].rgs = J.rgs_buf[k].data();
   }
-  if (!problems.empty()) {
-    if (hpk_device_count() <= 0) {
-      throw InternalError("hetplan_b200: no CUDA device visible; the B200 planner has no CPU "
-                          "fallback");
-    }
-    const int rc = hpk_grouping_search(problems.data(), (int)problems.size(), gres.data(),
-                                       nullptr);
-    if (rc != 0) gpu_fail(rc);
-  }
+}
 
-  // ---- phase 3: groupings -> stage mapping -> candidate inputs (host)
-  std::vector<Candidate> cands;
+// phase 3: groupings -> stage mapping -> candidate inputs (host)
+void job_candidates(PlanJob& J) {
+  const ClusterSpec& spec = J.spec;
+  const ModelConfig& cfg = J.cfg;
+  const ProfileTable& profile = J.profile;
+  const MemoryModel& memmodel = J.memmodel;
+  const PlannerOptions& options = J.options;
+  auto& work = J.work;
+  auto& gres = J.gres;
+  auto& cands = J.cands;
+  auto& pin = J.pin;
+  auto& pin_of = J.pin_of;
+  auto& pres = J.pres;
   for (auto& tw : work) {
     if (tw.problem < 0) continue;
     const hpk_grouping_result& r = gres[tw.problem];
@@ -294,8 +337,7 @@ ParallelPlan plan_cluster(const ClusterSpec& spec, const ModelConfig& cfg,
   }
   int n_bits = 0;
   while ((1 << n_bits) <= cfg.n_layers) ++n_bits;
-  std::vector<hpk_plan_candidate> pin;
-  std::vector<int> pin_of(cands.size(), -1);
+  pin_of.assign(cands.size(), -1);
   for (size_t ci = 0; ci < cands.size(); ++ci) {
     Candidate& c = cands[ci];
     if (c.map_error.kind != Pending::NONE) continue;
@@ -359,8 +401,8 @@ ParallelPlan plan_cluster(const ClusterSpec& spec, const ModelConfig& cfg,
     pin_of[ci] = (int)pin.size();
     pin.push_back(p);
   }
-  // ---- phase 4: one batched GPU launch for every candidate's partition + cost
-  std::vector<hpk_plan_result> pres(pin.size());
+  // result buffers of the batched partition + cost launch (phase 4)
+  pres.assign(pin.size(), hpk_plan_result{});
   for (size_t ci = 0; ci < cands.size(); ++ci) {
     if (pin_of[ci] < 0) continue;
     Candidate& c = cands[ci];
@@ -373,12 +415,18 @@ ParallelPlan plan_cluster(const ClusterSpec& spec, const ModelConfig& cfg,
     r.group_total = c.total.data();
     r.group_bubble = c.bubble.data();
   }
-  if (!pin.empty()) {
-    const int rc = hpk_partition_cost(pin.data(), (int)pin.size(), pres.data(), -1);
-    if (rc != 0) gpu_fail(rc);
-  }
+}
 
-  // ---- phase 5: the reference's selection loop (planner.cpp:138-205), replayed
+// phase 5: the reference's selection loop (planner.cpp:138-205), replayed
+ParallelPlan job_select(PlanJob& J) {
+  const ClusterSpec& spec = J.spec;
+  const ModelConfig& cfg = J.cfg;
+  const ProfileTable& profile = J.profile;
+  const PlannerOptions& options = J.options;
+  auto& work = J.work;
+  auto& cands = J.cands;
+  auto& pres = J.pres;
+  auto& pin_of = J.pin_of;
   std::optional<ParallelPlan> best;
   std::vector<CandidateSummary> summaries;
   for (auto& tw : work) {
@@ -502,4 +550,198 @@ ParallelPlan plan_cluster(const ClusterSpec& spec, const ModelConfig& cfg,
   return *best;
 }
 
+// Runs fn(job) for every unfinished job on up to `threads` host threads; an
+// exception finishes that job.
+template <typename Fn>
+void for_jobs(std::vector<PlanJob*>& jobs, int threads, Fn&& fn) {
+  std::atomic<size_t> next{0};
+  auto worker = [&] {
+    for (size_t i = next++; i < jobs.size(); i = next++) {
+      PlanJob& J = *jobs[i];
+      if (J.error || J.plan) continue;
+      try {
+        fn(J);
+      } catch (...) {
+        J.error = std::current_exception();
+      }
+    }
+  };
+  threads = std::max(1, std::min<int>(threads, (int)jobs.size()));
+  if (threads == 1) {
+    worker();
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t) pool.emplace_back(worker);
+  for (auto& t : pool) t.join();
+}
+
+// All jobs through the four phases with ONE grouping-search launch and ONE
+// partition/cost launch. A GPU failure fails every job that needed the GPU.
+void plan_jobs(std::vector<PlanJob*>& jobs, int threads) {
+  hpk_reset_timing();
+  for_jobs(jobs, threads, job_prepare);
+  // ---- phase 2: one batched GPU search over every TP dimension of every job
+  std::vector<hpk_grouping_problem> problems;
+  std::vector<std::pair<PlanJob*, size_t>> owner;
+  for (PlanJob* J : jobs) {
+    if (J->error) continue;
+    for (size_t k = 0; k < J->problems.size(); ++k) {
+      problems.push_back(J->problems[k]);
+      owner.emplace_back(J, k);
+    }
+  }
+  if (!problems.empty()) {
+    std::vector<hpk_grouping_result> gres(problems.size());
+    for (size_t i = 0; i < problems.size(); ++i) gres[i] = owner[i].first->gres[owner[i].second];
+    try {
+      if (hpk_device_count() <= 0) {
+        throw InternalError("hetplan_b200: no CUDA device visible; the B200 planner has no CPU "
+                            "fallback");
+      }
+      const int rc = hpk_grouping_search(problems.data(), (int)problems.size(), gres.data(),
+                                         nullptr);
+      if (rc != 0) gpu_fail(rc);
+    } catch (...) {
+      for (auto& o : owner) o.first->error = std::current_exception();
+      return;
+    }
+    for (size_t i = 0; i < problems.size(); ++i) owner[i].first->gres[owner[i].second] = gres[i];
+  }
+  for_jobs(jobs, threads, job_candidates);
+  // ---- phase 4: one batched GPU launch for every candidate's partition + cost
+  std::vector<hpk_plan_candidate> pin;
+  std::vector<hpk_plan_result> pres;
+  std::vector<std::pair<PlanJob*, size_t>> powner;
+  for (PlanJob* J : jobs) {
+    if (J->error) continue;
+    for (size_t k = 0; k < J->pin.size(); ++k) {
+      pin.push_back(J->pin[k]);
+      pres.push_back(J->pres[k]);
+      powner.emplace_back(J, k);
+    }
+  }
+  if (!pin.empty()) {
+    try {
+      const int rc = hpk_partition_cost(pin.data(), (int)pin.size(), pres.data(), -1);
+      if (rc != 0) gpu_fail(rc);
+    } catch (...) {
+      for (auto& o : powner) o.first->error = std::current_exception();
+      return;
+    }
+    for (size_t i = 0; i < pin.size(); ++i) powner[i].first->pres[powner[i].second] = pres[i];
+  }
+  for_jobs(jobs, threads, [](PlanJob& J) { J.plan = job_select(J); });
+}
+
+}  // namespace
+
+ParallelPlan plan_cluster(const ClusterSpec& spec, const ModelConfig& cfg,
+                          const ProfileTable& profile, const MemoryModel& memmodel,
+                          const PlannerOptions& options) {
+  PlanJob job(spec, cfg, profile, memmodel, options);
+  std::vector<PlanJob*> jobs{&job};
+  plan_jobs(jobs, 1);
+  if (job.error) std::rethrow_exception(job.error);
+  return std::move(*job.plan);
+}
+
 }  // namespace hetplan
+
+// ------------------------------------------------------------------ batch C ABI
+// The reference's opaque handles (P/src/c_api.cpp:35-47), same definitions.
+struct hp_cluster {
+  hetplan::ClusterSpec spec;
+};
+struct hp_model {
+  hetplan::ModelConfig config;
+  hetplan::MemoryModel memory;
+};
+struct hp_profile {
+  hetplan::ProfileTable table;
+};
+struct hp_plan {
+  hetplan::ParallelPlan plan;
+};
+
+namespace {
+hp_status status_of(const std::exception_ptr& e, std::string* msg) {
+  try {
+    std::rethrow_exception(e);
+  } catch (const hetplan::ParseError& x) {
+    *msg = x.what();
+    return HP_PARSE_ERROR;
+  } catch (const hetplan::InfeasibleError& x) {
+    *msg = x.what();
+    return HP_INFEASIBLE;
+  } catch (const hetplan::UnrecoverableError& x) {
+    *msg = x.what();
+    return HP_UNRECOVERABLE;
+  } catch (const hetplan::InvalidArgumentError& x) {
+    *msg = x.what();
+    return HP_INVALID_ARGUMENT;
+  } catch (const std::exception& x) {
+    *msg = x.what();
+    return HP_INTERNAL_ERROR;
+  } catch (...) {
+    *msg = "unknown error";
+    return HP_INTERNAL_ERROR;
+  }
+}
+}  // namespace
+
+extern "C" hp_status hp_plan_compute_batch(int n, const hp_cluster* const* clusters,
+                                           const hp_model* model,
+                                           const hp_profile* const* profiles,
+                                           const hp_plan_options* options, int host_threads,
+                                           hp_plan** out_plans, hp_status* out_status,
+                                           char** out_errors) {
+  if (n < 0 || (n > 0 && (!clusters || !profiles || !out_plans || !out_status)) || !model) {
+    return HP_INVALID_ARGUMENT;
+  }
+  hetplan::PlannerOptions po;  // as hp_plan_compute (c_api.cpp:191-204)
+  if (options) {
+    for (int i = 0; i < options->n_tp_dims; ++i) po.tp_dims.push_back(options->tp_dims[i]);
+    po.min_mem_override = options->min_mem_override;
+    po.exact_threshold = options->exact_threshold;
+    po.node_budget = options->node_budget;
+    po.top_k = options->top_k;
+    po.sync_overlap = options->sync_overlap_max ? hetplan::SyncOverlap::max
+                                                : hetplan::SyncOverlap::sum;
+    po.validate_with_sim = options->validate_with_sim != 0;
+    po.derive_power = options->derive_power != 0;
+    if (options->power_reference) po.power_reference = options->power_reference;
+  }
+  try {
+    std::vector<std::unique_ptr<hetplan::PlanJob>> store;
+    std::vector<hetplan::PlanJob*> jobs;
+    for (int i = 0; i < n; ++i) {
+      if (!clusters[i] || !profiles[i]) return HP_INVALID_ARGUMENT;
+      store.push_back(std::make_unique<hetplan::PlanJob>(clusters[i]->spec, model->config,
+                                                         profiles[i]->table, model->memory, po));
+      jobs.push_back(store.back().get());
+    }
+    int threads = host_threads > 0 ? host_threads : (int)std::thread::hardware_concurrency();
+    hetplan::plan_jobs(jobs, std::max(1, threads));
+    for (int i = 0; i < n; ++i) {
+      out_plans[i] = nullptr;
+      std::string msg;
+      if (jobs[i]->error) {
+        out_status[i] = status_of(jobs[i]->error, &msg);
+      } else {
+        out_status[i] = HP_OK;
+        out_plans[i] = new hp_plan{std::move(*jobs[i]->plan)};
+      }
+      if (out_errors) {
+        out_errors[i] = nullptr;
+        if (!msg.empty()) {
+          out_errors[i] = static_cast<char*>(std::malloc(msg.size() + 1));
+          std::memcpy(out_errors[i], msg.c_str(), msg.size() + 1);
+        }
+      }
+    }
+  } catch (...) {
+    return HP_INTERNAL_ERROR;
+  }
+  return HP_OK;
+}

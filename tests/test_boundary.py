@@ -47,6 +47,20 @@ def test_no_gpu_fails_loudly(product_lib):
     assert "no CUDA device" in ei.value.message
 
 
+def test_no_gpu_batch_fails_loudly_per_cluster(product_lib):
+    from paper_2512_20953_b200.engine import Engine
+    if Engine(product_lib.path).device_count() > 0:
+        pytest.skip("GPU present: covered by the gpu tests")
+    from paper_2512_20953_b200 import configs
+    snaps = configs.cfg5_snapshots(3)
+    cl = [product_lib.cluster_parse(w.cluster_json()) for w in snaps]
+    md = product_lib.model_parse(snaps[0].model_json())
+    pr = [product_lib.profile_synth(c, 0.05, snaps[0].max_layers) for c in cl]
+    out = product_lib.plan_compute_batch(cl, md, pr, host_threads=2)
+    assert [(st, h) for st, h, _ in out] == [(HP_INTERNAL_ERROR, None)] * 3
+    assert all("no CUDA device" in msg for _, _, msg in out)
+
+
 def test_non_planner_abi_matches_reference(product_lib, ref_lib, golden_plans):
     # parse errors: same status and message
     for lib in (product_lib, ref_lib):

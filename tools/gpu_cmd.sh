@@ -1,5 +1,4 @@
-set -x
-timeout 1200 python -m pytest tests -x -q -m gpu 2>&1 | tail -5
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()"
-timeout 600 python bench.py > gpurun_out/bench2.json 2> gpurun_out/bench2.err; tail -3 gpurun_out/bench2.err; cat gpurun_out/bench2.json
-for w in cfg1 cfg2 cfg3; do HPK_MINQ=0 timeout 300 python tools/cap_sweep.py $w 256,512,1024; done
+timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -3
+timeout 600 python bench.py --workload cfg5 --snapshots 200 --steps 2 --warmup 1 2>gpurun_out/cfg5a.err | tail -1
+timeout 900 python bench.py --workload cfg5 --snapshots 1000 --steps 2 --warmup 1 2>gpurun_out/cfg5b.err | tail -1
+tail -3 gpurun_out/cfg5b.err
