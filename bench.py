@@ -209,8 +209,9 @@ def run_b200(args):
         raise SystemExit("no CUDA device")
     w = workload(args.workload)
     probs = tp_problems(w)
-    # shard the TP-dimension problems over ranks: budgeted searches first
-    mine = [pb for i, (tp, pb) in enumerate(probs) if i % world == rank]
+    # shard the TP-dimension problems over ranks (round-robin, budgeted dims first)
+    from paper_2512_20953_b200.shard import shard_indices, sharded_map
+    mine = [probs[i][1] for i in shard_indices(len(probs), rank, world)]
 
     def barrier():
         if dist is not None:
@@ -233,6 +234,11 @@ def run_b200(args):
             dev_ms.append(t.search_ms + t.serial_ms + t.partition_ms)
             launches += t.kernel_launches
             visits_done += sum(r.visited for r in res)
+    # every rank ends with the full, problem-ordered result list (one all-gather)
+    full = sharded_map([pb for _, pb in probs],
+                       lambda b: [(r.visited, r.optimal, r.objective, r.rgs)
+                                  for r in eng.grouping_search(b, device=local)], dist)
+    assert len(full) == len(probs)
     ms_local = statistics.mean(dev_ms) if dev_ms else 0.0
     ms_max = ms_local
     total_visits = visits_done / max(1, args.steps)
@@ -296,8 +302,15 @@ def run_b200(args):
     ref_visits, model_ops = visits_of(w)
     achieved = model_ops / (ms_max * 1e-3) / 1e9 if ms_max > 0 else 0.0
     peak = f64.value / 1e9
+    traffic = None
+    try:  # dram read+write per launch of the dominant kernel, from the committed ncu capture
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+            traffic = json.load(f)["hpk_wave_kernel"]["traffic_bytes_per_launch"]
+    except Exception:
+        pass
     roofline = {"bound": "fp64-issue", "achieved": achieved, "peak": peak, "unit": "GFLOP/s",
-                "frac": achieved / peak if peak else None, "traffic": None,
+                "frac": achieved / peak if peak else None, "traffic": traffic,
+                "traffic_unit": "bytes/launch (ncu dram__bytes_read+write, profiles/r1_traffic.json)",
                 "ops_per_launch": model_ops, "int32_peak_gops": i32.value / 1e9,
                 "peak_source": "measured (hpk_measure_issue_peaks: DMUL+DADD chains, this GPU)",
                 "note": "fp64-op model of SURVEY.md 8(d) (reference ops), whole plan search"}
@@ -413,8 +426,9 @@ def run_b200_cfg5(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     eng = Engine()
+    from paper_2512_20953_b200.shard import shard_indices
     snaps = configs.cfg5_snapshots(args.snapshots)
-    mine = snaps[rank::world]
+    mine = [snaps[i] for i in shard_indices(len(snaps), rank, world)]
     probs = [pb for w in mine for _, pb in tp_problems(w)]
     lib = HetplanLib(LIB_PATH)
     cl, md, pr = _snapshot_inputs(lib, mine)

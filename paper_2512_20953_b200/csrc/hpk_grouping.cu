@@ -2743,7 +2743,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
   // ---------------- wave engine
   if (!wave_ix.empty()) {
     const int P = (int)wave_ix.size();
-    const long long seg_cap = cfg.segment_cap > 0 ? cfg.segment_cap : 512;
+    const long long seg_cap = cfg.segment_cap > 0 ? cfg.segment_cap : 1024;
     // list capacity (ids) and entry-pool capacity per problem; large by default
     // (the list must hold the whole speculative frontier), scaled down so that
     // big batches (cfg5 sweeps) stay within ~4 GB of HBM.
@@ -2825,7 +2825,8 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     kp.err = c.active + 1;
     kp.stop = c.active + 7;
     kp.minq = getenv("HPK_MINQ") ? atoll(getenv("HPK_MINQ")) : 0;
-    kp.wave_ns = getenv("HPK_WAVE_US") ? (unsigned long long)(atof(getenv("HPK_WAVE_US")) * 1000.0) : 0ull;
+    // run-phase time slice: 200 us (HPK_WAVE_US overrides; 0 = none)
+    kp.wave_ns = (unsigned long long)((getenv("HPK_WAVE_US") ? atof(getenv("HPK_WAVE_US")) : 200.0) * 1000.0);
     kp.n_problems = P;
     kp.lcap = lcap;
     kp.pcap = pcap;

@@ -33,6 +33,7 @@
 namespace hpkp {
 
 constexpr int THREADS = 256;
+constexpr int MAXS = 128;  // stages per group with the feasible-prefix fast path
 
 struct Cand {
   int n_layers, tp, k_total, n_groups;
@@ -91,6 +92,8 @@ __global__ void __launch_bounds__(THREADS) partition_cost_kernel(Args a) {
   __shared__ int s_first_missing;
   __shared__ double s_bottleneck;
   __shared__ int s_status;
+  __shared__ int s_lmax[MAXS], s_lcnt[MAXS];  // per stage: largest / number of feasible l >= 1
+  __shared__ int s_prefix;                    // every stage's feasible set is [1, lmax]
   const int ci = blockIdx.x;
   const Cand c = a.cands[ci];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -167,6 +170,32 @@ __global__ void __launch_bounds__(THREADS) partition_cost_kernel(Args a) {
       __syncthreads();
       break;
     }
+    // (c0) memory feasibility per stage. estimate_memory is non-decreasing in l
+    // (each term is l times a positive constant, then /tp; rounding is monotone),
+    // so the l passing `bytes <= capacity` (partition.cpp:66) form a prefix
+    // [1, lmax]: the DP loop then needs no per-l memory model. Checked, not
+    // assumed: a non-prefix stage falls back to the per-l test.
+    const bool fast = P <= MAXS;
+    if (fast) {
+      for (int i = tid; i < P; i += blockDim.x) {
+        s_lmax[i] = 0;
+        s_lcnt[i] = 0;
+      }
+      if (tid == 0) s_prefix = 1;
+      __syncthreads();
+      for (int x = tid; x < P * L; x += blockDim.x) {
+        const int i = x / L, l = 1 + x % L;
+        if (stage_memory(c, l, a.stage_index[s0 + i], P) <= a.stage_cap[s0 + i]) {
+          atomicAdd(&s_lcnt[i], 1);
+          atomicMax(&s_lmax[i], l);
+        }
+      }
+      __syncthreads();
+      for (int i = tid; i < P; i += blockDim.x)
+        if (s_lcnt[i] != s_lmax[i]) s_prefix = 0;
+      __syncthreads();
+    }
+    const bool prefix = fast && s_prefix;
     // (c) DP, stage P-1 .. 0; thread r owns best[i][r]
     for (int r = tid; r < W; r += blockDim.x) best[(size_t)P * W + r] = r == 0 ? 0.0 : INFINITY;
     __syncthreads();
@@ -175,6 +204,27 @@ __global__ void __launch_bounds__(THREADS) partition_cost_kernel(Args a) {
       const int sidx = a.stage_index[s0 + i];
       const double cap = a.stage_cap[s0 + i];
       const double* nb = best + (size_t)(i + 1) * W;
+      if (prefix) {
+        const int lmax = s_lmax[i];
+        const double* tr = tt + ty * W;
+        for (int r = tid; r < W; r += blockDim.x) {
+          double b = INFINITY;
+          if (min_l == 0) {  // l = 0: time 0 (partition.cpp:68)
+            const double nv = nb[r];
+            if (nv != INFINITY) b = nv;  // max(0, nv) = nv (times are >= 0)
+          }
+          const int top = r < lmax ? r : lmax;
+          for (int l = 1; l <= top; ++l) {
+            const double nv = nb[r - l];
+            const double e = tr[l];
+            const double mx = e < nv ? nv : e;  // std::max(e, nv)
+            b = mx < b ? mx : b;                // std::min (an infinite nv never wins)
+          }
+          best[(size_t)i * W + r] = b;
+        }
+        __syncthreads();
+        continue;
+      }
       for (int r = tid; r < W; r += blockDim.x) {
         double b = INFINITY;
         for (int l = min_l; l <= r; ++l) {

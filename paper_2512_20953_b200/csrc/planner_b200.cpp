@@ -159,6 +159,7 @@ struct PlanJob {
   std::vector<hpk_plan_candidate> pin;
   std::vector<int> pin_of;
   std::vector<hpk_plan_result> pres;
+  int map_threads = 1;        // host threads for this job's stage mapping
   std::exception_ptr error;  // raised by a phase; the job is finished
   std::optional<ParallelPlan> plan;
   PlanJob(const ClusterSpec& s, const ModelConfig& c, const ProfileTable& p, const MemoryModel& m,
@@ -330,10 +331,22 @@ void job_candidates(PlanJob& J) {
       Candidate c;
       c.tp = tw.tp;
       c.grouping = &tw.groupings[k];
-      c.map_error = capture([&] { c.mapping = map_nodes_and_stages(spec, *c.grouping, tw.tp); });
       tw.cand_ix.push_back((int)cands.size());
       cands.push_back(std::move(c));
     }
+  }
+  // the reference stage mapper (stage_map.cpp:63-216; reentrant, up to ~7 ms
+  // for 64 units) runs for the candidates concurrently, one host thread each
+  auto map_one = [&](Candidate& c) {
+    c.map_error = capture([&] { c.mapping = map_nodes_and_stages(spec, *c.grouping, c.tp); });
+  };
+  if (cands.size() > 1 && J.map_threads > 1) {
+    std::vector<std::thread> pool;
+    for (size_t ci = 1; ci < cands.size(); ++ci) pool.emplace_back(map_one, std::ref(cands[ci]));
+    map_one(cands[0]);
+    for (auto& t : pool) t.join();
+  } else {
+    for (auto& c : cands) map_one(c);
   }
   int n_bits = 0;
   while ((1 << n_bits) <= cfg.n_layers) ++n_bits;
@@ -640,6 +653,7 @@ ParallelPlan plan_cluster(const ClusterSpec& spec, const ModelConfig& cfg,
                           const ProfileTable& profile, const MemoryModel& memmodel,
                           const PlannerOptions& options) {
   PlanJob job(spec, cfg, profile, memmodel, options);
+  job.map_threads = 8;  // a single plan: its candidates map concurrently
   std::vector<PlanJob*> jobs{&job};
   plan_jobs(jobs, 1);
   if (job.error) std::rethrow_exception(job.error);
