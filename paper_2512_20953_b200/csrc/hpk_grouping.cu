@@ -144,6 +144,7 @@ struct KParams {
   int* stop;          // run phase: the queue has drained (capped runs stop early)
   long long minq;     // ... after at least this many visits (0: never stop early)
   unsigned long long wave_ns;  // run-phase time slice (0: none): later runs stop and split
+  int runners;        // warps per CTA that run segments (experiment knob; default all)
   int n_problems;
   int lcap, pcap, qcap, qmax, reserve;
   long long seg_cap;
@@ -519,18 +520,20 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
             break;
           }
         }
-        if (wave_end != 0) {  // the wave's time slice is over: stop at the next check
-          unsigned long long now;
-          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-          now = __shfl_sync(HPK_FULL_MASK, now, 0);
-          if (now > wave_end && o.visits < cap) cap = o.visits;
-        }
         if (stopf != nullptr) {
-          const int s = shfl(stop_pending, 0);
+          const int s = shfl(stop_pending, 0);  // the queue has drained
           if (lane == 0) stop_pending = *((volatile const int*)stopf);
           if (s) {
-            const long long lim = o.visits > minq ? o.visits : minq;
-            if (lim < cap) cap = lim;
+            if (minq > 0) {
+              const long long lim = o.visits > minq ? o.visits : minq;
+              if (lim < cap) cap = lim;
+            }
+            if (wave_end != 0) {  // ... and the wave's time slice is over: stop
+              unsigned long long now;
+              asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+              now = __shfl_sync(HPK_FULL_MASK, now, 0);
+              if (now > wave_end && o.visits < cap) cap = o.visits;
+            }
           }
         }
       }
@@ -2154,12 +2157,12 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
     unsigned long long t_w0 = 0;
     if (kp.trace && blockIdx.x == 0 && threadIdx.x == 0)
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_w0));
-    while (true) {
+    while (warp < kp.runners) {
       int it = 0;
       if (lane == 0) it = atomicAdd(&q->head, 1);
       it = shfl(it, 0);
       if (it >= qlen) {  // queue drained: tell the runs still going to wrap up
-        if (lane == 0 && kp.minq > 0) *((volatile int*)kp.stop) = 1;
+        if (lane == 0) *((volatile int*)kp.stop) = 1;
         break;
       }
       const RunItem item = items[it];
@@ -2174,7 +2177,7 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
       const bool stoppable = !E->capped && !E->uncapped && E->kind != KIND_PREFIX;
       RunOut o = run_segment(PV, E, E, C, item.cap, wsm + warp, lane, kp.err, kp.deadline_ns,
                               (kp.trace >= 2 && kp.trace < 5) ? kp.prof : nullptr,
-                              stoppable && kp.minq > 0 ? kp.stop : nullptr, kp.minq,
+                              stoppable ? kp.stop : nullptr, kp.minq,
                               stoppable && kp.wave_ns ? wave_t0 + kp.wave_ns : 0ull);
       int* pcv = list_arr(kp, p, S.cur, 1);
       int* cnt = list_arr(kp, p, S.cur, 2);
@@ -2825,6 +2828,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     kp.err = c.active + 1;
     kp.stop = c.active + 7;
     kp.minq = getenv("HPK_MINQ") ? atoll(getenv("HPK_MINQ")) : 0;
+    kp.runners = getenv("HPK_RUNNERS") ? atoi(getenv("HPK_RUNNERS")) : WARPS_PER_BLOCK;
     // run-phase time slice: 200 us (HPK_WAVE_US overrides; 0 = none)
     kp.wave_ns = (unsigned long long)((getenv("HPK_WAVE_US") ? atof(getenv("HPK_WAVE_US")) : 200.0) * 1000.0);
     kp.n_problems = P;
