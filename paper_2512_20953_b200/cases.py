@@ -97,6 +97,11 @@ def plan_cases(include_heavy: bool = True, n_snapshots: int = 24) -> list[PlanCa
         _case("opt-exhaustive-12", CLUSTER_24, MODEL_24, 64, PlanOptions(exact_threshold=12)),
         _case("missing-profile", CLUSTER_SMALL, MODEL_SMALL, 4),
     ]
+    # top_k > 1 on the budget-truncated configs (the wave engine's top-k state)
+    for name, k in (("cfg2", 2), ("cfg3", 4), ("cfg4", 2), ("cfg4", 4), ("cfg4", 8)):
+        w = configs.get(name)
+        out.append(PlanCase(f"{name}-topk{k}", w.cluster_json(), w.model_json(), w.max_layers,
+                            PlanOptions(top_k=k), heavy=True))
     for w in configs.cfg5_snapshots(n_snapshots):
         out.append(PlanCase(w.name, w.cluster_json(), w.model_json(), w.max_layers, heavy=True))
     if not include_heavy:

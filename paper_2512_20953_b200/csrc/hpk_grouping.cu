@@ -47,11 +47,15 @@ constexpr int BLOCK_THREADS = WARPS_PER_BLOCK * 32;
 constexpr int TILE = BLOCK_THREADS * 8;  // list positions per expansion / commit tile
 constexpr uint8_t KIND_FULL = 0;
 constexpr uint8_t KIND_PREFIX = 1;
+// top_k of the wave engine (grouping.cpp:117-132 with top_k > 1): the state
+// the DFS carries between segments is the vector of the top_k best leaf
+// objectives above the prune floor; larger top_k run on the serial replica.
+constexpr int KW = 8;
 
 // ------------------------------------------------------------------ layout
 
 struct GProb {
-  int n, K, exact_mem, pad0;
+  int n, K, exact_mem, top_k;
   long long budget;  // < 0: unlimited (exhaustive mode)
   double min_mem;
   double p[MAXN], m[MAXN];
@@ -97,6 +101,26 @@ struct GState {
   int max_list, error;
   uint8_t best_rgs[MAXN];
   uint8_t seed_rgs[MAXN];
+  // top_k > 1 (TOPK mode): the cutoff state at the commit front — the top_k
+  // best leaf objectives strictly above the floor (seed_obj), descending; the
+  // cutoff is T[top_k-1] once nT == top_k, else the floor (kth_objective(),
+  // grouping.cpp:129-132) — and the global candidate list best-first
+  // (SearchState::best, :99, ranking :112-115, insertion after equals :117-127).
+  int nT, nbest;
+  double T[KW];
+  double bl_obj[KW];
+  int bl_G[KW];
+  uint8_t bl_rgs[KW][MAXN];
+};
+
+// TOPK mode: what one run of a segment used and produced, one record per pool
+// entry (allocated only when a batch has a problem with top_k > 1).
+struct CandRec {
+  double tin[KW];  // the cutoff state the run entered with
+  int ntin, n;     // its size; candidates of the run
+  double obj[KW];  // the run's own top_k leaves, ranking order
+  int G[KW];
+  uint8_t rgs[KW][MAXN];
 };
 
 // Summary of one expansion tile's output range [ob, ob + n) of the new list,
@@ -116,6 +140,8 @@ struct RunItem {
   int problem, pos, id, front;
   long long cap;
   double cut;  // predicted entering cutoff (exact-checked at commit)
+  int ntv, pad;
+  double tv[KW];  // TOPK: the predicted entering state (cut = its cutoff)
 };
 
 struct RunQueue {
@@ -127,6 +153,7 @@ struct KParams {
   GProb* probs;
   GState* states;
   Entry* pools;       // [P][2][pcap]
+  CandRec* cands;     // TOPK only: [P][2][pcap], parallel to pools (else null)
   int* lists;         // [P][2][5][lcap]: ids, pcver, cnt, pfirst, info
   long long* lvis;    // [P][2][lcap]: visits of the finished run at each position
   double* ldbl;       // [P][2][3][lcap]: cutoff the run at each position used, its max
@@ -160,6 +187,9 @@ struct KParams {
 __device__ __forceinline__ Entry* pool_ptr(const KParams& kp, int p, int which) {
   return kp.pools + ((size_t)p * 2 + which) * kp.pcap;
 }
+__device__ __forceinline__ CandRec* cand_ptr(const KParams& kp, int p, int which) {
+  return kp.cands + ((size_t)p * 2 + which) * kp.pcap;
+}
 // list arrays of buffer `buf`: 0 ids, 1 pcver (1 = a finished run at this
 // position, -1 = needs a run), 2 cnt (expansion count), 3 pfirst, 4 info (the
 // run's best_G | 256 has_best | 512 PREFIX re-run that pruned an ancestor)
@@ -186,6 +216,10 @@ struct SchedSmem {
   double c_after, c_before;
   int fb, fs, sp_del, ndel, head, flag;
   double part[8 * 8];  // AggAcc partials (8 warps x 64 B)
+  // TOPK mode
+  double tv[KW];       // predicted cutoff state (push_items)
+  int ntv, sp_imp, fi, nq;
+  int qpos[TILE];      // committed positions whose candidates may enter the global list
 };
 
 // --------------------------------------------------------------- warp DFS
@@ -202,7 +236,69 @@ struct WarpSmem {
   uint8_t path[MAXN];
   uint8_t endp[MAXN];
   uint8_t best[MAXN];
+  // TOPK mode: the cutoff state (top_k objectives above the floor) and the
+  // run's own candidate list (ranking order), grouping.cpp:117-132
+  double T[KW];
+  double robj[KW];
+  int rG[KW];
+  int nT, rn;
+  uint8_t rrgs[KW][MAXN];
 };
+
+// ---- TOPK helpers (grouping.cpp:110-132)
+// better(): higher objective, then fewer groups; equal keys keep the earlier
+// enumeration (upper_bound inserts after equals), so a later candidate never
+// wins a tie.
+__device__ __forceinline__ bool rank_better(double ao, int ag, double bo, int bg) {
+  if (ao != bo) return ao > bo;
+  return ag < bg;
+}
+// kth_objective(): the floor until top_k objectives above it are known.
+__device__ __forceinline__ double state_cut(const double* T, int nT, int tk, double floor_) {
+  return nT >= tk ? T[tk - 1] : floor_;
+}
+// Adds objective v (> the state's cutoff, hence > floor) to the state (one thread).
+__device__ __forceinline__ void state_insert(double* T, int* nT, int tk, double v) {
+  const int n = *nT;
+  int pos = n < tk ? n : tk - 1;
+  while (pos > 0 && T[pos - 1] < v) {
+    T[pos] = T[pos - 1];
+    --pos;
+  }
+  T[pos] = v;
+  *nT = n < tk ? n + 1 : tk;
+}
+// offer() into a best-first candidate list of <= tk entries (warp-cooperative,
+// uniform arguments): insertion at upper_bound, the last entry drops out.
+// src(i) gives unit i's group of the new candidate.
+template <typename Src>
+__device__ __forceinline__ void cand_insert(double* obj, int* G, uint8_t (*rgs)[MAXN], int* cnt,
+                                            int tk, int nunits, double o, int g, Src src,
+                                            int lane) {
+  const int n = *cnt;
+  int pos = n;
+  for (int i = 0; i < n; ++i)
+    if (rank_better(o, g, obj[i], G[i])) {
+      pos = i;
+      break;
+    }
+  if (pos >= tk) return;
+  const int last = n < tk ? n : tk - 1;
+  for (int r = last; r > pos; --r)  // each lane moves its own bytes: no hazard
+    for (int i = lane; i < nunits; i += 32) rgs[r][i] = rgs[r - 1][i];
+  for (int i = lane; i < nunits; i += 32) rgs[pos][i] = src(i);
+  __syncwarp();
+  if (lane == 0) {
+    for (int r = last; r > pos; --r) {
+      obj[r] = obj[r - 1];
+      G[r] = G[r - 1];
+    }
+    obj[pos] = o;
+    G[pos] = g;
+    *cnt = last + 1;
+  }
+  __syncwarp();
+}
 
 // Problem view used by the runner: same member names as GProb, arrays in smem.
 struct PView {
@@ -391,10 +487,17 @@ struct RunOut {
 // stopf (optional): set once the wave's run queue has drained; a capped run
 // then stops at its next check after >= minq visits and is split like a run
 // that hit its cap, so no warp idles behind the wave's longest run.
+//
+// TOPK (top_k = tk > 1): the cutoff follows the state vector sm->T (entering
+// state loaded by the caller; cut = its cutoff) — a feasible leaf above the
+// cutoff joins it — and the run keeps its own top_k candidates in sm->r*,
+// written to rec at the end (grouping.cpp:117-132).
+template <bool TOPK>
 __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, double C,
                               long long cap, WarpSmem* sm, int lane, int* err,
                               unsigned long long deadline, unsigned long long* prof,
-                              const int* stopf, long long minq, unsigned long long wave_end) {
+                              const int* stopf, long long minq, unsigned long long wave_end,
+                              int tk, double floor_, CandRec* rec) {
   // prof (trace >= 2): [0] run cycles [1] leaf batches [2] leaves [3] loop iterations
   //   [4] single checks [5] descends [6] pops [7] prune skips [8] children skipped
   //   [9] exact fallbacks [10] mask computations
@@ -427,7 +530,11 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
   o.dstop = 0;
   o.stop_c = 0;
   o.exact = 0;
-  if (cap <= 0) return o;  // budget already exhausted: the reference aborts before entering u
+  if (TOPK && lane == 0) sm->rn = 0;
+  if (cap <= 0) {  // budget already exhausted: the reference aborts before entering u
+    if (TOPK && lane == 0) rec->n = 0;
+    return o;
+  }
   const int dend = prefix ? E->dend : 0;
   for (int i = lane; i < du; i += 32) sm->path[i] = E->u[i];
   if (prefix)
@@ -475,7 +582,15 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
       o.best_obj = obj;
       o.best_G = G;
       o.m = obj;
-      for (int i = lane; i < n; i += 32) sm->best[i] = sm->path[i];
+      if (TOPK) {
+        if (lane == 0) {
+          if (obj > cut) state_insert(sm->T, &sm->nT, tk, obj);
+        }
+        cand_insert(sm->robj, sm->rG, sm->rrgs, &sm->rn, tk, n, obj, G,
+                    [&](int i) { return sm->path[i]; }, lane);
+      } else {
+        for (int i = lane; i < n; i += 32) sm->best[i] = sm->path[i];
+      }
     }
     o.finished = true;
     goto done;
@@ -584,9 +699,9 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
             i1 = take ? oi1 : i1;
           }
           // each lane evaluates the children it owns (c = lane, lane+32)
-          double best_o = -1.0;
-          int best_Gc = 0, best_c = 1 << 30;
-          double mx = -1.0;
+          double obj_s[2];
+          int gc_s[2];
+          bool fe_s[2];
 #pragma unroll
           for (int k = 0; k < 2; ++k) {
             const int ch = lane + 32 * k;
@@ -595,10 +710,68 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
             const double mem_new = g.gm[k] + um;
             const int others_inf = n_inf - (inf_k[k] ? 1 : 0);
             const double other_min = (!isnew && ch == i1) ? m2 : m1;
-            const int Gc = isnew ? G + 1 : G;
-            if (ch >= c0 && ch < c0 + count && others_inf == 0 && !(mem_new < mm_)) {
-              const double z = eff_new < other_min ? eff_new : other_min;
-              const double obj = (double)Gc * z;
+            gc_s[k] = isnew ? G + 1 : G;
+            fe_s[k] = ch >= c0 && ch < c0 + count && others_inf == 0 && !(mem_new < mm_);
+            const double z = eff_new < other_min ? eff_new : other_min;
+            obj_s[k] = fe_s[k] ? (double)gc_s[k] * z : -1.0;
+          }
+          o.visits += count;
+          if (TOPK) {
+            double mx = obj_s[0] > obj_s[1] ? obj_s[0] : obj_s[1];
+            for (int off = W >> 1; off > 0; off >>= 1) {
+              const double om = __shfl_xor_sync(HPK_FULL_MASK, mx, off);
+              mx = om > mx ? om : mx;
+            }
+            if (W < 32) mx = shfl(mx, 0);
+            if (mx >= 0) {
+              o.m = mx > o.m ? mx : o.m;
+              if (mx > cut) {  // the cutoff state takes every leaf above the cutoff
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                  unsigned b = __ballot_sync(HPK_FULL_MASK, fe_s[k] && obj_s[k] > cut);
+                  while (b) {
+                    const int l = __ffs(b) - 1;
+                    b &= b - 1;
+                    const double v = shfl(obj_s[k], l);
+                    if (lane == 0) state_insert(sm->T, &sm->nT, tk, v);
+                  }
+                }
+                __syncwarp();
+                cut = state_cut(sm->T, sm->nT, tk, floor_);
+              }
+              // the run's own list: offers in enumeration (child) order
+              const int rn = sm->rn;
+              const double ko = rn >= tk ? sm->robj[tk - 1] : -1.0;
+              const int kg = rn >= tk ? sm->rG[tk - 1] : 0;
+              bool any = false;
+#pragma unroll
+              for (int k = 0; k < 2; ++k) {
+                unsigned b = __ballot_sync(HPK_FULL_MASK, fe_s[k] && (rn < tk || rank_better(obj_s[k], gc_s[k], ko, kg)));
+                if (b && !any) {
+                  __syncwarp();  // lane 0's path spills are visible
+                  any = true;
+                }
+                while (b) {
+                  const int l = __ffs(b) - 1;
+                  b &= b - 1;
+                  const double v = shfl(obj_s[k], l);
+                  const int gv = shfl(gc_s[k], l);
+                  const int ch = l + 32 * k;
+                  cand_insert(sm->robj, sm->rG, sm->rrgs, &sm->rn, tk, n, v, gv,
+                              [&](int i) { return i < n - 1 ? sm->path[i] : (uint8_t)ch; }, lane);
+                }
+              }
+            }
+          } else {
+          double best_o = -1.0;
+          int best_Gc = 0, best_c = 1 << 30;
+          double mx = -1.0;
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const int ch = lane + 32 * k;
+            if (fe_s[k]) {
+              const double obj = obj_s[k];
+              const int Gc = gc_s[k];
               mx = obj > mx ? obj : mx;
               if (best_o < 0 || key_better(obj, Gc, ch, best_o, best_Gc, best_c)) {
                 best_o = obj;
@@ -624,7 +797,6 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
             best_c = shfl(best_c, 0);
             mx = shfl(mx, 0);
           }
-          o.visits += count;
           if (best_o >= 0) {
             if (!o.has_best || best_o > o.best_obj ||
                 (best_o == o.best_obj && best_Gc < o.best_G)) {
@@ -638,6 +810,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
             }
             o.m = mx > o.m ? mx : o.m;
             cut = mx > cut ? mx : cut;
+          }
           }
         }
         HPK_PC(1, 1);
@@ -805,8 +978,23 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
   }
 done:
   __syncwarp();
-  if (o.has_best)
+  if (TOPK) {
+    const int rn = sm->rn;
+    o.has_best = rn > 0;
+    if (rn > 0) {
+      o.best_obj = sm->robj[0];
+      o.best_G = sm->rG[0];
+    }
+    for (int r = 0; r < rn; ++r)
+      for (int i = lane; i < n; i += 32) rec->rgs[r][i] = sm->rrgs[r][i];
+    if (lane < rn) {
+      rec->obj[lane] = sm->robj[lane];
+      rec->G[lane] = sm->rG[lane];
+    }
+    if (lane == 0) rec->n = rn;
+  } else if (o.has_best) {
     for (int i = lane; i < n; i += 32) Eout->best_rgs[i] = sm->best[i];
+  }
   __syncwarp();
   if (prof && lane == 0) {
     pcnt[0] = (unsigned long long)(clock64() - pc0);
@@ -949,6 +1137,33 @@ __device__ T block_scan8(const T* src, T* dst, int len, T* sh) {
   return carry;
 }
 
+// TOPK: offer a committed run's own candidates to the global list (one warp;
+// the run is later in the enumeration than everything already listed).
+__device__ void merge_run_cands(GState& S, const CandRec& r, int tk, int n, int lane) {
+  const int rn = r.n;
+  for (int t = 0; t < rn; ++t) {
+    const double o = r.obj[t];
+    const int g = r.G[t];
+    const int nb = S.nbest;
+    if (nb >= tk && !rank_better(o, g, S.bl_obj[tk - 1], S.bl_G[tk - 1])) break;  // ranked list
+    cand_insert(S.bl_obj, S.bl_G, S.bl_rgs, &S.nbest, tk, n, o, g,
+                [&](int i) { return r.rgs[t][i]; }, lane);
+  }
+}
+// TOPK: the committed run's leaves join the front's cutoff state (one thread).
+__device__ void merge_run_state(GState& S, const CandRec& r, int tk) {
+  for (int t = 0; t < r.n; ++t) {
+    const double v = r.obj[t];
+    if (v > S.seed_obj && v > state_cut(S.T, S.nT, tk, S.seed_obj)) state_insert(S.T, &S.nT, tk, v);
+  }
+}
+__device__ __forceinline__ bool same_state(const CandRec& r, const GState& S) {
+  if (r.ntin != S.nT) return false;
+  for (int t = 0; t < KW; ++t)
+    if (r.tin[t] != S.T[t]) return false;
+  return true;
+}
+
 __device__ void finish_problem(const KParams& kp, GState& S) {
   S.done = 1;
   atomicSub(kp.active, 1);
@@ -1003,11 +1218,19 @@ struct OpAddI {
   __device__ int operator()(int a, int b) const { return a + b; }
 };
 
+//
+// TOPK (tk > 1): the predicted state is a vector (SchedSmem::tv). It is
+// constant up to the first position whose run found a leaf above the
+// predicted cutoff (an improver); the tile is cut right after it, the
+// improver's own candidates are merged into the prediction, and the scan
+// resumes. An improver is exact only if it entered with the predicted VECTOR
+// (any other run only depends on the cutoff). At most 16 improvers per pass.
 __device__ void push_items(const KParams& kp, int queue, int p, const int* ids, const int* pran,
                            const long long* pvis, const double* pcut, const double* pm,
                            const Entry* pool, int head, int len, double C, int qmax,
                            long long budget_left, long long* shl, double* shd, int* shi,
-                           const TileAgg* ag, int nagg, int ashift) {
+                           const TileAgg* ag, int nagg, int ashift, SchedSmem* sh, int tk,
+                           double floor_, const CandRec* crec, const GState& S) {
   const int tid = threadIdx.x;
   RunQueue* q = kp.queues + queue;
   RunItem* items = kp.items + (size_t)queue * kp.qcap;
@@ -1016,6 +1239,13 @@ __device__ void push_items(const KParams& kp, int queue, int p, const int* ids, 
   int pushed = 0;
   int ta = 0;  // tile-summary cursor (summaries are at buffer offset -ashift)
   int base = 0;
+  const bool topk = tk > 1;
+  int n_imp = 0;
+  if (topk) {
+    if (tid < KW) sh->tv[tid] = S.T[tid];
+    if (tid == 0) sh->ntv = S.nT;
+    __syncthreads();
+  }
   while (base < len) {
     if (nagg) {
       // a summarised tile whose runs are all exact under the predicted cutoff
@@ -1035,7 +1265,7 @@ __device__ void push_items(const KParams& kp, int queue, int p, const int* ids, 
       }
     }
     const int lim = (nagg && ta < nagg) ? min(len, ag[ta].ob - ashift + ag[ta].n - head) : len;
-    const int jend = base + min(lim - base, (int)blockDim.x * 8);
+    int jend = base + min(lim - base, (int)blockDim.x * 8);
     const int j0 = base + tid * 8;  // this thread's 8 consecutive positions
     if (kp.trace >= 5 && tid == 0) {
       atomicAdd(kp.prof + 20, 1ull);
@@ -1052,6 +1282,29 @@ __device__ void push_items(const KParams& kp, int queue, int p, const int* ids, 
       cj[k] = ran[k] ? pcut[head + j] : -2.0;
       vj[k] = ran[k] ? pvis[head + j] : 0;
     }
+    int fi_rel = -1;  // TOPK: the tile's first improver (relative to base), -1: none
+    if (topk) {
+      if (tid == 0) sh->fi = 1 << 30;
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (ran[k] && mj[k] > cmax) {
+          atomicMin(&sh->fi, j0 + k - base);
+          break;
+        }
+      __syncthreads();
+      if (sh->fi < (1 << 30)) {
+        fi_rel = sh->fi;
+        jend = base + fi_rel + 1;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (j0 + k >= jend) {
+            ran[k] = false;
+            mj[k] = -1.0;
+          }
+      }
+      __syncthreads();
+    }
     double tmax = -1.0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) tmax = mj[k] > tmax ? mj[k] : tmax;
@@ -1062,11 +1315,18 @@ __device__ void push_items(const KParams& kp, int queue, int p, const int* ids, 
     long long vsum = 0;
     {
       double run = cmax > exm ? cmax : exm;
+      if (topk) run = cmax;  // constant up to (and including) the improver
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         chat[k] = run;
-        run = mj[k] > run ? mj[k] : run;
-        const bool exact = ran[k] && cj[k] == chat[k];
+        if (!topk) run = mj[k] > run ? mj[k] : run;
+        bool exact = ran[k] && cj[k] == chat[k];
+        if (topk && exact && j0 + k - base == fi_rel) {  // the improver: compare the vectors
+          const CandRec& r = crec[ids[head + j0 + k]];
+          bool same = r.ntin == sh->ntv;
+          for (int t = 0; t < KW && same; ++t) same = r.tin[t] == sh->tv[t];
+          exact = same;
+        }
         vj[k] = (j0 + k < jend) ? (exact ? vj[k] : 1) : 0;
         need[k] = (j0 + k < jend) && !exact;
         vsum += vj[k];
@@ -1114,6 +1374,12 @@ __device__ void push_items(const KParams& kp, int queue, int p, const int* ids, 
                      : budget_left < 0  ? 0x3fffffffffffffffLL
                                         : budget_left + 1;
             it.cut = chat[k];
+            if (topk) {
+              it.ntv = sh->ntv;
+              for (int t = 0; t < KW; ++t) it.tv[t] = sh->tv[t];
+            } else {
+              it.ntv = 0;
+            }
           }
         }
         ++rank;
@@ -1121,9 +1387,26 @@ __device__ void push_items(const KParams& kp, int queue, int p, const int* ids, 
     }
     pushed += take;
     before += tile_vis;
-    cmax = tile_max > cmax ? tile_max : cmax;
+    if (!topk) cmax = tile_max > cmax ? tile_max : cmax;
     base = jend;
     __syncthreads();
+    if (topk && fi_rel >= 0) {
+      // the improver's candidates join the predicted state (a stale run's
+      // values are still the best prediction available)
+      if (tid == 0) {
+        const CandRec& r = crec[ids[head + base - 1]];
+        int nt = sh->ntv;
+        for (int t = 0; t < r.n; ++t) {
+          const double v = r.obj[t];
+          if (v > floor_ && v > state_cut(sh->tv, nt, tk, floor_)) state_insert(sh->tv, &nt, tk, v);
+        }
+        sh->ntv = nt;
+      }
+      __syncthreads();
+      cmax = state_cut(sh->tv, sh->ntv, tk, floor_);
+      __syncthreads();
+      if (++n_imp >= 16) break;
+    }
     if (pushed >= qmax || (budget_left >= 0 && before >= budget_left)) break;
   }
 }
@@ -1380,11 +1663,18 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
   double* bo_out = list_dbl(kp, p, cur ^ 1, 2);
   Entry* pool = pool_ptr(kp, p, S.pool_cur);
 
+  const int tk = P.top_k;
+  const bool topk = tk > 1;
+  const CandRec* crec = topk ? cand_ptr(kp, p, S.pool_cur) : nullptr;
   if (S.rerun_pending) {
     // the capped re-run of the overflow segment (at the head) is back
+    if (topk) {
+      if (warp == 0) merge_run_cands(S, crec[ids_in[head]], tk, P.n, lane);
+      __syncthreads();
+    }
     if (tid == 0) {
       const Entry& e = pool[ids_in[head]];
-      if (e.has_best && (!S.has_best || e.best_obj > S.best_obj ||
+      if (!topk && e.has_best && (!S.has_best || e.best_obj > S.best_obj ||
                          (e.best_obj == S.best_obj && e.best_G < S.best_G))) {
         S.has_best = 1;
         S.best_obj = e.best_obj;
@@ -1563,8 +1853,10 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
       if (ta < nagg && ag[ta].ob == i) {
         const TileAgg a = ag[ta];
         if (a.nrun == a.n && a.ndel == 0 && a.mmax <= C && a.cutc == C &&
-            (B < 0 || V + a.sumvis < B)) {
-          if (a.bobj >= 0 && tid < 32) {
+            (B < 0 || V + a.sumvis < B) &&
+            (!topk || a.bobj < 0 ||
+             (S.nbest >= tk && !rank_better(a.bobj, a.bG, S.bl_obj[tk - 1], S.bl_G[tk - 1])))) {
+          if (!topk && a.bobj >= 0 && tid < 32) {
             const int gh = S.has_best;
             const double gbo = S.best_obj;
             const int gbg = S.best_G;
@@ -1615,10 +1907,13 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
     long long vsum = 0;
     {
       double run = C > exm ? C : exm;
+      if (topk) run = C;  // improvers end the tile (below)
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         ok[k] = pc[k] == 1 && cu[k] == run;
-        if (pc[k] == 1) run = mm[k] > run ? mm[k] : run;
+        if (topk && ok[k] && mm[k] > C)  // an improver is exact only with the front's vector
+          ok[k] = same_state(crec[ids_out[i + r0 + k]], S);
+        if (pc[k] == 1 && !topk) run = mm[k] > run ? mm[k] : run;
         cafter[k] = run;
         vsum += ok[k] ? vv[k] : 0;
       }
@@ -1637,7 +1932,8 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
         if (!ok[k] && r < fb) fb = r;
         const bool del = (inf[k] & 512) != 0;
         const bool over = B >= 0 && run >= B;
-        if (ok[k] && (del || over) && r < fs) fs = r;
+        const bool imp = topk && mm[k] > C;
+        if (ok[k] && (del || over || imp) && r < fs) fs = r;
       }
     }
     if (fb > tile) fb = tile;
@@ -1660,13 +1956,40 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
       sh->v_before = cum[k] - vv[k];
       sh->c_before = k > 0 ? cafter[k - 1] : (C > exm ? C : exm);
       sh->sp_del = (inf[k] & 512) != 0;
+      sh->sp_imp = topk && mm[k] > C;
     }
     __syncthreads();
     bool overflow = false;  // budget runs out INSIDE the special position: re-run it capped
     if (special_last && B >= 0 && sh->v_after > B) overflow = true;
     const int kcommit = overflow ? kc - 1 : kc;
     // best over the committed positions: (obj desc, G asc, position asc)
-    {
+    if (topk) {
+      // positions whose best candidate could enter the global list, in order
+      const int nb = S.nbest;
+      const double ko = nb >= tk ? S.bl_obj[tk - 1] : -1.0;
+      const int kg = nb >= tk ? S.bl_G[tk - 1] : 0;
+      bool qk[8];
+      int nql = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int r = r0 + k;
+        qk[k] = r < kcommit && (inf[k] & 256) &&
+                (nb < tk || rank_better(bo_out[i + r], inf[k] & 255, ko, kg));
+        nql += qk[k] ? 1 : 0;
+      }
+      int nqt;
+      int qo = block_excl_scan_1<int>(nql, 0, sh->i, OpAddI(), &nqt);
+      if (nqt > 0) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (qk[k]) sh->qpos[qo++] = r0 + k;
+        __syncthreads();
+        if (warp == 0)
+          for (int t = 0; t < nqt; ++t)
+            merge_run_cands(S, crec[ids_out[i + sh->qpos[t]]], tk, P.n, lane);
+        __syncthreads();
+      }
+    } else {
       double ko = -1;
       int kg = 0, ki = 1 << 30;
 #pragma unroll
@@ -1728,6 +2051,14 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
           }
         }
       }
+    }
+    if (topk && special_last && kcommit == kc && sh->sp_imp) {
+      // the committed improver's leaves raise the front's cutoff state
+      if (tid == 0) {
+        merge_run_state(S, crec[ids_out[i + kc - 1]], tk);
+        sh->c_after = state_cut(S.T, S.nT, tk, S.seed_obj);
+      }
+      __syncthreads();
     }
     if (kcommit > 0) {
       const double cn = (kcommit == kc) ? sh->c_after : sh->c_before;
@@ -1823,10 +2154,12 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
   if ((flag & 1) && S.pool_top > kp.pcap - 2 * kp.reserve - 64 * 32) {
     ashift = nhead;
     Entry* np = pool_ptr(kp, p, S.pool_cur ^ 1);
+    CandRec* ncr = topk ? cand_ptr(kp, p, S.pool_cur ^ 1) : nullptr;
     int* pcv_tmp = list_arr(kp, p, cur, 1);  // the input buffer is free now
     long long* vis_tmp = vis_in;
     for (int k = tid; k < nlen; k += blockDim.x) {
       np[k] = pool[ids_out[nhead + k]];
+      if (topk) ncr[k] = crec[ids_out[nhead + k]];
       pcv_tmp[k] = pcv_out[nhead + k];
       vis_tmp[k] = vis_out[nhead + k];
       cut_in[k] = cut_out[nhead + k];
@@ -1877,7 +2210,8 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
     const long long bl = P.budget < 0 ? -1 : P.budget - S.V;
     push_items(kp, next_queue, p, ids_out, pcv_out, vis_out, cut_out, m_out,
                pool_ptr(kp, p, S.pool_cur), nhead, nlen, S.C, qmax, bl, sh->l, sh->d, sh->i, ag,
-               nagg, ashift);
+               nagg, ashift, sh, P.top_k, S.seed_obj,
+               P.top_k > 1 ? cand_ptr(kp, p, S.pool_cur) : nullptr, S);
     if (tid == 0) S.runs_prev = runs_now;
   }
   if (warp == 0) {
@@ -1897,6 +2231,8 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
         it.front = 1;
         it.cap = sh->cap;
         it.cut = S.C;
+        it.ntv = S.nT;
+        for (int t = 0; t < KW; ++t) it.tv[t] = S.T[t];
         }
       }
     }
@@ -2021,6 +2357,9 @@ __device__ void init_problem(const KParams& kp, int p) {
     if (seed_ix >= 0)
       for (int i = 0; i < n; ++i) S.seed_rgs[i] = seeds[seed_ix][i];
     S.C = seed_obj;  // prune_floor (:312)
+    S.nT = 0;
+    S.nbest = 0;
+    for (int t = 0; t < KW; ++t) S.T[t] = -1.0;
     S.V = 0;
     S.has_best = 0;
     S.best_obj = 0;
@@ -2078,6 +2417,8 @@ __device__ void init_problem(const KParams& kp, int p) {
       kp.items[slot].front = 1;
       kp.items[slot].cap = kp.seg_cap;
       kp.items[slot].cut = S.C;
+      kp.items[slot].ntv = 0;
+      for (int t = 0; t < KW; ++t) kp.items[slot].tv[t] = -1.0;
     }
   }
   __syncthreads();
@@ -2175,10 +2516,34 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
       const PView PV = stage_problem(P, wsm + warp, lane);
       // (a PREFIX re-run must end at its end marker: it is never split)
       const bool stoppable = !E->capped && !E->uncapped && E->kind != KIND_PREFIX;
-      RunOut o = run_segment(PV, E, E, C, item.cap, wsm + warp, lane, kp.err, kp.deadline_ns,
+      const int tk = P.top_k;
+      RunOut o;
+      if (tk > 1) {
+        // the entering cutoff state travels with the item; the record keeps it
+        // for the commit walk's exactness check
+        CandRec* rec = cand_ptr(kp, p, S.pool_cur) + item.id;
+        WarpSmem* ws = wsm + warp;
+        if (lane < KW) {
+          ws->T[lane] = item.tv[lane];
+          rec->tin[lane] = lane < item.ntv ? item.tv[lane] : -1.0;
+        }
+        if (lane == 0) {
+          ws->nT = item.ntv;
+          rec->ntin = item.ntv;
+        }
+        __syncwarp();
+        o = run_segment<true>(PV, E, E, C, item.cap, ws, lane, kp.err, kp.deadline_ns,
                               (kp.trace >= 2 && kp.trace < 5) ? kp.prof : nullptr,
                               stoppable ? kp.stop : nullptr, kp.minq,
-                              stoppable && kp.wave_ns ? wave_t0 + kp.wave_ns : 0ull);
+                              stoppable && kp.wave_ns ? wave_t0 + kp.wave_ns : 0ull, tk,
+                              S.seed_obj, rec);
+      } else {
+        o = run_segment<false>(PV, E, E, C, item.cap, wsm + warp, lane, kp.err, kp.deadline_ns,
+                               (kp.trace >= 2 && kp.trace < 5) ? kp.prof : nullptr,
+                               stoppable ? kp.stop : nullptr, kp.minq,
+                               stoppable && kp.wave_ns ? wave_t0 + kp.wave_ns : 0ull, 1, 0.0,
+                               nullptr);
+      }
       int* pcv = list_arr(kp, p, S.cur, 1);
       int* cnt = list_arr(kp, p, S.cur, 2);
       int* pfirst = list_arr(kp, p, S.cur, 3);
@@ -2523,6 +2888,8 @@ struct DeviceCtx {
   GProb* probs = nullptr;
   GState* states = nullptr;
   Entry* pools = nullptr;
+  CandRec* cands = nullptr;
+  size_t cap_cands = 0;
   int* lists = nullptr;
   long long* lvis = nullptr;
   size_t cap_lvis = 0;
@@ -2636,6 +3003,25 @@ bool exact_sums(const double* v, int n, double extra, bool include_extra) {
   return std::ldexp(total, -emin) < 9007199254740992.0 * 0.5;
 }
 
+// z of a DFS leaf as the reference computes it (grouping.cpp:140-147): the
+// running min of the groups' effective powers, in group order.
+double leaf_z(const hpk_grouping_problem& pr, const uint8_t* rgs, int G) {
+  double pw[MAXN] = {0}, me[MAXN] = {0};
+  int cn[MAXN] = {0};
+  for (int u = 0; u < pr.n; ++u) {
+    pw[rgs[u]] += pr.power[u];
+    me[rgs[u]] += pr.memory[u];
+    cn[rgs[u]] += 1;
+  }
+  double z = 0;
+  for (int gi = 0; gi < G; ++gi) {
+    const double rho = (double)(cn[gi] - 1) / (double)(pr.n_microbatches + cn[gi] - 1);
+    const double gv = pw[gi] * (1.0 - rho);
+    z = gi == 0 ? gv : (gv < z ? gv : z);
+  }
+  return z;
+}
+
 }  // namespace
 
 // Hooks shared with hpk_partition.cu (same thread-local error / timing).
@@ -2739,7 +3125,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     if (pr.top_k > HPK_MAX_TOPK) return fail(6, "hetplan_b200: top_k above 16 unsupported");
     const bool contract = exact_sums(pr.power, pr.n, 0, false) &&
                           exact_sums(pr.memory, pr.n, 0, false);
-    const bool wave_ok = !cfg.force_serial && pr.n <= MAXN && pr.top_k <= 1 && contract;
+    const bool wave_ok = !cfg.force_serial && pr.n <= MAXN && pr.top_k <= KW && contract;
     (wave_ok ? wave_ix : serial_ix).push_back(i);
   }
 
@@ -2750,10 +3136,13 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     // list capacity (ids) and entry-pool capacity per problem; large by default
     // (the list must hold the whole speculative frontier), scaled down so that
     // big batches (cfg5 sweeps) stay within ~4 GB of HBM.
+    bool any_topk = false;
+    for (int k = 0; k < P; ++k) any_topk = any_topk || problems[wave_ix[k]].top_k > 1;
+    const size_t entry_bytes = sizeof(Entry) + (any_topk ? sizeof(CandRec) : 0);
     int lcap = cfg.max_list > 0 ? cfg.max_list : (1 << 17);
     int pcap = 2 * lcap;
     while (lcap > 4096 &&
-           (size_t)P * ((size_t)pcap * 2 * sizeof(Entry) + (size_t)lcap * 100) > ((size_t)4 << 30)) {
+           (size_t)P * ((size_t)pcap * 2 * entry_bytes + (size_t)lcap * 100) > ((size_t)4 << 30)) {
       lcap /= 2;
       pcap /= 2;
     }
@@ -2770,6 +3159,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
       g.K = pr.n_microbatches;
       g.budget = pr.n <= pr.exact_threshold ? -1 : pr.node_budget;
       g.min_mem = pr.min_mem;
+      g.top_k = std::max(1, pr.top_k);
       g.exact_mem = exact_sums(pr.memory, pr.n, pr.min_mem, true) ? 1 : 0;
       for (int i = 0; i < pr.n; ++i) {
         g.p[i] = pr.power[i];
@@ -2781,6 +3171,8 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     if (int rc = grow(c.probs, c.cap_probs, (size_t)P)) return rc;
     if (int rc = grow(c.states, c.cap_states, (size_t)P)) return rc;
     if (int rc = grow(c.pools, c.cap_pools, (size_t)P * 2 * pcap)) return rc;
+    if (any_topk)
+      if (int rc = grow(c.cands, c.cap_cands, (size_t)P * 2 * pcap)) return rc;
     if (int rc = grow(c.lists, c.cap_lists, (size_t)P * 2 * 5 * lcap)) return rc;
     if (int rc = grow(c.scratch, c.cap_scratch, (size_t)P * (lcap + 1))) return rc;
     if (int rc = grow(c.lvis, c.cap_lvis, (size_t)P * 2 * lcap)) return rc;
@@ -2812,6 +3204,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     kp.probs = c.probs;
     kp.states = c.states;
     kp.pools = c.pools;
+    kp.cands = any_topk ? c.cands : nullptr;
     kp.lists = c.lists;
     kp.lvis = c.lvis;
     kp.ldbl = c.ldbl;
@@ -2884,6 +3277,29 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
                            std::to_string(i) + ", waves " + std::to_string(s.waves) +
                            ", visits " + std::to_string(s.V) + ")");
       const bool optimal = !s.aborted;
+      if (pr.top_k > 1) {
+        // result rules, grouping.cpp:316-334, over the top_k list
+        if (s.nbest == 0 && s.seed_obj < 0) {
+          r.status = 3;
+          continue;
+        }
+        if (s.nbest == 0 || (!optimal && s.seed_obj > s.bl_obj[0])) {
+          r.count = 1;
+          r.objective[0] = s.seed_obj;
+          r.z[0] = s.seed_z;
+          r.optimal = 0;
+          for (int u = 0; u < pr.n; ++u) r.rgs[u] = s.seed_rgs[u];
+          continue;
+        }
+        r.count = s.nbest;
+        r.optimal = optimal ? 1 : 0;
+        for (int t = 0; t < s.nbest; ++t) {
+          r.objective[t] = s.bl_obj[t];
+          r.z[t] = leaf_z(pr, s.bl_rgs[t], s.bl_G[t]);
+          for (int u = 0; u < pr.n; ++u) r.rgs[(size_t)t * pr.n + u] = s.bl_rgs[t][u];
+        }
+        continue;
+      }
       // result rules, grouping.cpp:316-334
       if (!s.has_best) {
         if (s.seed_obj < 0) {

@@ -21,10 +21,11 @@ def _same(r, o):
             and r.optimal == o.optimal)
 
 
-def _random_problems(seed, count, nmax=11):
+def _random_problems(seed, count, nmax=11, top_ks=(1,)):
     rng = random.Random(seed)
     out = []
     for t in range(count):
+        topk = rng.choice(top_ks) if len(top_ks) > 1 else top_ks[0]
         n = rng.randint(1, nmax)
         if t % 5 == 0:
             P = [2.0] * n  # heavy ties
@@ -40,7 +41,7 @@ def _random_problems(seed, count, nmax=11):
             MIN = float(round(MIN))
         thr = rng.choice([0, 4, 8])
         B = rng.choice([0, 1, 2, 17, 300, 3000, 20000])
-        out.append(GroupingProblem(P, M, K, MIN, T, N, thr, B))
+        out.append(GroupingProblem(P, M, K, MIN, T, N, thr, B, topk))
     return out
 
 
@@ -56,6 +57,44 @@ def test_wave_engine_random_batch(engine, oracle, cap):
             bad.append((pb, r, o.rgs, o.objective, o.visited, o.optimal))
         assert r.engine == 0
     assert not bad, bad[:2]
+
+
+@pytest.mark.parametrize("cap", [3, 64, 2048])
+def test_wave_engine_top_k_random_batch(engine, oracle, cap):
+    """top_k > 1 on the wave engine: the cutoff state is the top_k vector
+    (grouping.cpp:117-132); every returned candidate, visits and the optimal
+    flag match the oracle."""
+    probs = _random_problems(1000 + cap, 160, nmax=10 if cap < 16 else 11,
+                             top_ks=(2, 3, 4, 8))
+    res = engine.grouping_search(probs, segment_cap=cap, max_seconds=60)
+    bad = []
+    for pb, r in zip(probs, res):
+        o = oracle.solve_grouping(pb.power, pb.memory, pb.n_microbatches, pb.min_mem,
+                                  pb.type_key, pb.node_key, pb.exact_threshold, pb.node_budget,
+                                  pb.top_k)
+        if not _same(r, o):
+            bad.append((pb, r, o.rgs, o.objective, o.visited, o.optimal))
+        assert r.engine == 0
+    assert not bad, bad[:2]
+
+
+@pytest.mark.parametrize("name,k", [("cfg2", 2), ("cfg3", 3), ("cfg4", 2), ("cfg4", 8)])
+def test_configs_top_k_every_tp_dimension(engine, oracle, name, k):
+    w = configs.get(name)
+    g = 0
+    for nd in w.cluster["nodes"]:
+        g = math.gcd(g, nd["count"])
+    probs = []
+    for tp in [t for t in range(1, g + 1) if g % t == 0]:
+        P, M, T, N = units_for(w.cluster, tp)
+        probs.append(GroupingProblem(P, M, w.model["n_microbatches"], min_mem_for(w.model), T, N,
+                                     top_k=k))
+    res = engine.grouping_search(probs, max_seconds=60)
+    for pb, r in zip(probs, res):
+        o = oracle.solve_grouping(pb.power, pb.memory, pb.n_microbatches, pb.min_mem,
+                                  pb.type_key, pb.node_key, top_k=k)
+        assert r.engine == 0
+        assert _same(r, o), (name, k, pb.n, r.objective, o.objective, r.visited, o.visited)
 
 
 def test_serial_engine_random_batch(engine, oracle):
@@ -105,12 +144,18 @@ def test_configs_every_tp_dimension(engine, oracle, name):
             assert r.exact_checks <= max(16, r.segment_visits // 1000), (name, pb.n)
 
 
-def test_top_k_and_non_dyadic_take_the_serial_engine(engine, oracle):
-    pb = GroupingProblem([1.0, 1.0, 2.0, 0.7, 1.3], [8.0, 8.0, 8.0, 9.0, 7.0], 8, 6.0,
+def test_non_dyadic_and_large_top_k_take_the_serial_engine(engine, oracle):
+    nd = GroupingProblem([1.0, 1.0, 2.0, 0.7, 1.3], [8.0, 8.0, 8.0, 9.0, 7.0], 8, 6.0,
                          [0, 0, 1, 2, 3], [0, 0, 1, 2, 3], top_k=3)
-    r = engine.grouping_search([pb])[0]
-    o = oracle.solve_grouping(pb.power, pb.memory, 8, 6.0, pb.type_key, pb.node_key, top_k=3)
-    assert r.engine == 1 and _same(r, o)
+    big = GroupingProblem([1.0, 1.0, 2.0, 0.5, 1.5, 2.0], [8.0, 8.0, 8.0, 9.0, 7.0, 4.0], 8, 6.0,
+                          [0, 0, 1, 2, 3, 1], [0, 0, 1, 2, 3, 3], top_k=12)
+    small = GroupingProblem(big.power, big.memory, 8, 6.0, big.type_key, big.node_key, top_k=3)
+    res = engine.grouping_search([nd, big, small])
+    assert [r.engine for r in res] == [1, 1, 0]
+    for pb, r in zip([nd, big, small], res):
+        o = oracle.solve_grouping(pb.power, pb.memory, 8, 6.0, pb.type_key, pb.node_key,
+                                  top_k=pb.top_k)
+        assert _same(r, o)
 
 
 def _host_decide(A, D, rem, cut, mb, md):
