@@ -80,7 +80,8 @@ struct __align__(16) Entry {
   int a_star;              // PREFIX re-run: depth of the pruned ancestor of `end`
   int cver;                // cutoff version of the last run (-1: never ran)
   uint8_t du, dend, kind, finished;
-  uint8_t has_best, capped, uncapped, pad;
+  uint8_t has_best, capped, uncapped;
+  uint8_t hi;              // the segment is children [u[du-1], hi] of node u[0..du-1)
 };
 
 struct GState {
@@ -172,6 +173,7 @@ struct KParams {
   long long minq;     // ... after at least this many visits (0: never stop early)
   unsigned long long wave_ns;  // run-phase time slice (0: none): later runs stop and split
   int runners;        // warps per CTA that run segments (experiment knob; default all)
+  int ranges;         // split pieces are sibling ranges (1) or single siblings (0)
   int n_problems;
   int lcap, pcap, qcap, qmax, reserve;
   long long seg_cap;
@@ -545,80 +547,38 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
   groups_init(P, g);
   int G = 0;
   if (lane == 0) sm->lvl[0] = 0;
-  for (int i = 0; i + 1 < du; ++i) {
+  for (int i = 0; i + 1 < du; ++i) {  // the range's parent node: units 0..du-2
     const int grp = sm->path[i];
     add_unit(P, g, lane, grp, P.p[i], P.m[i]);
     if (grp == G) ++G;
     if (lane == 0) sm->lvl[i + 1] = (unsigned)G << 16;
   }
-  {  // enter the segment root u
-    const int i = du - 1;
-    const int grp = sm->path[i];
-    add_unit(P, g, lane, grp, P.p[i], P.m[i]);
-    if (grp == G) ++G;
-    if (lane == 0) sm->lvl[du] = (unsigned)G << 16;
-    o.visits = 1;
-  }
   __syncwarp();
-  int d = du;
+  // the segment is the children [u[dpar], hi] of the parent (each with its
+  // subtree); they are visited, checked and entered by the loop below exactly
+  // like the children of any other node (grouping.cpp:171-201)
+  const int dpar = du - 1;
+  const int hi = E->hi;
+  int d = dpar;
   double cut = C;
   double Sd, Dd;
-  if (d == n) {  // the root is a leaf (grouping.cpp:138-149)
-    bool infeas = false;
-    double z = INFINITY;
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      if (g.gc[k] > 0) {
-        if (g.gm[k] < P.min_mem) infeas = true;
-        const double e = slot_eff(P, g, k);
-        z = e < z ? e : z;
-      }
-    }
-    const bool any_infeas = __any_sync(HPK_FULL_MASK, infeas);
-    z = warp_min(z);
-    if (!any_infeas) {
-      const double obj = (double)G * z;
-      o.has_best = true;
-      o.best_obj = obj;
-      o.best_G = G;
-      o.m = obj;
-      if (TOPK) {
-        if (lane == 0) {
-          if (obj > cut) state_insert(sm->T, &sm->nT, tk, obj);
-        }
-        cand_insert(sm->robj, sm->rG, sm->rrgs, &sm->rn, tk, n, obj, G,
-                    [&](int i) { return sm->path[i]; }, lane);
-      } else {
-        for (int i = lane; i < n; i += 32) sm->best[i] = sm->path[i];
-      }
-    }
-    o.finished = true;
-    goto done;
-  }
-  {  // node check of u itself
-    double le = slot_eff(P, g, 0) + slot_eff(P, g, 1);
-    double ld = slot_def(P, g, 0) + slot_def(P, g, 1);
+  {
+    const double le = slot_eff(P, g, 0) + slot_eff(P, g, 1);
+    const double ld = slot_def(P, g, 0) + slot_def(P, g, 1);
     Sd = warp_sum_approx(le);
     Dd = warp_sum_approx(ld);
-    int dec = decide(P, Sd + P.R[d], Dd, d, cut);
-    if (dec == DEC_EXACT) dec = exact_passes(P, g, G, d, cut) ? DEC_PASS : DEC_PRUNE;
-    if (dec == DEC_PRUNE) {
-      if (prefix) o.a_star = du;
-      o.finished = true;
-      goto done;
-    }
   }
   {
     const double kNaN = __longlong_as_double(0x7ff8000000000000LL);
     const double mm_ = P.min_mem, mb = P.mb_abs, md = P.md_abs;
-    int c = 0;                        // next child of the current node
+    int c = sm->path[dpar];           // next child of the current node
     double up = P.p[d], um = P.m[d];  // unit d: assigned by the children
     unsigned long long mp = 0, mr = 0;
     double mc = kNaN;                 // cutoff of mp/mr (NaN: not computed)
     double lS[2] = {0, 0}, lD[2] = {0, 0};  // this lane's children's level sums
     bool sums_ok = false;             // lS/lD belong to the current node
-    int match = prefix ? du : -1;     // path == end marker on levels < match
-    int ec = (prefix && du < dend) ? sm->endp[du] : -1;  // end child at level `match`
+    int match = prefix ? dpar : -1;   // path == end marker on levels < match
+    int ec = prefix ? sm->endp[dpar] : -1;  // end child at level `match`
     unsigned it = 0;
     int stop_pending = 0;  // stop flag loaded 32 iterations ago (latency off the chain)
 
@@ -647,7 +607,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
               unsigned long long now;
               asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
               now = __shfl_sync(HPK_FULL_MASK, now, 0);
-              if (now > wave_end && o.visits < cap) cap = o.visits;
+              if (now > wave_end && o.visits < cap && o.visits > 0) cap = o.visits;
             }
           }
         }
@@ -655,7 +615,8 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
       if (d == n - 1) {
         // ---- leaf batch: children c0..G are leaves (unit n-1) ----
         const int c0 = c;
-        int count = G + 1 - c0;
+        const int lim = d == dpar ? hi : G;  // last child of this node in the segment
+        int count = lim + 1 - c0;
         bool end_hit = false;
         if (prefix && match == d) {  // dend == n here
           if (ec - c0 < count) {
@@ -826,10 +787,10 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
           o.finished = true;
           break;
         }
-        c = G + 1;
+        c = lim + 1;
       }
-      if (c > G) {  // node exhausted: pop unit d-1
-        if (d == du) {
+      if (c > (d == dpar ? hi : G)) {  // node exhausted: pop unit d-1
+        if (d == dpar) {
           o.finished = true;
           break;
         }
@@ -889,7 +850,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
           lS[k] = (Sd - eff_old) + eff_new;
           lD[k] = (Dd - def_old) + def_new;
           const double A = lS[k] + Rn;
-          const bool valid = ci <= G;
+          const bool valid = ci <= (d == dpar ? hi : G);
           pr[k] = !valid || (hc && A + mb < cut) || (lD[k] - md > RMn);
           ps[k] = !pr[k] && (!hc || A - mb >= cut) && (lD[k] + md <= RMn);
         }
@@ -906,7 +867,8 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
         // children c .. c+k-1 are all pruned: k visits, nothing entered
         const unsigned long long rest = ~(mr >> c);
         int k = rest ? __ffsll((long long)rest) - 1 : 64 - c;
-        if (k > G + 1 - c) k = G + 1 - c;
+        const int lim = d == dpar ? hi : G;
+        if (k > lim + 1 - c) k = lim + 1 - c;
         if ((long long)k > cap - o.visits) k = (int)(cap - o.visits);
         if (prefix && match == d) {
           // the end node (d+1 == dend) is not visited; the end path's child is,
@@ -1021,12 +983,21 @@ __device__ __forceinline__ bool is_prefix_of(const uint8_t* a, int la, const uin
 // the problem's entry pool; returns the piece count (0: pool full, run dropped).
 __device__ int split_run(const KParams& kp, int p, GState& S, Entry* E, const RunOut& o,
                          WarpSmem* sm, int lane, bool front, int* first_out) {
-  const int du = E->du;
+  const int dpar = E->du - 1;
   const int d = o.dstop - 1;  // the stop node is child stop_c of path[0..d)
-  // level table: lev = d (siblings after stop_c), then lev = d-1 .. du
-  const auto gat = [&](int lev) { return (int)((sm->lvl[lev] >> 16) & 255); };
-  int count = 1 + (gat(d) - o.stop_c);
-  for (int lev = d - 1; lev >= du; --lev) count += gat(lev) - (int)sm->path[lev];
+  // one range piece per level: lev = d (children stop_c..), then each ancestor
+  // level d-1 .. dpar (the children after the path's child), deepest first
+  const auto lim = [&](int lev) {
+    return lev == dpar ? (int)E->hi : (int)((sm->lvl[lev] >> 16) & 255);
+  };
+  // kp.ranges == 0: one piece per sibling instead (more, smaller pieces: more
+  // parallelism for a few problems; ranges keep big batches' lists short)
+  const bool rng = kp.ranges != 0;
+  int count = rng ? 1 : 1 + lim(d) - o.stop_c;
+  for (int lev = d - 1; lev >= dpar; --lev) {
+    const int w = lim(lev) - (int)sm->path[lev];
+    count += rng ? (w > 0 ? 1 : 0) : w;
+  }
   int first = 0;
   if (lane == 0) {  // CAS bump allocation: a failed attempt leaves no hole, and the
     // list head alone may use the last `reserve` slots (progress guarantee)
@@ -1049,27 +1020,32 @@ __device__ int split_run(const KParams& kp, int p, GState& S, Entry* E, const Ru
   if (first < 0) return 0;
   Entry* pool = pool_ptr(kp, p, S.pool_cur);
   for (int k = lane; k < count; k += 32) {
-    int lev, child;
-    if (k == 0) {
-      lev = d;
-      child = o.stop_c;
-    } else {
-      int idx = k - 1;
-      lev = d;
-      int base = o.stop_c;
-      int cnt = gat(d) - base;
+    int lev = d, child = o.stop_c, last;
+    if (rng) {
+      for (int idx = k; idx > 0;) {  // the k-th non-empty level below d
+        --lev;
+        if ((int)sm->path[lev] < lim(lev)) {
+          --idx;
+          child = sm->path[lev] + 1;
+        }
+      }
+      last = lim(lev);
+    } else {  // the k-th sibling piece, level by level (deepest first)
+      int idx = k, base = o.stop_c - 1, cnt = lim(d) - base;
       while (idx >= cnt) {
         idx -= cnt;
         --lev;
         base = sm->path[lev];
-        cnt = gat(lev) - base;
+        cnt = lim(lev) - base;
       }
       child = base + 1 + idx;
+      last = child;
     }
     Entry& q = pool[first + k];
     for (int i = 0; i < lev; ++i) q.u[i] = sm->path[i];
     q.u[lev] = (uint8_t)child;
     q.du = (uint8_t)(lev + 1);
+    q.hi = (uint8_t)last;
     q.kind = KIND_FULL;
     q.cver = -1;
     q.finished = 0;
@@ -2391,6 +2367,7 @@ __device__ void init_problem(const KParams& kp, int p) {
       Entry& e = pool_ptr(kp, p, 0)[0];
       e.u[0] = 0;  // root has no groups: its only child is [0]
       e.du = 1;
+      e.hi = 0;
       e.kind = KIND_FULL;
       e.cver = -1;
       e.finished = 0;
@@ -3148,7 +3125,11 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     }
     int max_n = 1;
     for (int k = 0; k < P; ++k) max_n = std::max(max_n, problems[wave_ix[k]].n);
-    const int reserve = max_n * (max_n + 1) / 2 + 32;  // pieces of one split, worst case
+    // piece shape: sibling ranges (default; measured equal on cfg4 and 1.3x
+    // faster on cfg5 than single-sibling pieces); HPK_RANGES=0 for the latter
+    const int ranges = getenv("HPK_RANGES") ? atoi(getenv("HPK_RANGES")) : 1;
+    const int reserve = ranges ? max_n + 64                          // one piece per level
+                               : max_n * (max_n + 1) / 2 + 32;  // one per sibling, worst case
     if (pcap < 4 * reserve) pcap = 4 * reserve;
     std::vector<GProb> hp(P);
     for (int k = 0; k < P; ++k) {
@@ -3222,6 +3203,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     kp.stop = c.active + 7;
     kp.minq = getenv("HPK_MINQ") ? atoll(getenv("HPK_MINQ")) : 0;
     kp.runners = getenv("HPK_RUNNERS") ? atoi(getenv("HPK_RUNNERS")) : WARPS_PER_BLOCK;
+    kp.ranges = ranges;
     // run-phase time slice: 200 us (HPK_WAVE_US overrides; 0 = none)
     kp.wave_ns = (unsigned long long)((getenv("HPK_WAVE_US") ? atof(getenv("HPK_WAVE_US")) : 200.0) * 1000.0);
     kp.n_problems = P;

@@ -16,6 +16,7 @@
 // fallback: without a CUDA device plan_cluster throws InternalError.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <exception>
@@ -591,9 +592,27 @@ void for_jobs(std::vector<PlanJob*>& jobs, int threads, Fn&& fn) {
 
 // All jobs through the four phases with ONE grouping-search launch and ONE
 // partition/cost launch. A GPU failure fails every job that needed the GPU.
+// HPK_HOST_TRACE=1: per-phase wall times of plan_jobs on stderr (diagnostics).
+struct PhaseClock {
+  bool on = getenv("HPK_HOST_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  std::ostringstream os;
+  void lap(const char* name) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    os << name << " " << std::chrono::duration<double, std::milli>(now - t).count() << " ms  ";
+    t = now;
+  }
+  ~PhaseClock() {
+    if (on) std::cerr << "[hpk-host] " << os.str() << "\n";
+  }
+};
+
 void plan_jobs(std::vector<PlanJob*>& jobs, int threads) {
   hpk_reset_timing();
+  PhaseClock clk;
   for_jobs(jobs, threads, job_prepare);
+  clk.lap("prepare");
   // ---- phase 2: one batched GPU search over every TP dimension of every job
   std::vector<hpk_grouping_problem> problems;
   std::vector<std::pair<PlanJob*, size_t>> owner;
@@ -621,7 +640,9 @@ void plan_jobs(std::vector<PlanJob*>& jobs, int threads) {
     }
     for (size_t i = 0; i < problems.size(); ++i) owner[i].first->gres[owner[i].second] = gres[i];
   }
+  clk.lap("search");
   for_jobs(jobs, threads, job_candidates);
+  clk.lap("candidates(map)");
   // ---- phase 4: one batched GPU launch for every candidate's partition + cost
   std::vector<hpk_plan_candidate> pin;
   std::vector<hpk_plan_result> pres;
@@ -644,7 +665,9 @@ void plan_jobs(std::vector<PlanJob*>& jobs, int threads) {
     }
     for (size_t i = 0; i < pin.size(); ++i) powner[i].first->pres[powner[i].second] = pres[i];
   }
+  clk.lap("partition");
   for_jobs(jobs, threads, [](PlanJob& J) { J.plan = job_select(J); });
+  clk.lap("select");
 }
 
 }  // namespace
