@@ -231,6 +231,25 @@ typedef struct hpk_plan_result {
 int hpk_partition_cost(const hpk_plan_candidate* cands, int n_cands, hpk_plan_result* results,
                        int device);
 
+/* The DP-affinity pass of the stage mapper (map_nodes_and_stages,
+ * P/src/stage_map.cpp:188-214) for one candidate plan: slots in stage order
+ * per group after the joint / fallback placement (:94-186), each holding the
+ * unit of type slot_type[s] on node slot_node[s]. The first strictly
+ * improving same-type swap in (group, slot, group, slot) scan order is applied
+ * until none is left (count_intra_node_dp_pairs, :39-58). On return
+ * slot_perm[s] is the index of the original slot whose unit now sits in s. */
+typedef struct hpk_affinity_problem {
+  int n_groups, n_slots;
+  const int* group_off;  /* [n_groups+1] slot offsets */
+  const int* slot_type;  /* [n_slots] dense type ids */
+  const int* slot_node;  /* [n_slots] node id of the slot's unit */
+  int* slot_perm;        /* [n_slots] out (caller-owned) */
+  int swaps;             /* out: swaps applied */
+} hpk_affinity_problem;
+
+/* All problems in one launch (one CTA each). */
+int hpk_stage_affinity(hpk_affinity_problem* problems, int n_problems, int device);
+
 /* Device-side timing of this thread's last hpk_grouping_search /
  * hpk_partition_cost calls (CUDA events on the launching stream). */
 typedef struct hpk_timing {

@@ -6,6 +6,8 @@
 #pragma once
 
 #include <cstdint>
+#include <cstddef>
+#include <cuda_runtime.h>
 
 #define HPK_FULL_MASK 0xffffffffu
 
@@ -60,3 +62,41 @@ __device__ __forceinline__ bool key_better(double ao, int ag, int ia, double bo,
 }
 
 }  // namespace hpk
+
+// Host-side staging arena shared by the hpk_* wrappers: one pinned host buffer
+// and one device buffer, grown on demand and kept for the next call, so a
+// launch costs one H2D and one D2H copy instead of a malloc / copy / free per
+// array. Layout: inputs first (copied H2D as one span), outputs after.
+struct HpkArena {
+  char* h = nullptr;  // pinned
+  char* d = nullptr;
+  size_t cap = 0;
+  size_t used = 0;
+  void reset() { used = 0; }
+  // reserves bytes (16-aligned); returns the offset
+  size_t take(size_t bytes) {
+    used = (used + 15) & ~(size_t)15;
+    const size_t o = used;
+    used += bytes;
+    return o;
+  }
+  // makes room for `used` bytes (contents are not preserved)
+  cudaError_t fit() {
+    if (used <= cap) return cudaSuccess;
+    if (h) cudaFreeHost(h);
+    if (d) cudaFree(d);
+    h = nullptr;
+    d = nullptr;
+    size_t want = cap * 2 > used ? cap * 2 : used;
+    cudaError_t e = cudaMallocHost(&h, want);
+    if (e != cudaSuccess) return e;
+    e = cudaMalloc(&d, want);
+    if (e != cudaSuccess) return e;
+    cap = want;
+    return cudaSuccess;
+  }
+  template <typename T>
+  T* hp(size_t off) const { return reinterpret_cast<T*>(h + off); }
+  template <typename T>
+  T* dp(size_t off) const { return reinterpret_cast<T*>(d + off); }
+};

@@ -177,6 +177,7 @@ struct KParams {
   int n_problems;
   int lcap, pcap, qcap, qmax, reserve;
   long long seg_cap;
+  int ramp;           // first-wave visit cap, doubled every wave up to seg_cap (0: off)
   int max_waves;
   unsigned long long deadline_ns;  // %globaltimer watchdog (relative at launch)
   unsigned long long* deadline_slot;
@@ -1217,6 +1218,10 @@ __device__ void push_items(const KParams& kp, int queue, int p, const int* ids, 
   int base = 0;
   const bool topk = tk > 1;
   int n_imp = 0;
+  // ramp-up: short runs while the list is young (they split the tree into
+  // runnable pieces quickly), the full segment cap after a few waves
+  const long long wave_cap = kp.ramp > 0 ? min(kp.seg_cap, (long long)kp.ramp << min(S.waves, 30))
+                                         : kp.seg_cap;
   if (topk) {
     if (tid < KW) sh->tv[tid] = S.T[tid];
     if (tid == 0) sh->ntv = S.nT;
@@ -1346,7 +1351,7 @@ __device__ void push_items(const KParams& kp, int queue, int p, const int* ids, 
             it.front = (j == 0);
             // an uncapped (list-full) run is the head's: under a budget it
             // needs at most budget_left + 1 visits to show the overflow
-            it.cap = !pool[id].uncapped ? kp.seg_cap
+            it.cap = !pool[id].uncapped ? wave_cap
                      : budget_left < 0  ? 0x3fffffffffffffffLL
                                         : budget_left + 1;
             it.cut = chat[k];
@@ -2392,7 +2397,7 @@ __device__ void init_problem(const KParams& kp, int p) {
       kp.items[slot].pos = 0;
       kp.items[slot].id = 0;
       kp.items[slot].front = 1;
-      kp.items[slot].cap = kp.seg_cap;
+      kp.items[slot].cap = kp.ramp > 0 ? min(kp.seg_cap, (long long)kp.ramp) : kp.seg_cap;
       kp.items[slot].cut = S.C;
       kp.items[slot].ntv = 0;
       for (int t = 0; t < KW; ++t) kp.items[slot].tv[t] = -1.0;
@@ -3213,6 +3218,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     kp.qcap = qcap;
     kp.qmax = qmax;
     kp.seg_cap = seg_cap;
+    kp.ramp = getenv("HPK_RAMP") ? atoi(getenv("HPK_RAMP")) : 0;
     kp.max_waves = cfg.max_waves > 0 ? cfg.max_waves : 1000000;  // watchdog
     kp.deadline_ns = (unsigned long long)(cfg.max_seconds > 0 ? cfg.max_seconds : 120.0) * 1000000000ull;
     kp.deadline_slot = reinterpret_cast<unsigned long long*>(c.active + 2);

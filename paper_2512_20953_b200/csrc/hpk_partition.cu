@@ -29,6 +29,7 @@
 #include <vector>
 
 #include "hetplan_b200.h"
+#include "hpk_common.cuh"
 
 namespace hpkp {
 
@@ -393,6 +394,7 @@ struct Ctx {
   int device = -1;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  HpkArena arena;
   std::mutex mu;
 };
 Ctx g_ctx[16];
@@ -505,50 +507,68 @@ extern "C" int hpk_partition_cost(const hpk_plan_candidate* cands, int n_cands,
     total_groups += in.n_groups;
     total_stages += ns;
   }
-  // device buffers (per call; small)
-  Cand* d_c;
-  int *d_goff, *d_mb, *d_sty, *d_sidx, *d_snode, *d_srank, *d_layers;
-  double *d_scap, *d_prof, *d_tt, *d_gbest, *d_time, *d_mem, *d_fill, *d_steady, *d_total,
-      *d_bubble;
-  unsigned char* d_tm;
-  Outs* d_outs;
+  // one staging arena (cached per device): inputs | outputs | device scratch
   const size_t S = std::max(1, total_stages), Gn = std::max(1, total_groups);
-  HPKP_CUDA(cudaMalloc(&d_c, sizeof(Cand) * n_cands));
-  HPKP_CUDA(cudaMalloc(&d_goff, sizeof(int) * goff.size()));
-  HPKP_CUDA(cudaMalloc(&d_mb, sizeof(int) * Gn));
-  HPKP_CUDA(cudaMalloc(&d_sty, sizeof(int) * S));
-  HPKP_CUDA(cudaMalloc(&d_sidx, sizeof(int) * S));
-  HPKP_CUDA(cudaMalloc(&d_snode, sizeof(int) * S));
-  HPKP_CUDA(cudaMalloc(&d_srank, sizeof(int) * S));
-  HPKP_CUDA(cudaMalloc(&d_layers, sizeof(int) * S));
-  HPKP_CUDA(cudaMalloc(&d_scap, sizeof(double) * S));
-  HPKP_CUDA(cudaMalloc(&d_prof, sizeof(double) * std::max<size_t>(1, prof.size())));
-  HPKP_CUDA(cudaMalloc(&d_tt, sizeof(double) * std::max<size_t>(1, tt_total)));
-  HPKP_CUDA(cudaMalloc(&d_tm, std::max<size_t>(1, tt_total)));
-  HPKP_CUDA(cudaMalloc(&d_gbest, sizeof(double) * std::max<size_t>(1, gbest_total)));
-  HPKP_CUDA(cudaMalloc(&d_time, sizeof(double) * S));
-  HPKP_CUDA(cudaMalloc(&d_mem, sizeof(double) * S));
-  HPKP_CUDA(cudaMalloc(&d_fill, sizeof(double) * Gn));
-  HPKP_CUDA(cudaMalloc(&d_steady, sizeof(double) * Gn));
-  HPKP_CUDA(cudaMalloc(&d_total, sizeof(double) * Gn));
-  HPKP_CUDA(cudaMalloc(&d_bubble, sizeof(double) * Gn));
-  HPKP_CUDA(cudaMalloc(&d_outs, sizeof(Outs) * n_cands));
-  auto up = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
-    if (!bytes) return cudaSuccess;
-    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, cx.stream);
+  HpkArena& ar = cx.arena;
+  ar.reset();
+  const size_t o_c = ar.take(sizeof(Cand) * n_cands);
+  const size_t o_goff = ar.take(sizeof(int) * goff.size());
+  const size_t o_mb = ar.take(sizeof(int) * Gn);
+  const size_t o_sty = ar.take(sizeof(int) * S);
+  const size_t o_sidx = ar.take(sizeof(int) * S);
+  const size_t o_snode = ar.take(sizeof(int) * S);
+  const size_t o_srank = ar.take(sizeof(int) * S);
+  const size_t o_scap = ar.take(sizeof(double) * S);
+  const size_t o_prof = ar.take(sizeof(double) * std::max<size_t>(1, prof.size()));
+  const size_t in_end = ar.used;
+  const size_t o_outs = ar.take(sizeof(Outs) * n_cands);
+  const size_t o_layers = ar.take(sizeof(int) * S);
+  const size_t o_time = ar.take(sizeof(double) * S);
+  const size_t o_mem = ar.take(sizeof(double) * S);
+  const size_t o_fill = ar.take(sizeof(double) * Gn);
+  const size_t o_steady = ar.take(sizeof(double) * Gn);
+  const size_t o_total = ar.take(sizeof(double) * Gn);
+  const size_t o_bubble = ar.take(sizeof(double) * Gn);
+  const size_t out_end = ar.used;
+  const size_t o_tt = ar.take(sizeof(double) * std::max<size_t>(1, tt_total));
+  const size_t o_tm = ar.take(std::max<size_t>(1, tt_total));
+  const size_t o_gbest = ar.take(sizeof(double) * std::max<size_t>(1, gbest_total));
+  HPKP_CUDA(ar.fit());
+  auto stage = [&](size_t off, const void* src, size_t bytes) {
+    if (bytes) std::memcpy(ar.h + off, src, bytes);
   };
-  HPKP_CUDA(up(d_c, hc.data(), sizeof(Cand) * n_cands));
-  HPKP_CUDA(up(d_goff, goff.data(), sizeof(int) * goff.size()));
-  HPKP_CUDA(up(d_mb, mb.data(), sizeof(int) * mb.size()));
-  HPKP_CUDA(up(d_sty, sty.data(), sizeof(int) * sty.size()));
-  HPKP_CUDA(up(d_sidx, sidx.data(), sizeof(int) * sidx.size()));
-  HPKP_CUDA(up(d_snode, snode.data(), sizeof(int) * snode.size()));
-  HPKP_CUDA(up(d_srank, srank.data(), sizeof(int) * srank.size()));
-  HPKP_CUDA(up(d_scap, scap.data(), sizeof(double) * scap.size()));
-  HPKP_CUDA(up(d_prof, prof.data(), sizeof(double) * prof.size()));
-  HPKP_CUDA(cudaMemsetAsync(d_outs, 0, sizeof(Outs) * n_cands, cx.stream));
-  const long long h2d = (long long)(sizeof(Cand) * n_cands + sizeof(int) * (goff.size() + mb.size() + 4 * sty.size()) +
-                                    sizeof(double) * (scap.size() + prof.size()));
+  stage(o_c, hc.data(), sizeof(Cand) * n_cands);
+  stage(o_goff, goff.data(), sizeof(int) * goff.size());
+  stage(o_mb, mb.data(), sizeof(int) * mb.size());
+  stage(o_sty, sty.data(), sizeof(int) * sty.size());
+  stage(o_sidx, sidx.data(), sizeof(int) * sidx.size());
+  stage(o_snode, snode.data(), sizeof(int) * snode.size());
+  stage(o_srank, srank.data(), sizeof(int) * srank.size());
+  stage(o_scap, scap.data(), sizeof(double) * scap.size());
+  stage(o_prof, prof.data(), sizeof(double) * prof.size());
+  HPKP_CUDA(cudaMemcpyAsync(ar.d, ar.h, in_end, cudaMemcpyHostToDevice, cx.stream));
+  HPKP_CUDA(cudaMemsetAsync(ar.d + o_outs, 0, sizeof(Outs) * n_cands, cx.stream));
+  const long long h2d = (long long)in_end;
+  Cand* d_c = ar.dp<Cand>(o_c);
+  int* d_goff = ar.dp<int>(o_goff);
+  int* d_mb = ar.dp<int>(o_mb);
+  int* d_sty = ar.dp<int>(o_sty);
+  int* d_sidx = ar.dp<int>(o_sidx);
+  int* d_snode = ar.dp<int>(o_snode);
+  int* d_srank = ar.dp<int>(o_srank);
+  double* d_scap = ar.dp<double>(o_scap);
+  double* d_prof = ar.dp<double>(o_prof);
+  Outs* d_outs = ar.dp<Outs>(o_outs);
+  int* d_layers = ar.dp<int>(o_layers);
+  double* d_time = ar.dp<double>(o_time);
+  double* d_mem = ar.dp<double>(o_mem);
+  double* d_fill = ar.dp<double>(o_fill);
+  double* d_steady = ar.dp<double>(o_steady);
+  double* d_total = ar.dp<double>(o_total);
+  double* d_bubble = ar.dp<double>(o_bubble);
+  double* d_tt = ar.dp<double>(o_tt);
+  unsigned char* d_tm = ar.dp<unsigned char>(o_tm);
+  double* d_gbest = ar.dp<double>(o_gbest);
   Args a;
   a.cands = d_c;
   a.group_stage_off = d_goff;
@@ -578,25 +598,20 @@ extern "C" int hpk_partition_cost(const hpk_plan_candidate* cands, int n_cands,
   partition_cost_kernel<<<n_cands, THREADS, smem, cx.stream>>>(a);
   HPKP_CUDA(cudaGetLastError());
   HPKP_CUDA(cudaEventRecord(cx.ev1, cx.stream));
-  std::vector<Outs> ho(n_cands);
-  std::vector<int> hl(S);
-  std::vector<double> htime(S), hmem(S), hfill(Gn), hsteady(Gn), htotal(Gn), hbub(Gn);
-  auto down = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
-    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, cx.stream);
-  };
-  HPKP_CUDA(down(ho.data(), d_outs, sizeof(Outs) * n_cands));
-  HPKP_CUDA(down(hl.data(), d_layers, sizeof(int) * S));
-  HPKP_CUDA(down(htime.data(), d_time, sizeof(double) * S));
-  HPKP_CUDA(down(hmem.data(), d_mem, sizeof(double) * S));
-  HPKP_CUDA(down(hfill.data(), d_fill, sizeof(double) * Gn));
-  HPKP_CUDA(down(hsteady.data(), d_steady, sizeof(double) * Gn));
-  HPKP_CUDA(down(htotal.data(), d_total, sizeof(double) * Gn));
-  HPKP_CUDA(down(hbub.data(), d_bubble, sizeof(double) * Gn));
+  HPKP_CUDA(cudaMemcpyAsync(ar.h + o_outs, ar.d + o_outs, out_end - o_outs, cudaMemcpyDeviceToHost,
+                            cx.stream));
   HPKP_CUDA(cudaStreamSynchronize(cx.stream));
+  const Outs* ho = ar.hp<Outs>(o_outs);
+  const int* hl = ar.hp<int>(o_layers);
+  const double* htime = ar.hp<double>(o_time);
+  const double* hmem = ar.hp<double>(o_mem);
+  const double* hfill = ar.hp<double>(o_fill);
+  const double* hsteady = ar.hp<double>(o_steady);
+  const double* htotal = ar.hp<double>(o_total);
+  const double* hbub = ar.hp<double>(o_bubble);
   float ms = 0;
   cudaEventElapsedTime(&ms, cx.ev0, cx.ev1);
-  const long long d2h = (long long)(sizeof(Outs) * n_cands + S * (sizeof(int) + 2 * sizeof(double)) +
-                                    4 * Gn * sizeof(double));
+  const long long d2h = (long long)(out_end - o_outs);
   hpk_timing_bridge::add_partition(ms, h2d, d2h);
   for (int k = 0; k < n_cands; ++k) {
     const Cand& c = hc[k];
@@ -622,26 +637,6 @@ extern "C" int hpk_partition_cost(const hpk_plan_candidate* cands, int n_cands,
       if (r.group_bubble) r.group_bubble[j] = hbub[c.group_base + j];
     }
   }
-  cudaFree(d_c);
-  cudaFree(d_goff);
-  cudaFree(d_mb);
-  cudaFree(d_sty);
-  cudaFree(d_sidx);
-  cudaFree(d_snode);
-  cudaFree(d_srank);
-  cudaFree(d_layers);
-  cudaFree(d_scap);
-  cudaFree(d_prof);
-  cudaFree(d_tt);
-  cudaFree(d_tm);
-  cudaFree(d_gbest);
-  cudaFree(d_time);
-  cudaFree(d_mem);
-  cudaFree(d_fill);
-  cudaFree(d_steady);
-  cudaFree(d_total);
-  cudaFree(d_bubble);
-  cudaFree(d_outs);
   return 0;
 }
 

@@ -8,11 +8,13 @@
 // line by line; the arithmetic of the hot path runs on the B200:
 //   * every TP dimension's DP-grouping search is one problem of ONE batched
 //     hpk_grouping_search launch (grouping.cpp:269-335 semantics, bit-exact);
+//   * every candidate's stage-mapper DP-affinity pass (stage_map.cpp:188-214)
+//     is one CTA of ONE batched hpk_stage_affinity launch;
 //   * every candidate's layer partition + Eq. (1) cost is one CTA of ONE
 //     batched hpk_partition_cost launch (partition.cpp:51-110, cost.cpp:29-147).
 // Host work left here: option handling, TP-unit formation (build_tp_units,
-// reference code), the reference stage mapper (map_nodes_and_stages,
-// stage_map.cpp:63-216) and plan assembly/validation. There is no CPU
+// reference code), the stage mapper's joint / fallback placement (restated,
+// stage_map.cpp:63-186) and plan assembly/validation. There is no CPU
 // fallback: without a CUDA device plan_cluster throws InternalError.
 #include <algorithm>
 #include <atomic>
@@ -101,12 +103,158 @@ Pending capture(Fn&& fn) {
   return p;
 }
 
+// Stage mapping, map_nodes_and_stages (stage_map.cpp:63-216), restated: the
+// joint weakest-type-first phase and the fallback fill (:76-186) run here on
+// the host (cheap, data-dependent control); the DP-affinity hill climb
+// (:188-214, ~3.5 ms per 64-unit candidate on the host) runs on the GPU for
+// every candidate of the planning call in one hpk_stage_affinity launch.
+// Units are pooled in (node, first local rank) order (:84-91) — a strict
+// order, so the unstable sort of the reference is deterministic.
+StageMapping premap_stages(const ClusterSpec& spec, const GroupingSolution& grouping) {
+  for (const auto& kv : grouping.assignment) {
+    if (!spec.has_device(kv.first)) {
+      throw InvalidArgumentError("grouping references device " + kv.first.str() +
+                                 " absent from the cluster spec");
+    }
+  }
+  const int G = (int)grouping.groups.size();
+  // dense type ids; need[g][type] = the group's remaining slots of that type
+  std::map<std::string, int> tid;
+  std::vector<const TpUnit*> pool;
+  for (const auto& grp : grouping.groups)
+    for (const auto& u : grp) {
+      pool.push_back(&u);
+      tid.emplace(u.gpu_type, (int)tid.size());
+    }
+  const int T = (int)tid.size();
+  std::vector<int> need((size_t)G * T, 0);
+  for (int g = 0; g < G; ++g)
+    for (const auto& u : grouping.groups[g]) need[(size_t)g * T + tid.at(u.gpu_type)] += 1;
+  std::sort(pool.begin(), pool.end(), [](const TpUnit* a, const TpUnit* b) {
+    if (a->node_id != b->node_id) return a->node_id < b->node_id;
+    return a->devices.front().local_rank < b->devices.front().local_rank;
+  });
+  const int N = (int)pool.size();
+  std::vector<int> ptype(N);
+  for (int i = 0; i < N; ++i) ptype[i] = tid.at(pool[i]->gpu_type);
+  std::vector<char> taken(N, 0);
+  // types by (power of the first pooled unit of the type, name) (:93-104)
+  std::vector<std::pair<double, std::string>> order;
+  {
+    std::vector<char> seen(T, 0);
+    for (int i = 0; i < N; ++i)
+      if (!seen[ptype[i]]) {
+        seen[ptype[i]] = 1;
+        order.push_back({pool[i]->power, pool[i]->gpu_type});
+      }
+    std::sort(order.begin(), order.end());
+  }
+  StageMapping mapping;
+  mapping.groups.assign(G, {});
+  std::vector<int> next_stage(G, 1);
+  auto place = [&](int g, int i) {
+    taken[i] = 1;
+    need[(size_t)g * T + ptype[i]] -= 1;
+    mapping.groups[g].stages.push_back({next_stage[g]++, *pool[i]});
+  };
+  // joint phase (:106-163): the weakest type with units left goes to every
+  // group at once, all from the lowest-id node holding >= G of them
+  while (true) {
+    int t = -1;
+    std::string tname;
+    for (const auto& pr : order) {
+      const int k = tid.at(pr.second);
+      for (int i = 0; i < N && t < 0; ++i)
+        if (!taken[i] && ptype[i] == k) t = k;
+      if (t >= 0) {
+        tname = pr.second;
+        break;
+      }
+    }
+    if (t < 0) break;
+    bool all_need = true;
+    for (int g = 0; g < G && all_need; ++g) all_need = need[(size_t)g * T + t] > 0;
+    if (!all_need) {
+      mapping.joint_phase_completed = false;
+      mapping.halt_reason = "type " + tname + " is not needed by every DP group";
+      break;
+    }
+    std::map<int, std::vector<int>> by_node;  // ascending node id, pool order inside
+    for (int i = 0; i < N; ++i)
+      if (!taken[i] && ptype[i] == t) by_node[pool[i]->node_id].push_back(i);
+    const std::vector<int>* supply = nullptr;
+    for (const auto& kv : by_node)
+      if ((int)kv.second.size() >= G) {
+        supply = &kv.second;
+        break;
+      }
+    if (!supply) {
+      mapping.joint_phase_completed = false;
+      mapping.halt_reason = "no single node can host a " + tname + " stage for every DP group";
+      break;
+    }
+    for (int g = 0; g < G; ++g) place(g, (*supply)[g]);
+  }
+  // fallback (:165-186): leftovers in (power, node, rank) order, each to the
+  // first group still needing its type
+  std::vector<int> rest;
+  for (int i = 0; i < N; ++i)
+    if (!taken[i]) rest.push_back(i);
+  std::sort(rest.begin(), rest.end(), [&](int a, int b) {
+    const TpUnit& x = *pool[a];
+    const TpUnit& y = *pool[b];
+    if (x.power != y.power) return x.power < y.power;
+    if (x.node_id != y.node_id) return x.node_id < y.node_id;
+    return x.devices.front().local_rank < y.devices.front().local_rank;
+  });
+  for (int i : rest) {
+    int g = 0;
+    while (g < G && need[(size_t)g * T + ptype[i]] <= 0) ++g;
+    HP_CHECK(g < G, "every pooled unit belongs to some group's type multiset");
+    place(g, i);
+  }
+  for (int g = 0; g < G; ++g) {
+    HP_CHECK(mapping.groups[g].stages.size() == grouping.groups[g].size(),
+             "stage count matches the grouping");
+  }
+  return mapping;
+}
+
+// The GPU affinity pass's inputs for a pre-mapped candidate.
+struct AffinityIn {
+  std::vector<int> goff, type, node, perm;
+};
+AffinityIn affinity_inputs(const StageMapping& m) {
+  AffinityIn a;
+  std::map<std::string, int> tid;
+  a.goff.push_back(0);
+  for (const auto& g : m.groups) {
+    for (const auto& st : g.stages) {
+      a.type.push_back(tid.emplace(st.unit.gpu_type, (int)tid.size()).first->second);
+      a.node.push_back(st.unit.node_id);
+    }
+    a.goff.push_back((int)a.type.size());
+  }
+  a.perm.assign(a.type.size(), 0);
+  return a;
+}
+// Applies the swaps (slot s now holds the unit of slot perm[s]).
+void apply_affinity(StageMapping& m, const AffinityIn& a) {
+  std::vector<TpUnit> units;
+  for (const auto& g : m.groups)
+    for (const auto& st : g.stages) units.push_back(st.unit);
+  size_t s = 0;
+  for (auto& g : m.groups)
+    for (auto& st : g.stages) st.unit = units[a.perm[s++]];
+}
+
 // One candidate = one grouping of one TP dimension, mapped to stages.
 struct Candidate {
   int tp = 0;
   const GroupingSolution* grouping = nullptr;
-  Pending map_error;  // from map_nodes_and_stages
+  Pending map_error;  // from the stage mapping (premap_stages)
   StageMapping mapping;
+  AffinityIn aff;     // the GPU affinity pass of the mapping
   std::vector<int> microbatches;
   // flattened GPU inputs
   std::vector<int> goff, stype, sindex, snode, srank0;
@@ -160,7 +308,6 @@ struct PlanJob {
   std::vector<hpk_plan_candidate> pin;
   std::vector<int> pin_of;
   std::vector<hpk_plan_result> pres;
-  int map_threads = 1;        // host threads for this job's stage mapping
   std::exception_ptr error;  // raised by a phase; the job is finished
   std::optional<ParallelPlan> plan;
   PlanJob(const ClusterSpec& s, const ModelConfig& c, const ProfileTable& p, const MemoryModel& m,
@@ -290,16 +437,9 @@ void job_prepare(PlanJob& J) {
 // phase 3: groupings -> stage mapping -> candidate inputs (host)
 void job_candidates(PlanJob& J) {
   const ClusterSpec& spec = J.spec;
-  const ModelConfig& cfg = J.cfg;
-  const ProfileTable& profile = J.profile;
-  const MemoryModel& memmodel = J.memmodel;
-  const PlannerOptions& options = J.options;
   auto& work = J.work;
   auto& gres = J.gres;
   auto& cands = J.cands;
-  auto& pin = J.pin;
-  auto& pin_of = J.pin_of;
-  auto& pres = J.pres;
   for (auto& tw : work) {
     if (tw.problem < 0) continue;
     const hpk_grouping_result& r = gres[tw.problem];
@@ -336,19 +476,27 @@ void job_candidates(PlanJob& J) {
       cands.push_back(std::move(c));
     }
   }
-  // the reference stage mapper (stage_map.cpp:63-216; reentrant, up to ~7 ms
-  // for 64 units) runs for the candidates concurrently, one host thread each
-  auto map_one = [&](Candidate& c) {
-    c.map_error = capture([&] { c.mapping = map_nodes_and_stages(spec, *c.grouping, c.tp); });
-  };
-  if (cands.size() > 1 && J.map_threads > 1) {
-    std::vector<std::thread> pool;
-    for (size_t ci = 1; ci < cands.size(); ++ci) pool.emplace_back(map_one, std::ref(cands[ci]));
-    map_one(cands[0]);
-    for (auto& t : pool) t.join();
-  } else {
-    for (auto& c : cands) map_one(c);
+  // stage mapping, joint + fallback phases (host); the affinity pass follows
+  // on the GPU for every candidate of the call (plan_jobs)
+  for (auto& c : cands) {
+    c.map_error = capture([&] { c.mapping = premap_stages(spec, *c.grouping); });
+    if (c.map_error.kind == Pending::NONE) c.aff = affinity_inputs(c.mapping);
   }
+}
+
+// phase 3b: mapped candidates -> partition / cost inputs (host)
+void job_partition_inputs(PlanJob& J) {
+  const ClusterSpec& spec = J.spec;
+  const ModelConfig& cfg = J.cfg;
+  const ProfileTable& profile = J.profile;
+  const MemoryModel& memmodel = J.memmodel;
+  const PlannerOptions& options = J.options;
+  auto& cands = J.cands;
+  auto& pin = J.pin;
+  auto& pin_of = J.pin_of;
+  auto& pres = J.pres;
+  for (auto& c : cands)
+    if (c.map_error.kind == Pending::NONE) apply_affinity(c.mapping, c.aff);
   int n_bits = 0;
   while ((1 << n_bits) <= cfg.n_layers) ++n_bits;
   pin_of.assign(cands.size(), -1);
@@ -642,7 +790,40 @@ void plan_jobs(std::vector<PlanJob*>& jobs, int threads) {
   }
   clk.lap("search");
   for_jobs(jobs, threads, job_candidates);
-  clk.lap("candidates(map)");
+  clk.lap("candidates(premap)");
+  // ---- phase 3 (GPU): the stage mapper's affinity pass, every candidate at once
+  {
+    std::vector<hpk_affinity_problem> ap;
+    std::vector<PlanJob*> aowner;
+    for (PlanJob* J : jobs) {
+      if (J->error) continue;
+      for (auto& c : J->cands) {
+        if (c.map_error.kind != Pending::NONE) continue;
+        hpk_affinity_problem a;
+        a.n_groups = (int)c.aff.goff.size() - 1;
+        a.n_slots = (int)c.aff.type.size();
+        a.group_off = c.aff.goff.data();
+        a.slot_type = c.aff.type.data();
+        a.slot_node = c.aff.node.data();
+        a.slot_perm = c.aff.perm.data();
+        a.swaps = 0;
+        ap.push_back(a);
+        aowner.push_back(J);
+      }
+    }
+    if (!ap.empty()) {
+      try {
+        const int rc = hpk_stage_affinity(ap.data(), (int)ap.size(), -1);
+        if (rc != 0) gpu_fail(rc);
+      } catch (...) {
+        for (PlanJob* J : aowner) J->error = std::current_exception();
+        return;
+      }
+    }
+  }
+  clk.lap("affinity");
+  for_jobs(jobs, threads, job_partition_inputs);
+  clk.lap("partition-inputs");
   // ---- phase 4: one batched GPU launch for every candidate's partition + cost
   std::vector<hpk_plan_candidate> pin;
   std::vector<hpk_plan_result> pres;
@@ -676,7 +857,6 @@ ParallelPlan plan_cluster(const ClusterSpec& spec, const ModelConfig& cfg,
                           const ProfileTable& profile, const MemoryModel& memmodel,
                           const PlannerOptions& options) {
   PlanJob job(spec, cfg, profile, memmodel, options);
-  job.map_threads = 8;  // a single plan: its candidates map concurrently
   std::vector<PlanJob*> jobs{&job};
   plan_jobs(jobs, 1);
   if (job.error) std::rethrow_exception(job.error);
