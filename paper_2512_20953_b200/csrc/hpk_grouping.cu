@@ -222,7 +222,6 @@ struct SchedSmem {
   // TOPK mode
   double tv[KW];       // predicted cutoff state (push_items)
   int ntv, sp_imp, fi, nq;
-  int qpos[TILE];      // committed positions whose candidates may enter the global list
 };
 
 // --------------------------------------------------------------- warp DFS
@@ -244,8 +243,7 @@ struct WarpSmem {
   double T[KW];
   double robj[KW];
   int rG[KW];
-  int nT, rn;
-  uint8_t rrgs[KW][MAXN];
+  int nT, rn;  // (the candidates' RGS rows live in the run's CandRec, global)
 };
 
 // ---- TOPK helpers (grouping.cpp:110-132)
@@ -556,30 +554,84 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
   }
   __syncwarp();
   // the segment is the children [u[dpar], hi] of the parent (each with its
-  // subtree); they are visited, checked and entered by the loop below exactly
-  // like the children of any other node (grouping.cpp:171-201)
+  // subtree). A range is visited, checked and entered by the loop below like
+  // the children of any other node (grouping.cpp:171-201); a single child is
+  // entered directly (one visit, one node check) and the loop starts inside it.
   const int dpar = du - 1;
   const int hi = E->hi;
-  int d = dpar;
+  const bool single = hi == sm->path[dpar];
+  const int dtop = single ? du : dpar;  // the loop ends when this level is exhausted
+  int d = dtop;
   double cut = C;
   double Sd, Dd;
+  if (single) {  // enter the segment root u
+    const int i = du - 1;
+    const int grp = sm->path[i];
+    add_unit(P, g, lane, grp, P.p[i], P.m[i]);
+    if (grp == G) ++G;
+    if (lane == 0) sm->lvl[du] = (unsigned)G << 16;
+    o.visits = 1;
+    __syncwarp();
+    if (d == n) {  // the root is a leaf (grouping.cpp:138-149)
+      bool infeas = false;
+      double z = INFINITY;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if (g.gc[k] > 0) {
+          if (g.gm[k] < P.min_mem) infeas = true;
+          const double e = slot_eff(P, g, k);
+          z = e < z ? e : z;
+        }
+      }
+      const bool any_infeas = __any_sync(HPK_FULL_MASK, infeas);
+      z = warp_min(z);
+      if (!any_infeas) {
+        const double obj = (double)G * z;
+        o.has_best = true;
+        o.best_obj = obj;
+        o.best_G = G;
+        o.m = obj;
+        if (TOPK) {
+          if (lane == 0) {
+            if (obj > cut) state_insert(sm->T, &sm->nT, tk, obj);
+          }
+          cand_insert(sm->robj, sm->rG, rec->rgs, &sm->rn, tk, n, obj, G,
+                      [&](int i) { return sm->path[i]; }, lane);
+        } else {
+          for (int i = lane; i < n; i += 32) sm->best[i] = sm->path[i];
+        }
+      }
+      o.finished = true;
+      goto done;
+    }
+  }
   {
     const double le = slot_eff(P, g, 0) + slot_eff(P, g, 1);
     const double ld = slot_def(P, g, 0) + slot_def(P, g, 1);
     Sd = warp_sum_approx(le);
     Dd = warp_sum_approx(ld);
   }
+  if (single) {  // node check of u itself
+    int dec = decide(P, Sd + P.R[d], Dd, d, cut);
+    if (dec == DEC_EXACT) dec = exact_passes(P, g, G, d, cut) ? DEC_PASS : DEC_PRUNE;
+    if (dec == DEC_PRUNE) {
+      if (prefix) o.a_star = du;
+      o.finished = true;
+      goto done;
+    }
+  }
   {
     const double kNaN = __longlong_as_double(0x7ff8000000000000LL);
     const double mm_ = P.min_mem, mb = P.mb_abs, md = P.md_abs;
-    int c = sm->path[dpar];           // next child of the current node
+    const int hil = single ? 255 : hi;  // last child at level dtop (single: all of them)
+    int c = single ? 0 : (int)sm->path[dpar];  // next child of the current node
     double up = P.p[d], um = P.m[d];  // unit d: assigned by the children
     unsigned long long mp = 0, mr = 0;
     double mc = kNaN;                 // cutoff of mp/mr (NaN: not computed)
     double lS[2] = {0, 0}, lD[2] = {0, 0};  // this lane's children's level sums
     bool sums_ok = false;             // lS/lD belong to the current node
-    int match = prefix ? dpar : -1;   // path == end marker on levels < match
-    int ec = prefix ? sm->endp[dpar] : -1;  // end child at level `match`
+    int match = prefix ? dtop : -1;   // path == end marker on levels < match
+    int ec = (prefix && dtop < dend) ? sm->endp[dtop] : -1;  // end child at level `match`
     unsigned it = 0;
     int stop_pending = 0;  // stop flag loaded 32 iterations ago (latency off the chain)
 
@@ -616,7 +668,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
       if (d == n - 1) {
         // ---- leaf batch: children c0..G are leaves (unit n-1) ----
         const int c0 = c;
-        const int lim = d == dpar ? hi : G;  // last child of this node in the segment
+        const int lim = d == dtop && hil < G ? hil : G;  // last child of this node in the segment
         int count = lim + 1 - c0;
         bool end_hit = false;
         if (prefix && match == d) {  // dend == n here
@@ -719,7 +771,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
                   const double v = shfl(obj_s[k], l);
                   const int gv = shfl(gc_s[k], l);
                   const int ch = l + 32 * k;
-                  cand_insert(sm->robj, sm->rG, sm->rrgs, &sm->rn, tk, n, v, gv,
+                  cand_insert(sm->robj, sm->rG, rec->rgs, &sm->rn, tk, n, v, gv,
                               [&](int i) { return i < n - 1 ? sm->path[i] : (uint8_t)ch; }, lane);
                 }
               }
@@ -790,8 +842,8 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
         }
         c = lim + 1;
       }
-      if (c > (d == dpar ? hi : G)) {  // node exhausted: pop unit d-1
-        if (d == dpar) {
+      if (c > (d == dtop && hil < G ? hil : G)) {  // node exhausted: pop unit d-1
+        if (d == dtop) {
           o.finished = true;
           break;
         }
@@ -851,7 +903,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
           lS[k] = (Sd - eff_old) + eff_new;
           lD[k] = (Dd - def_old) + def_new;
           const double A = lS[k] + Rn;
-          const bool valid = ci <= (d == dpar ? hi : G);
+          const bool valid = ci <= (d == dtop && hil < G ? hil : G);
           pr[k] = !valid || (hc && A + mb < cut) || (lD[k] - md > RMn);
           ps[k] = !pr[k] && (!hc || A - mb >= cut) && (lD[k] + md <= RMn);
         }
@@ -868,7 +920,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
         // children c .. c+k-1 are all pruned: k visits, nothing entered
         const unsigned long long rest = ~(mr >> c);
         int k = rest ? __ffsll((long long)rest) - 1 : 64 - c;
-        const int lim = d == dpar ? hi : G;
+        const int lim = d == dtop && hil < G ? hil : G;
         if (k > lim + 1 - c) k = lim + 1 - c;
         if ((long long)k > cap - o.visits) k = (int)(cap - o.visits);
         if (prefix && match == d) {
@@ -948,8 +1000,6 @@ done:
       o.best_obj = sm->robj[0];
       o.best_G = sm->rG[0];
     }
-    for (int r = 0; r < rn; ++r)
-      for (int i = lane; i < n; i += 32) rec->rgs[r][i] = sm->rrgs[r][i];
     if (lane < rn) {
       rec->obj[lane] = sm->robj[lane];
       rec->G[lane] = sm->rG[lane];
@@ -1961,13 +2011,15 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
       int nqt;
       int qo = block_excl_scan_1<int>(nql, 0, sh->i, OpAddI(), &nqt);
       if (nqt > 0) {
+        // (the problem's scan scratch is free during the commit walk)
+        int* qpos = kp.scratch + (size_t)p * (kp.lcap + 1);
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-          if (qk[k]) sh->qpos[qo++] = r0 + k;
+          if (qk[k]) qpos[qo++] = r0 + k;
         __syncthreads();
         if (warp == 0)
           for (int t = 0; t < nqt; ++t)
-            merge_run_cands(S, crec[ids_out[i + sh->qpos[t]]], tk, P.n, lane);
+            merge_run_cands(S, crec[ids_out[i + qpos[t]]], tk, P.n, lane);
         __syncthreads();
       }
     } else {
@@ -3130,9 +3182,10 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     }
     int max_n = 1;
     for (int k = 0; k < P; ++k) max_n = std::max(max_n, problems[wave_ix[k]].n);
-    // piece shape: sibling ranges (default; measured equal on cfg4 and 1.3x
-    // faster on cfg5 than single-sibling pieces); HPK_RANGES=0 for the latter
-    const int ranges = getenv("HPK_RANGES") ? atoi(getenv("HPK_RANGES")) : 1;
+    // piece shape: sibling ranges for big batches (cfg5: 1.3x faster, shorter
+    // lists), single siblings for a few problems (cfg3: 1.9x faster — more
+    // parallel pieces near one search's commit front); HPK_RANGES overrides
+    const int ranges = getenv("HPK_RANGES") ? atoi(getenv("HPK_RANGES")) : (P > 16 ? 1 : 0);
     const int reserve = ranges ? max_n + 64                          // one piece per level
                                : max_n * (max_n + 1) / 2 + 32;  // one per sibling, worst case
     if (pcap < 4 * reserve) pcap = 4 * reserve;
