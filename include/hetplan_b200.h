@@ -163,7 +163,7 @@ typedef struct hpk_grouping_result {
   int status;                        /* 0 ok, 3 infeasible ((3b): no feasible partition) */
   int count;                         /* solutions (<= top_k), best first */
   int optimal;                       /* 0 if the node budget ran out (grouping.cpp:317) */
-  int engine;                        /* 0 = parallel wave engine, 1 = serial replica kernel */
+  int engine;                        /* 0 wave engine, 1 serial replica, 2 enumeration */
   long long visited;                 /* GroupingSolution::nodes_visited */
   double objective[HPK_MAX_TOPK];
   double z[HPK_MAX_TOPK];
@@ -181,6 +181,8 @@ typedef struct hpk_search_config {
   long long segment_cap; /* visits per segment run per wave (0: default) */
   int max_list;          /* segment list capacity per problem (0: default) */
   int force_serial;      /* 1: use the serial replica kernel for every problem */
+  int enumerate;         /* 1: exhaustive top_k = 1 problems with n <= 12 take the
+                            enumeration engine (engine 2: winner only, visited = -1) */
   int max_waves;         /* watchdog on the wave loop (0: default 1000000) */
   double max_seconds;    /* device wall-clock watchdog (0: default 120 s) */
 } hpk_search_config;

@@ -2905,6 +2905,145 @@ __global__ void hpk_serial_kernel(SerialProb* probs, int n_probs, SerialCand* ca
   pb.optimal = optimal ? 1 : 0;
 }
 
+// ------------------------------------------------------ enumeration engine
+// Exhaustive searches (n <= exact_threshold) with top_k = 1 on the planner
+// path: the reference's winner is the global maximum of the key (objective
+// desc, #groups asc, enumeration order asc) over every feasible leaf — the
+// prune floor is a seed's objective and that seed is itself a leaf, so bound
+// pruning never removes a leaf that could win.
+// Every restricted-growth string is unranked in lexicographic (= DFS preorder)
+// order and evaluated with fresh sums, which equal the DFS's incremental
+// sums under the value contract. Visits are not counted (the plan does not
+// report them), so the search config opts in (hpk_search_config::enumerate).
+constexpr int ENUM_MAXN = 12;  // Bell(12) = 4,213,597 leaves
+
+struct EnumProb {
+  int n, K;
+  double min_mem;
+  double p[ENUM_MAXN], m[ENUM_MAXN];
+  long long total;  // Bell(n)
+  int block0, nblocks;
+};
+struct EnumBest {
+  double obj;
+  int G;
+  long long rank;
+};
+
+// D[r][g]: completions of an RGS prefix with r positions left and g groups used
+struct EnumTable {
+  long long D[ENUM_MAXN + 1][ENUM_MAXN + 2];
+};
+
+__device__ __forceinline__ bool enum_better(double ao, int ag, long long ar, double bo, int bg,
+                                            long long br) {
+  if (ao != bo) return ao > bo;
+  if (ag != bg) return ag < bg;
+  return ar < br;
+}
+
+__global__ void __launch_bounds__(256) hpk_enum_kernel(const EnumProb* probs, int n_probs,
+                                                       const EnumTable* tab, EnumBest* out,
+                                                       int per_block) {
+  // block -> (problem, chunk of ranks)
+  int pi = 0;
+  while (pi + 1 < n_probs && probs[pi + 1].block0 <= (int)blockIdx.x) ++pi;
+  const EnumProb& P = probs[pi];
+  const int n = P.n;
+  const long long lo = (long long)(blockIdx.x - P.block0) * per_block;
+  const long long hi = min(P.total, lo + per_block);
+  double bo = -1.0;
+  int bg = 0;
+  long long br = 0x7fffffffffffffffLL;
+  for (long long rk = lo + threadIdx.x; rk < hi; rk += blockDim.x) {
+    // unrank (lexicographic RGS): digit 0 is 0; each later digit is an
+    // existing group (D[r][g] completions each) or the new group g
+    int a[ENUM_MAXN];
+    a[0] = 0;
+    int g = 1;
+    long long k = rk;
+#pragma unroll
+    for (int i = 1; i < ENUM_MAXN; ++i) {
+      if (i < n) {
+        const int r = n - 1 - i;
+        const long long w = tab->D[r][g];
+        long long q = k / w;
+        if (q < g) {
+          a[i] = (int)q;
+          k -= q * w;
+        } else {
+          a[i] = g;
+          k -= (long long)g * w;
+          ++g;
+        }
+      }
+    }
+    // leaf (grouping.cpp:138-149): every group's memory >= MIN_mem, z = the
+    // running min of the groups' Eq. (2) effective powers in group order
+    bool ok = true;
+    double z = 0;
+    for (int gi = 0; gi < g; ++gi) {
+      double pw = 0, me = 0;
+      int cnt = 0;
+#pragma unroll
+      for (int i = 0; i < ENUM_MAXN; ++i) {
+        if (i < n && a[i] == gi) {
+          pw += P.p[i];
+          me += P.m[i];
+          ++cnt;
+        }
+      }
+      if (me < P.min_mem) {
+        ok = false;
+        break;
+      }
+      const double rho = (double)(cnt - 1) / (double)(P.K + cnt - 1);
+      const double e = pw * (1.0 - rho);
+      z = gi == 0 ? e : (e < z ? e : z);
+    }
+    if (!ok) continue;
+    const double obj = (double)g * z;
+    if (bo < 0 || enum_better(obj, g, rk, bo, bg, br)) {
+      bo = obj;
+      bg = g;
+      br = rk;
+    }
+  }
+  // block reduction of the key
+  __shared__ double so[8];
+  __shared__ int sg[8];
+  __shared__ long long sr[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double oo = __shfl_xor_sync(HPK_FULL_MASK, bo, o);
+    const int og = __shfl_xor_sync(HPK_FULL_MASK, bg, o);
+    const long long orr = __shfl_xor_sync(HPK_FULL_MASK, br, o);
+    if (oo >= 0 && (bo < 0 || enum_better(oo, og, orr, bo, bg, br))) {
+      bo = oo;
+      bg = og;
+      br = orr;
+    }
+  }
+  if (lane == 0) {
+    so[warp] = bo;
+    sg[warp] = bg;
+    sr[warp] = br;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      if (so[w] >= 0 && (bo < 0 || enum_better(so[w], sg[w], sr[w], bo, bg, br))) {
+        bo = so[w];
+        bg = sg[w];
+        br = sr[w];
+      }
+    out[blockIdx.x].obj = bo;
+    out[blockIdx.x].G = bg;
+    out[blockIdx.x].rank = br;
+  }
+}
+
 }  // namespace hpk
 
 // ================================================================== host
@@ -2941,6 +3080,7 @@ struct DeviceCtx {
   int* active = nullptr;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  HpkArena arena;  // enumeration engine's inputs / outputs
   std::mutex mu;
 };
 
@@ -3111,6 +3251,7 @@ void hpk_search_config_init(hpk_search_config* cfg) {
   cfg->segment_cap = 0;
   cfg->max_list = 0;
   cfg->force_serial = 0;
+  cfg->enumerate = 0;
   cfg->max_waves = 0;
   cfg->max_seconds = 0;
 }
@@ -3143,7 +3284,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
   HPK_CUDA(cudaSetDevice(device));
 
   // Partition problems between the engines.
-  std::vector<int> wave_ix, serial_ix;
+  std::vector<int> wave_ix, serial_ix, enum_ix;
   for (int i = 0; i < n_problems; ++i) {
     const hpk_grouping_problem& pr = problems[i];
     results[i].status = 0;
@@ -3160,7 +3301,103 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     const bool contract = exact_sums(pr.power, pr.n, 0, false) &&
                           exact_sums(pr.memory, pr.n, 0, false);
     const bool wave_ok = !cfg.force_serial && pr.n <= MAXN && pr.top_k <= KW && contract;
-    (wave_ok ? wave_ix : serial_ix).push_back(i);
+    const bool enum_ok = wave_ok && cfg.enumerate && pr.n <= pr.exact_threshold &&
+                         pr.n <= ENUM_MAXN && pr.top_k <= 1;
+    (enum_ok ? enum_ix : wave_ok ? wave_ix : serial_ix).push_back(i);
+  }
+
+  // ---------------- enumeration engine (exhaustive, top_k = 1, planner path)
+  if (!enum_ix.empty()) {
+    EnumTable tab;
+    std::memset(&tab, 0, sizeof(tab));
+    for (int g = 0; g <= ENUM_MAXN + 1; ++g) tab.D[0][g] = 1;
+    for (int r = 1; r <= ENUM_MAXN; ++r)
+      for (int g = 0; g <= ENUM_MAXN; ++g) tab.D[r][g] = g * tab.D[r - 1][g] + tab.D[r - 1][g + 1];
+    const int per_block = 4096;
+    const int E = (int)enum_ix.size();
+    std::vector<EnumProb> ep(E);
+    int nblocks = 0;
+    for (int k = 0; k < E; ++k) {
+      const hpk_grouping_problem& pr = problems[enum_ix[k]];
+      EnumProb& e = ep[k];
+      std::memset(&e, 0, sizeof(e));
+      e.n = pr.n;
+      e.K = pr.n_microbatches;
+      e.min_mem = pr.min_mem;
+      for (int i = 0; i < pr.n; ++i) {
+        e.p[i] = pr.power[i];
+        e.m[i] = pr.memory[i];
+      }
+      e.total = tab.D[pr.n - 1][1];  // Bell(n): digit 0 is fixed
+      e.block0 = nblocks;
+      e.nblocks = (int)((e.total + per_block - 1) / per_block);
+      nblocks += e.nblocks;
+    }
+    HpkArena& ar = c.arena;
+    ar.reset();
+    const size_t o_p = ar.take(sizeof(EnumProb) * E);
+    const size_t o_t = ar.take(sizeof(EnumTable));
+    const size_t in_end = ar.used;
+    const size_t o_b = ar.take(sizeof(EnumBest) * nblocks);
+    HPK_CUDA(ar.fit());
+    std::memcpy(ar.h + o_p, ep.data(), sizeof(EnumProb) * E);
+    std::memcpy(ar.h + o_t, &tab, sizeof(EnumTable));
+    HPK_CUDA(cudaMemcpyAsync(ar.d, ar.h, in_end, cudaMemcpyHostToDevice, c.stream));
+    HPK_CUDA(cudaEventRecord(c.ev0, c.stream));
+    hpk_enum_kernel<<<nblocks, 256, 0, c.stream>>>(ar.dp<EnumProb>(o_p), E, ar.dp<EnumTable>(o_t),
+                                                   ar.dp<EnumBest>(o_b), per_block);
+    HPK_CUDA(cudaGetLastError());
+    HPK_CUDA(cudaEventRecord(c.ev1, c.stream));
+    HPK_CUDA(cudaMemcpyAsync(ar.h + o_b, ar.d + o_b, sizeof(EnumBest) * nblocks,
+                             cudaMemcpyDeviceToHost, c.stream));
+    HPK_CUDA(cudaStreamSynchronize(c.stream));
+    float ms = 0;
+    HPK_CUDA(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
+    t_timing.search_ms += ms;
+    t_timing.kernel_launches += 1;
+    t_timing.h2d_bytes += (long long)in_end;
+    t_timing.d2h_bytes += (long long)(sizeof(EnumBest) * nblocks);
+    const EnumBest* eb = ar.hp<EnumBest>(o_b);
+    for (int k = 0; k < E; ++k) {
+      const int i = enum_ix[k];
+      const hpk_grouping_problem& pr = problems[i];
+      hpk_grouping_result& r = results[i];
+      EnumBest b{-1.0, 0, 0x7fffffffffffffffLL};
+      for (int q = 0; q < ep[k].nblocks; ++q) {
+        const EnumBest& x = eb[ep[k].block0 + q];
+        if (x.obj >= 0 && (b.obj < 0 || x.obj > b.obj || (x.obj == b.obj && (x.G < b.G ||
+                                                        (x.G == b.G && x.rank < b.rank))))) {
+          b = x;
+        }
+      }
+      r.engine = 2;
+      r.visited = -1;  // not counted by this engine
+      if (b.obj < 0) {  // no feasible leaf: no seed is feasible either (seeds are leaves)
+        r.status = 3;
+        continue;
+      }
+      uint8_t rgs[ENUM_MAXN];
+      rgs[0] = 0;
+      int g = 1;
+      long long kk = b.rank;
+      for (int u = 1; u < pr.n; ++u) {
+        const long long w = tab.D[pr.n - 1 - u][g];
+        const long long q = kk / w;
+        if (q < g) {
+          rgs[u] = (uint8_t)q;
+          kk -= q * w;
+        } else {
+          rgs[u] = (uint8_t)g;
+          kk -= (long long)g * w;
+          ++g;
+        }
+      }
+      r.count = 1;
+      r.optimal = 1;
+      r.objective[0] = b.obj;
+      r.z[0] = leaf_z(pr, rgs, b.G);
+      for (int u = 0; u < pr.n; ++u) r.rgs[u] = rgs[u];
+    }
   }
 
   // ---------------- wave engine

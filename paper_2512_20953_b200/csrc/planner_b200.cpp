@@ -779,8 +779,13 @@ void plan_jobs(std::vector<PlanJob*>& jobs, int threads) {
         throw InternalError("hetplan_b200: no CUDA device visible; the B200 planner has no CPU "
                             "fallback");
       }
+      // the plan needs the winners, not the visit counts: exhaustive top-1
+      // searches take the enumeration engine
+      hpk_search_config scfg;
+      hpk_search_config_init(&scfg);
+      scfg.enumerate = 1;
       const int rc = hpk_grouping_search(problems.data(), (int)problems.size(), gres.data(),
-                                         nullptr);
+                                         &scfg);
       if (rc != 0) gpu_fail(rc);
     } catch (...) {
       for (auto& o : owner) o.first->error = std::current_exception();

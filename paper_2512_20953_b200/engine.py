@@ -58,6 +58,7 @@ class hpk_search_config(C.Structure):
         ("segment_cap", C.c_longlong),
         ("max_list", C.c_int),
         ("force_serial", C.c_int),
+        ("enumerate", C.c_int),
         ("max_waves", C.c_int),
         ("max_seconds", C.c_double),
     ]
@@ -154,7 +155,7 @@ class Engine:
     def grouping_search(self, problems: Sequence[GroupingProblem], *, device: int = -1,
                         segment_cap: int = 0, max_list: int = 0,
                         force_serial: bool = False, max_waves: int = 0,
-                        max_seconds: float = 0.0) -> List[GroupingResult]:
+                        max_seconds: float = 0.0, enumeration: bool = False) -> List[GroupingResult]:
         n = len(problems)
         arr = (hpk_grouping_problem * n)()
         res = (hpk_grouping_result * n)()
@@ -176,6 +177,7 @@ class Engine:
         cfg.segment_cap = segment_cap
         cfg.max_list = max_list
         cfg.force_serial = int(force_serial)
+        cfg.enumerate = int(enumeration)
         cfg.max_waves = max_waves
         cfg.max_seconds = max_seconds
         rc = self.lib.hpk_grouping_search(arr, n, res, C.byref(cfg))

@@ -188,3 +188,21 @@ def test_device_filter_decision_matches_host(engine):
             assert rc == 0
             want = [_host_decide(A, D, 100.0, cut, mb, md) for (A, D, cut) in cases]
             assert list(out) == want
+
+
+def test_enumeration_engine_matches_the_dfs_winner(engine, oracle):
+    """Exhaustive top-1 searches on the enumeration engine (planner path): the
+    winner (RGS, objective, z) equals the reference DFS's — SURVEY.md fact 4."""
+    probs = [GroupingProblem(pb.power, pb.memory, pb.n_microbatches, pb.min_mem, pb.type_key,
+                             pb.node_key, 12, pb.node_budget)
+             for pb in _random_problems(77, 300, nmax=12)]
+    res = engine.grouping_search(probs, enumeration=True, max_seconds=60)
+    for pb, r in zip(probs, res):
+        o = oracle.solve_grouping(pb.power, pb.memory, pb.n_microbatches, pb.min_mem,
+                                  pb.type_key, pb.node_key, 12, pb.node_budget)
+        assert r.engine == 2
+        if o.status != 0:
+            assert r.status == o.status
+            continue
+        assert (r.status, r.rgs, r.objective, r.z, r.optimal) == \
+            (0, o.rgs, o.objective, o.z, o.optimal), pb
