@@ -2961,19 +2961,19 @@ __global__ void __launch_bounds__(256) hpk_enum_kernel(const EnumProb* probs, in
     int a[ENUM_MAXN];
     a[0] = 0;
     int g = 1;
-    long long k = rk;
+    unsigned k = (unsigned)rk;  // Bell(12) < 2^32: 32-bit unranking
 #pragma unroll
     for (int i = 1; i < ENUM_MAXN; ++i) {
       if (i < n) {
         const int r = n - 1 - i;
-        const long long w = tab->D[r][g];
-        long long q = k / w;
-        if (q < g) {
+        const unsigned w = (unsigned)tab->D[r][g];
+        const unsigned q = k / w;
+        if (q < (unsigned)g) {
           a[i] = (int)q;
           k -= q * w;
         } else {
           a[i] = g;
-          k -= (long long)g * w;
+          k -= (unsigned)g * w;
           ++g;
         }
       }
@@ -3201,6 +3201,11 @@ double leaf_z(const hpk_grouping_problem& pr, const uint8_t* rgs, int G) {
 // Hooks shared with hpk_partition.cu (same thread-local error / timing).
 void hpkp_fail(const std::string& msg) { t_err = msg; }
 namespace hpk_timing_bridge {
+void add_launch(long long h2d, long long d2h) {
+  t_timing.kernel_launches += 1;
+  t_timing.h2d_bytes += h2d;
+  t_timing.d2h_bytes += d2h;
+}
 void add_partition(double ms, long long h2d, long long d2h) {
   t_timing.partition_ms += ms;
   t_timing.h2d_bytes += h2d;
@@ -3313,7 +3318,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     for (int g = 0; g <= ENUM_MAXN + 1; ++g) tab.D[0][g] = 1;
     for (int r = 1; r <= ENUM_MAXN; ++r)
       for (int g = 0; g <= ENUM_MAXN; ++g) tab.D[r][g] = g * tab.D[r - 1][g] + tab.D[r - 1][g + 1];
-    const int per_block = 4096;
+    const int per_block = 512;  // spread even the 8-unit cases over several SMs
     const int E = (int)enum_ix.size();
     std::vector<EnumProb> ep(E);
     int nblocks = 0;

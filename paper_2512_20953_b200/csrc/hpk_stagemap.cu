@@ -33,6 +33,9 @@
 #include "hpk_common.cuh"
 
 void hpkp_fail(const std::string& msg);  // thread-local error of the hpk_* layer
+namespace hpk_timing_bridge {
+void add_launch(long long h2d, long long d2h);  // this thread's hpk_timing
+}
 
 namespace hpks {
 
@@ -242,6 +245,7 @@ extern "C" int hpk_stage_affinity(hpk_affinity_problem* probs, int n, int device
                             cudaMemcpyDeviceToHost, cx.stream));
   HPKS_CUDA(cudaStreamSynchronize(cx.stream));
   const int* perm = ar.hp<int>(o_perm);
+  hpk_timing_bridge::add_launch((long long)in_end, (long long)(out_end - o_perm + sizeof(Prob) * n));
   std::memcpy(hp.data(), ar.h + o_probs, sizeof(Prob) * n);
   for (int k = 0; k < n; ++k) {
     for (int s = 0; s < probs[k].n_slots; ++s) probs[k].slot_perm[s] = perm[hp[k].in_off + s];
