@@ -107,6 +107,11 @@ struct GState {
   // cutoff is T[top_k-1] once nT == top_k, else the floor (kth_objective(),
   // grouping.cpp:129-132) — and the global candidate list best-first
   // (SearchState::best, :99, ranking :112-115, insertion after equals :117-127).
+  // parallel push (schedule step S4): published by the problem's commit CTA,
+  // valid when pp_wave == the current wave
+  int pp_wave, pp_mode, pp_head, pp_len, pp_ashift, pp_qmax, pp_ntile;
+  long long pp_bl;
+  double pp_C;
   int nT, nbest;
   double T[KW];
   double bl_obj[KW];
@@ -137,6 +142,12 @@ struct TileAgg {
   int bG, bidx;
 };
 
+// Per-tile aggregate of the parallel push (needs, lower-bound visits).
+struct PushAgg {
+  int stamp, nneed;
+  long long vis;
+};
+
 struct RunItem {
   int problem, pos, id, front;
   long long cap;
@@ -165,6 +176,8 @@ struct KParams {
   int* wcount;        // [2]
   int xtn, wcap;
   TileAgg* agg;       // [P][xtn]
+  PushAgg* pagg;      // [P][xtn]: the parallel push's per-tile aggregates
+  int par_push;       // 1: step D runs as per-tile push items over every CTA
   RunQueue* queues;   // [2]
   RunItem* items;     // [2][qcap]
   int* active;        // problems still running
@@ -1442,6 +1455,220 @@ __device__ void push_items(const KParams& kp, int queue, int p, const int* ids, 
   }
 }
 
+// ---- S4: the queue step of the commit CTAs (push_items, k = 1) spread over
+// every CTA, one item per list tile (the S2 expansion tiles). The predicted
+// cutoff entering tile t is max(C, max objective of the runs in earlier tiles)
+// — from the tile summaries alone, so every tile scans itself independently;
+// the budget window and the queue share (lower-bound visits and needs before
+// the tile) come from the earlier tiles' published aggregates. Items are the
+// sequential push's, in per-tile order.
+__device__ void push_tile(const KParams& kp, int p, int t, int queue, int wave, SchedSmem* sh) {
+  GState& S = kp.states[p];
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    unsigned ns = 32;
+    while (*((volatile int*)&S.pp_wave) != wave) {
+      __nanosleep(ns);
+      ns = ns < 256 ? ns * 2 : 256;
+    }
+    __threadfence();
+  }
+  __syncthreads();
+  if (*((volatile int*)&S.pp_mode) != 1 || t >= S.pp_ntile) {
+    __syncthreads();
+    return;
+  }
+  const int head = S.pp_head, len = S.pp_len, ashift = S.pp_ashift, qmax = S.pp_qmax;
+  const long long bl = S.pp_bl;
+  const double C = S.pp_C;
+  const TileAgg* ag = kp.agg + (size_t)p * kp.xtn;
+  PushAgg* pa = kp.pagg + (size_t)p * kp.xtn;
+  const TileAgg a = ag[t];
+  const int tlo = a.ob - ashift;
+  const int lo = max(tlo, head), hi = min(tlo + a.n, head + len);
+  double cin = C;
+  for (int u = 0; u < t; ++u) cin = ag[u].mmax > cin ? ag[u].mmax : cin;
+  const int cur = S.cur;
+  const int* ids = list_arr(kp, p, cur, 0);
+  const int* pran = list_arr(kp, p, cur, 1);
+  const long long* pvis = list_vis(kp, p, cur);
+  const double* pcut = list_dbl(kp, p, cur, 0);
+  const double* pm = list_dbl(kp, p, cur, 1);
+  const Entry* pool = pool_ptr(kp, p, S.pool_cur);
+  // pass 1: needs and lower-bound visits of the tile
+  long long tvis = 0;
+  int tneed = 0;
+  const bool whole = lo == tlo && hi == tlo + a.n;
+  if (whole && a.nrun == a.n && a.mmax <= cin && a.cutc == cin) {
+    tvis = a.sumvis;  // every run exact under the predicted cutoff
+  } else {
+    double cmax = cin;
+    for (int base = lo; base < hi; base += blockDim.x * 8) {
+      const int j0 = base + threadIdx.x * 8;
+      bool ran[8];
+      double mj[8], cj[8];
+      long long vj[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int j = j0 + k;
+        ran[k] = j < hi && pran[j] == 1;
+        mj[k] = ran[k] ? pm[j] : -1.0;
+        cj[k] = ran[k] ? pcut[j] : -2.0;
+        vj[k] = ran[k] ? pvis[j] : 0;
+      }
+      double tmax = -1.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) tmax = mj[k] > tmax ? mj[k] : tmax;
+      double chunk_max;
+      const double exm = block_excl_scan_1<double>(tmax, -1.0, sh->d, OpMax(), &chunk_max);
+      double run = cmax > exm ? cmax : exm;
+      long long v = 0;
+      int nn = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (j0 + k < hi) {
+          const bool exact = ran[k] && cj[k] == run;
+          v += exact ? vj[k] : 1;
+          nn += exact ? 0 : 1;
+        }
+        run = mj[k] > run ? mj[k] : run;
+      }
+      long long vt;
+      int nt;
+      block_excl_scan_1<long long>(v, 0, sh->l, OpAddL(), &vt);
+      block_excl_scan_1<int>(nn, 0, sh->i, OpAddI(), &nt);
+      tvis += vt;
+      tneed += nt;
+      cmax = chunk_max > cmax ? chunk_max : cmax;
+    }
+  }
+  if (tid == 0) {
+    pa[t].nneed = tneed;
+    pa[t].vis = tvis;
+    __threadfence();
+    *((volatile int*)&pa[t].stamp) = wave;
+  }
+  if (tneed == 0) return;
+  // look-back: needs and visits of the earlier tiles
+  if (tid < 32) {
+    long long bv = 0;
+    int bn = 0;
+    for (int u = tid; u < t; u += 32) {
+      unsigned ns = 32;
+      while (*((volatile int*)&pa[u].stamp) != wave) {
+        __nanosleep(ns);
+        ns = ns < 256 ? ns * 2 : 256;
+      }
+      __threadfence();
+      bv += *((volatile long long*)&pa[u].vis);
+      bn += *((volatile int*)&pa[u].nneed);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      bv += __shfl_xor_sync(HPK_FULL_MASK, bv, o);
+      bn += __shfl_xor_sync(HPK_FULL_MASK, bn, o);
+    }
+    if (tid == 0) {
+      sh->v_before = bv;
+      sh->i[50] = bn;
+    }
+  }
+  __syncthreads();
+  long long before = sh->v_before;
+  int rank0 = sh->i[50];
+  __syncthreads();
+  if (rank0 >= qmax || (bl >= 0 && before >= bl)) return;
+  // pass 2: queue the needing positions inside the budget window, in order
+  RunQueue* q = kp.queues + queue;
+  RunItem* items = kp.items + (size_t)queue * kp.qcap;
+  double cmax = cin;
+  for (int base = lo; base < hi; base += blockDim.x * 8) {
+    const int j0 = base + threadIdx.x * 8;
+    bool ran[8];
+    double mj[8], cj[8];
+    long long vj[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int j = j0 + k;
+      ran[k] = j < hi && pran[j] == 1;
+      mj[k] = ran[k] ? pm[j] : -1.0;
+      cj[k] = ran[k] ? pcut[j] : -2.0;
+      vj[k] = ran[k] ? pvis[j] : 0;
+    }
+    double tmax = -1.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) tmax = mj[k] > tmax ? mj[k] : tmax;
+    double chunk_max;
+    const double exm = block_excl_scan_1<double>(tmax, -1.0, sh->d, OpMax(), &chunk_max);
+    double chat[8];
+    bool need[8];
+    long long vsum = 0;
+    {
+      double run = cmax > exm ? cmax : exm;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        chat[k] = run;
+        run = mj[k] > run ? mj[k] : run;
+        const bool exact = ran[k] && cj[k] == chat[k];
+        vj[k] = (j0 + k < hi) ? (exact ? vj[k] : 1) : 0;
+        need[k] = (j0 + k < hi) && !exact;
+        vsum += vj[k];
+      }
+    }
+    long long chunk_vis;
+    const long long exv = block_excl_scan_1<long long>(vsum, 0, sh->l, OpAddL(), &chunk_vis);
+    int nneed = 0;
+    {
+      long long run = before + exv;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        need[k] = need[k] && (bl < 0 || run < bl);
+        run += vj[k];
+        nneed += need[k] ? 1 : 0;
+      }
+    }
+    int chunk_need;
+    const int exn = block_excl_scan_1<int>(nneed, 0, sh->i, OpAddI(), &chunk_need);
+    if (tid == 0) {
+      const int take = max(0, min(chunk_need, qmax - rank0));
+      sh->i[40] = take;
+      sh->i[41] = take > 0 ? atomicAdd(&q->len, take) : 0;
+    }
+    __syncthreads();
+    const int take = sh->i[40], slot0 = sh->i[41];
+    int r = exn;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (need[k]) {
+        if (r < take) {
+          if (slot0 + r >= kp.qcap) {
+            atomicOr(kp.err, 4);  // must not happen
+          } else {
+            const int j = j0 + k;
+            RunItem& it = items[slot0 + r];
+            const int id = ids[j];
+            it.problem = p;
+            it.pos = j;
+            it.id = id;
+            it.front = (j == head);
+            it.cap = !pool[id].uncapped ? kp.seg_cap
+                     : bl < 0           ? 0x3fffffffffffffffLL
+                                        : bl + 1;
+            it.cut = chat[k];
+            it.ntv = 0;
+          }
+        }
+        ++r;
+      }
+    }
+    rank0 += take;
+    before += chunk_vis;
+    cmax = chunk_max > cmax ? chunk_max : cmax;
+    __syncthreads();
+    if (rank0 >= qmax || (bl >= 0 && before >= bl)) break;
+  }
+}
+
 // ---- list expansion, spread over every CTA (schedule step S2). The list of a
 // problem is cut into tiles of TILE positions; the runners added the piece
 // counts of their splits to xt[tile] (atomic), so a tile's output offset is
@@ -1668,12 +1895,21 @@ __device__ void expand_tile(const KParams& kp, int p, int t, SchedSmem* sh) {
 
 // Per-problem scheduler (one CTA): expand splits, ordered commit, compaction,
 // queue the next wave.
+__device__ void publish_push(GState& S, int mode, int wave) {
+  S.pp_mode = mode;
+  __threadfence();
+  *((volatile int*)&S.pp_wave) = wave;
+}
+
 __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void* smem_tmp,
-                                 int wnext) {
+                                 int wnext, int wave) {
   GState& S = kp.states[p];
   const GProb& P = kp.probs[p];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (S.done) return;
+  if (S.done) {
+    if (tid == 0) publish_push(S, 0, wave);
+    return;
+  }
   const int cur = S.cur, head = S.head, len = S.len;
   int* ids_in = list_arr(kp, p, cur, 0);
   int* pcv_in = list_arr(kp, p, cur, 1);
@@ -1716,6 +1952,7 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
       S.aborted = 1;
       S.rerun_pending = 0;
       finish_problem(kp, S);
+      publish_push(S, 0, wave);
     }
     __syncthreads();
     return;
@@ -2241,12 +2478,28 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
     const int headroom = kp.lcap - kp.reserve - nlen;
     const int qmax = max(1, min(max(32, kp.qmax / act), headroom / est));
     const long long bl = P.budget < 0 ? -1 : P.budget - S.V;
-    push_items(kp, next_queue, p, ids_out, pcv_out, vis_out, cut_out, m_out,
-               pool_ptr(kp, p, S.pool_cur), nhead, nlen, S.C, qmax, bl, sh->l, sh->d, sh->i, ag,
-               nagg, ashift, sh, P.top_k, S.seed_obj,
-               P.top_k > 1 ? cand_ptr(kp, p, S.pool_cur) : nullptr, S);
-    if (tid == 0) S.runs_prev = runs_now;
+    if (kp.par_push && P.top_k <= 1 && nagg > 0) {
+      // the tiles of the list are pushed by every CTA after the commits (S4)
+      if (tid == 0) {
+        S.pp_head = nhead;
+        S.pp_len = nlen;
+        S.pp_ashift = ashift;
+        S.pp_qmax = qmax;
+        S.pp_ntile = nagg;
+        S.pp_bl = bl;
+        S.pp_C = S.C;
+        S.runs_prev = runs_now;
+        publish_push(S, 1, wave);
+      }
+    } else {
+      push_items(kp, next_queue, p, ids_out, pcv_out, vis_out, cut_out, m_out,
+                 pool_ptr(kp, p, S.pool_cur), nhead, nlen, S.C, qmax, bl, sh->l, sh->d, sh->i,
+                 ag, nagg, ashift, sh, P.top_k, S.seed_obj,
+                 P.top_k > 1 ? cand_ptr(kp, p, S.pool_cur) : nullptr, S);
+      if (tid == 0) S.runs_prev = runs_now;
+    }
   }
+  if (tid == 0 && *((volatile int*)&S.pp_wave) != wave) publish_push(S, 0, wave);
   if (warp == 0) {
     if (flag & 2) {
       if (lane == 0) {
@@ -2392,6 +2645,8 @@ __device__ void init_problem(const KParams& kp, int p) {
     S.C = seed_obj;  // prune_floor (:312)
     S.nT = 0;
     S.nbest = 0;
+    S.pp_wave = -1;
+    S.pp_mode = 0;
     for (int t = 0; t < KW; ++t) S.T[t] = -1.0;
     S.V = 0;
     S.has_best = 0;
@@ -2652,7 +2907,19 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
     }
     // S3: commit, compaction, queue the next wave (one CTA per problem)
     for (int p = blockIdx.x; p < kp.n_problems; p += gridDim.x)
-      schedule_problem(kp, p, cur ^ 1, smem_tmp, (wave & 1) ^ 1);
+      schedule_problem(kp, p, cur ^ 1, smem_tmp, (wave & 1) ^ 1, wave);
+    // S4: the queue step, one item per list tile (the S2 items), every CTA;
+    // each item waits for its problem's commit (done before by its own CTA)
+    if (kp.par_push) {
+      const int wb = wave & 1;
+      const int nwk = *((volatile int*)(kp.wcount + wb));
+      SchedSmem* sh = reinterpret_cast<SchedSmem*>(smem_tmp);
+      for (int w = blockIdx.x; w < nwk; w += gridDim.x) {
+        const int2 wk = kp.work[(size_t)wb * kp.wcap + w];
+        push_tile(kp, wk.x, wk.y, cur ^ 1, wave, sh);
+        __syncthreads();
+      }
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       *((volatile int*)kp.stop) = 0;  // re-armed for the next run phase
       unsigned long long now;
@@ -3075,6 +3342,8 @@ struct DeviceCtx {
   size_t cap_work = 0;
   TileAgg* agg = nullptr;
   size_t cap_agg = 0;
+  PushAgg* pagg = nullptr;
+  size_t cap_pagg = 0;
   RunQueue* queues = nullptr;
   RunItem* items = nullptr;
   int* active = nullptr;
@@ -3462,6 +3731,8 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     if (int rc = grow(c.xt, c.cap_xt, (size_t)P * xtn)) return rc;
     if (int rc = grow(c.work, c.cap_work, (size_t)2 * P * xtn)) return rc;
     if (int rc = grow(c.agg, c.cap_agg, (size_t)P * xtn)) return rc;
+    if (int rc = grow(c.pagg, c.cap_pagg, (size_t)P * xtn)) return rc;
+    HPK_CUDA(cudaMemsetAsync(c.pagg, 0xff, sizeof(PushAgg) * P * xtn, c.stream));  // stamps -1
     HPK_CUDA(cudaMemsetAsync(c.xt, 0, sizeof(int) * P * xtn, c.stream));
     const int grid = c.sms * c.blocks_per_sm;
     const int nwarps = grid * WARPS_PER_BLOCK;
@@ -3493,6 +3764,8 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     kp.xt = c.xt;
     kp.xtn = xtn;
     kp.agg = c.agg;
+    kp.pagg = c.pagg;
+    kp.par_push = getenv("HPK_PAR_PUSH") ? atoi(getenv("HPK_PAR_PUSH")) : 1;
     kp.work = c.work;
     kp.wcap = P * xtn;
     kp.wcount = c.active + 60;
