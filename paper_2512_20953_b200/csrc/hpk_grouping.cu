@@ -189,6 +189,7 @@ struct KParams {
   int ranges;         // split pieces are sibling ranges (1) or single siblings (0)
   int n_problems;
   int lcap, pcap, qcap, qmax, reserve;
+  int qmax_one;       // cap of one problem's share (a lone search floods its list past it)
   long long seg_cap;
   int ramp;           // first-wave visit cap, doubled every wave up to seg_cap (0: off)
   int max_waves;
@@ -2476,7 +2477,7 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
     const long long dr = runs_now - S.runs_prev;
     const int est = (int)min((long long)kp.reserve, max(1LL, (etot + dr - 1) / max(1LL, dr)));
     const int headroom = kp.lcap - kp.reserve - nlen;
-    const int qmax = max(1, min(max(32, kp.qmax / act), headroom / est));
+    const int qmax = max(1, min(min(max(32, kp.qmax / act), kp.qmax_one), headroom / est));
     const long long bl = P.budget < 0 ? -1 : P.budget - S.V;
     if (kp.par_push && P.top_k <= 1 && nagg > 0) {
       // the tiles of the list are pushed by every CTA after the commits (S4)
@@ -3738,7 +3739,9 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     const int nwarps = grid * WARPS_PER_BLOCK;
     // total run slots per wave, shared by the active problems (most segments are
     // small: several per warp keep the warps busy through the time slice)
-    const int qmax = (getenv("HPK_QMUL") ? atoi(getenv("HPK_QMUL")) : 2) * nwarps;
+    // (4 per warp and a 300 us slice: measured best on cfg4 / cfg3 after the
+    // parallel queue step; HPK_QMUL / HPK_WAVE_US override)
+    const int qmax = (getenv("HPK_QMUL") ? atoi(getenv("HPK_QMUL")) : 4) * nwarps;
     const int qcap = qmax + 33 * P + 64;
     if (int rc = grow(c.items, c.cap_items, (size_t)2 * qcap)) return rc;
 
@@ -3777,14 +3780,15 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     kp.minq = getenv("HPK_MINQ") ? atoll(getenv("HPK_MINQ")) : 0;
     kp.runners = getenv("HPK_RUNNERS") ? atoi(getenv("HPK_RUNNERS")) : WARPS_PER_BLOCK;
     kp.ranges = ranges;
-    // run-phase time slice: 200 us (HPK_WAVE_US overrides; 0 = none)
-    kp.wave_ns = (unsigned long long)((getenv("HPK_WAVE_US") ? atof(getenv("HPK_WAVE_US")) : 200.0) * 1000.0);
+    // run-phase time slice: 300 us (HPK_WAVE_US overrides; 0 = none)
+    kp.wave_ns = (unsigned long long)((getenv("HPK_WAVE_US") ? atof(getenv("HPK_WAVE_US")) : 300.0) * 1000.0);
     kp.n_problems = P;
     kp.lcap = lcap;
     kp.pcap = pcap;
     kp.reserve = reserve;
     kp.qcap = qcap;
     kp.qmax = qmax;
+    kp.qmax_one = (getenv("HPK_QONE") ? atoi(getenv("HPK_QONE")) : 2) * nwarps;
     kp.seg_cap = seg_cap;
     kp.ramp = getenv("HPK_RAMP") ? atoi(getenv("HPK_RAMP")) : 0;
     kp.max_waves = cfg.max_waves > 0 ? cfg.max_waves : 1000000;  // watchdog
