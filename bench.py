@@ -209,9 +209,10 @@ def run_b200(args):
         raise SystemExit("no CUDA device")
     w = workload(args.workload)
     probs = tp_problems(w)
-    # shard the TP-dimension problems over ranks (round-robin, budgeted dims first)
-    from paper_2512_20953_b200.shard import shard_indices, sharded_map
-    mine = [probs[i][1] for i in shard_indices(len(probs), rank, world)]
+    # shard the TP-dimension problems over ranks (longest-first by estimated cost)
+    from paper_2512_20953_b200.shard import search_cost, shard_indices, sharded_map
+    costs = [search_cost(pb) for _, pb in probs]  # longest search on its own GPU first
+    mine = [probs[i][1] for i in shard_indices(len(probs), rank, world, costs)]
 
     def barrier():
         if dist is not None:
@@ -237,7 +238,7 @@ def run_b200(args):
     # every rank ends with the full, problem-ordered result list (one all-gather)
     full = sharded_map([pb for _, pb in probs],
                        lambda b: [(r.visited, r.optimal, r.objective, r.rgs)
-                                  for r in eng.grouping_search(b, device=local)], dist)
+                                  for r in eng.grouping_search(b, device=local)], dist, costs)
     assert len(full) == len(probs)
     ms_local = statistics.mean(dev_ms) if dev_ms else 0.0
     ms_max = ms_local

@@ -3788,7 +3788,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     kp.reserve = reserve;
     kp.qcap = qcap;
     kp.qmax = qmax;
-    kp.qmax_one = (getenv("HPK_QONE") ? atoi(getenv("HPK_QONE")) : 2) * nwarps;
+    kp.qmax_one = (int)((getenv("HPK_QONE") ? atof(getenv("HPK_QONE")) : 1.7) * nwarps);
     kp.seg_cap = seg_cap;
     kp.ramp = getenv("HPK_RAMP") ? atoi(getenv("HPK_RAMP")) : 0;
     kp.max_waves = cfg.max_waves > 0 ? cfg.max_waves : 1000000;  // watchdog

@@ -64,3 +64,16 @@ def test_two_rank_gloo_matches_serial():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert res[0] == res[1] == serial
+
+
+def test_longest_first_sharding_isolates_the_slowest_search():
+    # cfg4's TP dims: tp1 (64 units), tp2 (32), tp4 (16) budgeted, tp8 (8) exhaustive
+    from types import SimpleNamespace
+    from paper_2512_20953_b200.shard import search_cost
+    probs = [SimpleNamespace(n=n, exact_threshold=8) for n in (64, 32, 16, 8)]
+    costs = [search_cost(p) for p in probs]
+    assert [shard_indices(4, r, 2, costs) for r in range(2)] == [[0], [1, 2, 3]]
+    assert [shard_indices(4, r, 4, costs) for r in range(4)] == [[0], [1], [2], [3]]
+    parts = [shard_indices(4, r, 3, costs) for r in range(3)]
+    assert sorted(i for p in parts for i in p) == [0, 1, 2, 3]
+    assert merge_shards([["a"], ["b", "c", "d"]], 4, costs) == ["a", "b", "c", "d"]
