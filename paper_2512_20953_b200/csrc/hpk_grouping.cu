@@ -3790,7 +3790,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     kp.qmax = qmax;
     kp.qmax_one = (int)((getenv("HPK_QONE") ? atof(getenv("HPK_QONE")) : 1.7) * nwarps);
     kp.seg_cap = seg_cap;
-    kp.ramp = getenv("HPK_RAMP") ? atoi(getenv("HPK_RAMP")) : 0;
+    kp.ramp = getenv("HPK_RAMP") ? atoi(getenv("HPK_RAMP")) : 64;  // measured: -0.7 ms cfg4, -1.3 ms tp1 alone
     kp.max_waves = cfg.max_waves > 0 ? cfg.max_waves : 1000000;  // watchdog
     kp.deadline_ns = (unsigned long long)(cfg.max_seconds > 0 ? cfg.max_seconds : 120.0) * 1000000000ull;
     kp.deadline_slot = reinterpret_cast<unsigned long long*>(c.active + 2);
