@@ -258,6 +258,7 @@ struct WarpSmem {
   double robj[KW];
   int rG[KW];
   int nT, rn;  // (the candidates' RGS rows live in the run's CandRec, global)
+  int staged;  // problem whose tables tp..tRM hold (-1: none)
 };
 
 // ---- TOPK helpers (grouping.cpp:110-132)
@@ -326,16 +327,22 @@ struct PView {
   double min_mem, mb_abs, md_abs;
 };
 
-__device__ __forceinline__ PView stage_problem(const GProb& G, WarpSmem* sm, int lane) {
+// (the tables are constant after init: a warp re-stages only when its next
+// run item belongs to another problem)
+__device__ __forceinline__ PView stage_problem(const GProb& G, WarpSmem* sm, int lane, int pid) {
   const int n = G.n;
-  for (int i = lane; i < n; i += 32) {
-    sm->tp[i] = G.p[i];
-    sm->tm[i] = G.m[i];
-  }
-  for (int i = lane; i <= n + 1; i += 32) sm->tf[i] = G.f[i];
-  for (int i = lane; i <= n; i += 32) {
-    sm->tR[i] = G.R[i];
-    sm->tRM[i] = G.RM[i];
+  if (sm->staged != pid) {
+    for (int i = lane; i < n; i += 32) {
+      sm->tp[i] = G.p[i];
+      sm->tm[i] = G.m[i];
+    }
+    for (int i = lane; i <= n + 1; i += 32) sm->tf[i] = G.f[i];
+    for (int i = lane; i <= n; i += 32) {
+      sm->tR[i] = G.R[i];
+      sm->tRM[i] = G.RM[i];
+    }
+    __syncwarp();
+    if (lane == 0) sm->staged = pid;
   }
   __syncwarp();
   PView v;
@@ -2757,6 +2764,7 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
   WarpSmem* wsm = reinterpret_cast<WarpSmem*>(smem_raw);
   void* smem_tmp = smem_raw + sizeof(WarpSmem) * WARPS_PER_BLOCK;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) wsm[warp].staged = -1;
 
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long now;
@@ -2803,7 +2811,7 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
       Entry* E = pool_ptr(kp, p, S.pool_cur) + item.id;
       const double C = item.cut;
       const int cver = 1;
-      const PView PV = stage_problem(P, wsm + warp, lane);
+      const PView PV = stage_problem(P, wsm + warp, lane, p);
       // (a PREFIX re-run must end at its end marker: it is never split)
       const bool stoppable = !E->capped && !E->uncapped && E->kind != KIND_PREFIX;
       const int tk = P.top_k;
