@@ -3194,7 +3194,8 @@ __global__ void hpk_serial_kernel(SerialProb* probs, int n_probs, SerialCand* ca
 constexpr int ENUM_MAXN = 12;  // Bell(12) = 4,213,597 leaves
 
 struct EnumProb {
-  int n, K;
+  int n, K, top_k, out0;  // out0: this problem's first output slot
+  double floor_;  // the best seed's objective (the DFS's prune floor)
   double min_mem;
   double p[ENUM_MAXN], m[ENUM_MAXN];
   long long total;  // Bell(n)
@@ -3218,9 +3219,14 @@ __device__ __forceinline__ bool enum_better(double ao, int ag, long long ar, dou
   return ar < br;
 }
 
+// top_k = k > 1: the DFS's list is the global top k by key whenever at least k
+// feasible leaves reach the floor (every such leaf's ancestors then pass the
+// cutoff, which never exceeds the global k-th objective); each block reports
+// its k best and its count of leaves at or above the floor, and the host falls
+// back to the wave engine when the count is short.
 __global__ void __launch_bounds__(256) hpk_enum_kernel(const EnumProb* probs, int n_probs,
                                                        const EnumTable* tab, EnumBest* out,
-                                                       int per_block) {
+                                                       int* nabove, int per_block) {
   // block -> (problem, chunk of ranks)
   int pi = 0;
   while (pi + 1 < n_probs && probs[pi + 1].block0 <= (int)blockIdx.x) ++pi;
@@ -3228,9 +3234,12 @@ __global__ void __launch_bounds__(256) hpk_enum_kernel(const EnumProb* probs, in
   const int n = P.n;
   const long long lo = (long long)(blockIdx.x - P.block0) * per_block;
   const long long hi = min(P.total, lo + per_block);
-  double bo = -1.0;
-  int bg = 0;
-  long long br = 0x7fffffffffffffffLL;
+  const int tk = P.top_k;
+  // this thread's k best, best first
+  double lo_[KW];
+  int lg_[KW];
+  long long lr_[KW];
+  int ln = 0, above = 0;
   for (long long rk = lo + threadIdx.x; rk < hi; rk += blockDim.x) {
     // unrank (lexicographic RGS): digit 0 is 0; each later digit is an
     // existing group (D[r][g] completions each) or the new group g
@@ -3279,44 +3288,77 @@ __global__ void __launch_bounds__(256) hpk_enum_kernel(const EnumProb* probs, in
     }
     if (!ok) continue;
     const double obj = (double)g * z;
-    if (bo < 0 || enum_better(obj, g, rk, bo, bg, br)) {
-      bo = obj;
-      bg = g;
-      br = rk;
+    above += obj >= P.floor_ ? 1 : 0;
+    if (ln < tk || enum_better(obj, g, rk, lo_[ln - 1], lg_[ln - 1], lr_[ln - 1])) {
+      int pos = ln < tk ? ln : tk - 1;
+      while (pos > 0 && enum_better(obj, g, rk, lo_[pos - 1], lg_[pos - 1], lr_[pos - 1])) {
+        lo_[pos] = lo_[pos - 1];
+        lg_[pos] = lg_[pos - 1];
+        lr_[pos] = lr_[pos - 1];
+        --pos;
+      }
+      lo_[pos] = obj;
+      lg_[pos] = g;
+      lr_[pos] = rk;
+      ln = ln < tk ? ln + 1 : tk;
     }
   }
-  // block reduction of the key
+  // the block's k best: k rounds of a block argmax over the threads' heads
   __shared__ double so[8];
   __shared__ int sg[8];
   __shared__ long long sr[8];
+  __shared__ int sa[8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int head = 0;
+  for (int round = 0; round < tk; ++round) {
+    double bo = head < ln ? lo_[head] : -1.0;
+    int bg = head < ln ? lg_[head] : 0;
+    long long br = head < ln ? lr_[head] : 0x7fffffffffffffffLL;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double oo = __shfl_xor_sync(HPK_FULL_MASK, bo, o);
-    const int og = __shfl_xor_sync(HPK_FULL_MASK, bg, o);
-    const long long orr = __shfl_xor_sync(HPK_FULL_MASK, br, o);
-    if (oo >= 0 && (bo < 0 || enum_better(oo, og, orr, bo, bg, br))) {
-      bo = oo;
-      bg = og;
-      br = orr;
+    for (int o = 16; o > 0; o >>= 1) {
+      const double oo = __shfl_xor_sync(HPK_FULL_MASK, bo, o);
+      const int og = __shfl_xor_sync(HPK_FULL_MASK, bg, o);
+      const long long orr = __shfl_xor_sync(HPK_FULL_MASK, br, o);
+      if (oo >= 0 && (bo < 0 || enum_better(oo, og, orr, bo, bg, br))) {
+        bo = oo;
+        bg = og;
+        br = orr;
+      }
     }
-  }
-  if (lane == 0) {
-    so[warp] = bo;
-    sg[warp] = bg;
-    sr[warp] = br;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
+    if (lane == 0) {
+      so[warp] = bo;
+      sg[warp] = bg;
+      sr[warp] = br;
+    }
+    __syncthreads();
+    bo = so[0];
+    bg = sg[0];
+    br = sr[0];
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
       if (so[w] >= 0 && (bo < 0 || enum_better(so[w], sg[w], sr[w], bo, bg, br))) {
         bo = so[w];
         bg = sg[w];
         br = sr[w];
       }
-    out[blockIdx.x].obj = bo;
-    out[blockIdx.x].G = bg;
-    out[blockIdx.x].rank = br;
+    // every thread now holds the block winner (ranks are unique): its owner pops it
+    if (head < ln && lr_[head] == br && bo >= 0) ++head;
+    if (threadIdx.x == 0) {
+      EnumBest& e = out[(size_t)P.out0 + (size_t)(blockIdx.x - P.block0) * tk + round];
+      e.obj = bo;
+      e.G = bg;
+      e.rank = br;
+    }
+    __syncthreads();
+  }
+  // leaves at or above the floor
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) above += __shfl_xor_sync(HPK_FULL_MASK, above, o);
+  if (lane == 0) sa[warp] = above;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sa[w];
+    nabove[blockIdx.x] = t;
   }
 }
 
@@ -3474,6 +3516,58 @@ double leaf_z(const hpk_grouping_problem& pr, const uint8_t* rgs, int G) {
   return z;
 }
 
+// The prune floor of solve_grouping_topk (grouping.cpp:299-312): the best of
+// the four seed partitions (one group, singletons, by type, by node; first
+// occurrence numbering), evaluated with fresh sums in unit order (:227-247),
+// strict '>' so the first seed wins ties; -1 if none is feasible.
+double seed_floor(const hpk_grouping_problem& pr) {
+  const int n = pr.n;
+  double best = -1;
+  for (int k = 0; k < 4; ++k) {
+    std::vector<int> rgs(n);
+    std::vector<int> seen;
+    for (int i = 0; i < n; ++i) {
+      if (k == 0) {
+        rgs[i] = 0;
+      } else if (k == 1) {
+        rgs[i] = i;
+      } else {
+        const int key = k == 2 ? pr.type_key[i] : pr.node_key[i];
+        int ix = -1;
+        for (size_t j = 0; j < seen.size(); ++j)
+          if (seen[j] == key) ix = (int)j;
+        if (ix < 0) {
+          ix = (int)seen.size();
+          seen.push_back(key);
+        }
+        rgs[i] = ix;
+      }
+    }
+    const int m = *std::max_element(rgs.begin(), rgs.end()) + 1;
+    std::vector<double> pw(m, 0), me(m, 0);
+    std::vector<int> cnt(m, 0);
+    for (int i = 0; i < n; ++i) {
+      pw[rgs[i]] += pr.power[i];
+      me[rgs[i]] += pr.memory[i];
+      cnt[rgs[i]] += 1;
+    }
+    double z = 0, obj = -1;
+    bool ok = true;
+    for (int gi = 0; gi < m && ok; ++gi) {
+      if (cnt[gi] == 0 || me[gi] < pr.min_mem) {
+        ok = false;
+        break;
+      }
+      const double rho = (double)(cnt[gi] - 1) / (double)(pr.n_microbatches + cnt[gi] - 1);
+      const double gv = pw[gi] * (1.0 - rho);
+      z = gi == 0 ? gv : (gv < z ? gv : z);
+    }
+    if (ok) obj = (double)m * z;
+    if (obj > best) best = obj;
+  }
+  return best;
+}
+
 }  // namespace
 
 // Hooks shared with hpk_partition.cu (same thread-local error / timing).
@@ -3585,11 +3679,11 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
                           exact_sums(pr.memory, pr.n, 0, false);
     const bool wave_ok = !cfg.force_serial && pr.n <= MAXN && pr.top_k <= KW && contract;
     const bool enum_ok = wave_ok && cfg.enumerate && pr.n <= pr.exact_threshold &&
-                         pr.n <= ENUM_MAXN && pr.top_k <= 1;
+                         pr.n <= ENUM_MAXN;
     (enum_ok ? enum_ix : wave_ok ? wave_ix : serial_ix).push_back(i);
   }
 
-  // ---------------- enumeration engine (exhaustive, top_k = 1, planner path)
+  // ---------------- enumeration engine (exhaustive searches, planner path)
   if (!enum_ix.empty()) {
     EnumTable tab;
     std::memset(&tab, 0, sizeof(tab));
@@ -3599,13 +3693,15 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     const int per_block = 512;  // spread even the 8-unit cases over several SMs
     const int E = (int)enum_ix.size();
     std::vector<EnumProb> ep(E);
-    int nblocks = 0;
+    int nblocks = 0, nout = 0;
     for (int k = 0; k < E; ++k) {
       const hpk_grouping_problem& pr = problems[enum_ix[k]];
       EnumProb& e = ep[k];
       std::memset(&e, 0, sizeof(e));
       e.n = pr.n;
       e.K = pr.n_microbatches;
+      e.top_k = std::max(1, pr.top_k);
+      e.floor_ = seed_floor(pr);
       e.min_mem = pr.min_mem;
       for (int i = 0; i < pr.n; ++i) {
         e.p[i] = pr.power[i];
@@ -3614,72 +3710,93 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
       e.total = tab.D[pr.n - 1][1];  // Bell(n): digit 0 is fixed
       e.block0 = nblocks;
       e.nblocks = (int)((e.total + per_block - 1) / per_block);
+      e.out0 = nout;
       nblocks += e.nblocks;
+      nout += e.nblocks * e.top_k;
     }
     HpkArena& ar = c.arena;
     ar.reset();
     const size_t o_p = ar.take(sizeof(EnumProb) * E);
     const size_t o_t = ar.take(sizeof(EnumTable));
     const size_t in_end = ar.used;
-    const size_t o_b = ar.take(sizeof(EnumBest) * nblocks);
+    const size_t o_b = ar.take(sizeof(EnumBest) * nout);
+    const size_t o_a = ar.take(sizeof(int) * nblocks);
+    const size_t out_end = ar.used;
     HPK_CUDA(ar.fit());
     std::memcpy(ar.h + o_p, ep.data(), sizeof(EnumProb) * E);
     std::memcpy(ar.h + o_t, &tab, sizeof(EnumTable));
     HPK_CUDA(cudaMemcpyAsync(ar.d, ar.h, in_end, cudaMemcpyHostToDevice, c.stream));
     HPK_CUDA(cudaEventRecord(c.ev0, c.stream));
     hpk_enum_kernel<<<nblocks, 256, 0, c.stream>>>(ar.dp<EnumProb>(o_p), E, ar.dp<EnumTable>(o_t),
-                                                   ar.dp<EnumBest>(o_b), per_block);
+                                                   ar.dp<EnumBest>(o_b), ar.dp<int>(o_a),
+                                                   per_block);
     HPK_CUDA(cudaGetLastError());
     HPK_CUDA(cudaEventRecord(c.ev1, c.stream));
-    HPK_CUDA(cudaMemcpyAsync(ar.h + o_b, ar.d + o_b, sizeof(EnumBest) * nblocks,
-                             cudaMemcpyDeviceToHost, c.stream));
+    HPK_CUDA(cudaMemcpyAsync(ar.h + o_b, ar.d + o_b, out_end - o_b, cudaMemcpyDeviceToHost,
+                             c.stream));
     HPK_CUDA(cudaStreamSynchronize(c.stream));
     float ms = 0;
     HPK_CUDA(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
     t_timing.search_ms += ms;
     t_timing.kernel_launches += 1;
     t_timing.h2d_bytes += (long long)in_end;
-    t_timing.d2h_bytes += (long long)(sizeof(EnumBest) * nblocks);
+    t_timing.d2h_bytes += (long long)(out_end - o_b);
     const EnumBest* eb = ar.hp<EnumBest>(o_b);
+    const int* na = ar.hp<int>(o_a);
+    auto key_less = [](const EnumBest& x, const EnumBest& y) {  // x ranks before y
+      if (x.obj != y.obj) return x.obj > y.obj;
+      if (x.G != y.G) return x.G < y.G;
+      return x.rank < y.rank;
+    };
     for (int k = 0; k < E; ++k) {
       const int i = enum_ix[k];
       const hpk_grouping_problem& pr = problems[i];
       hpk_grouping_result& r = results[i];
-      EnumBest b{-1.0, 0, 0x7fffffffffffffffLL};
+      const int tk = ep[k].top_k;
+      std::vector<EnumBest> all;
+      long long above = 0;
       for (int q = 0; q < ep[k].nblocks; ++q) {
-        const EnumBest& x = eb[ep[k].block0 + q];
-        if (x.obj >= 0 && (b.obj < 0 || x.obj > b.obj || (x.obj == b.obj && (x.G < b.G ||
-                                                        (x.G == b.G && x.rank < b.rank))))) {
-          b = x;
+        above += na[ep[k].block0 + q];
+        for (int t = 0; t < tk; ++t) {
+          const EnumBest& x = eb[(size_t)ep[k].out0 + (size_t)q * tk + t];
+          if (x.obj >= 0) all.push_back(x);
         }
       }
+      if (tk > 1 && above < tk) {  // the DFS's list depends on its pruning: wave engine
+        wave_ix.push_back(i);
+        continue;
+      }
+      std::sort(all.begin(), all.end(), key_less);
       r.engine = 2;
       r.visited = -1;  // not counted by this engine
-      if (b.obj < 0) {  // no feasible leaf: no seed is feasible either (seeds are leaves)
+      if (all.empty()) {  // no feasible leaf: no seed is feasible either (seeds are leaves)
         r.status = 3;
         continue;
       }
-      uint8_t rgs[ENUM_MAXN];
-      rgs[0] = 0;
-      int g = 1;
-      long long kk = b.rank;
-      for (int u = 1; u < pr.n; ++u) {
-        const long long w = tab.D[pr.n - 1 - u][g];
-        const long long q = kk / w;
-        if (q < g) {
-          rgs[u] = (uint8_t)q;
-          kk -= q * w;
-        } else {
-          rgs[u] = (uint8_t)g;
-          kk -= (long long)g * w;
-          ++g;
-        }
-      }
-      r.count = 1;
+      const int cnt = std::min<int>(tk, (int)all.size());
+      r.count = cnt;
       r.optimal = 1;
-      r.objective[0] = b.obj;
-      r.z[0] = leaf_z(pr, rgs, b.G);
-      for (int u = 0; u < pr.n; ++u) r.rgs[u] = rgs[u];
+      for (int t = 0; t < cnt; ++t) {
+        uint8_t rgs[ENUM_MAXN];
+        rgs[0] = 0;
+        int g = 1;
+        long long kk = all[t].rank;
+        for (int u = 1; u < pr.n; ++u) {
+          const long long w = tab.D[pr.n - 1 - u][g];
+          const long long q = kk / w;
+          if (q < g) {
+            rgs[u] = (uint8_t)q;
+            kk -= q * w;
+          } else {
+            rgs[u] = (uint8_t)g;
+            kk -= (long long)g * w;
+            ++g;
+          }
+        }
+        r.objective[t] = all[t].obj;
+        r.z[t] = leaf_z(pr, rgs, all[t].G);
+        for (int u = 0; u < pr.n; ++u) r.rgs[(size_t)t * pr.n + u] = rgs[u];
+      }
     }
   }
 

@@ -206,3 +206,24 @@ def test_enumeration_engine_matches_the_dfs_winner(engine, oracle):
             continue
         assert (r.status, r.rgs, r.objective, r.z, r.optimal) == \
             (0, o.rgs, o.objective, o.z, o.optimal), pb
+
+
+def test_enumeration_engine_top_k(engine, oracle):
+    """Exhaustive top-k on the enumeration engine: the global top k when at least
+    k feasible leaves reach the prune floor, else the wave engine takes over —
+    either way the list equals the reference DFS's."""
+    probs = [GroupingProblem(pb.power, pb.memory, pb.n_microbatches, pb.min_mem, pb.type_key,
+                             pb.node_key, 12, pb.node_budget, pb.top_k)
+             for pb in _random_problems(78, 300, nmax=12, top_ks=(2, 3, 5, 8))]
+    res = engine.grouping_search(probs, enumeration=True, max_seconds=60)
+    engines = set()
+    for pb, r in zip(probs, res):
+        o = oracle.solve_grouping(pb.power, pb.memory, pb.n_microbatches, pb.min_mem,
+                                  pb.type_key, pb.node_key, 12, pb.node_budget, pb.top_k)
+        engines.add(r.engine)
+        if o.status != 0:
+            assert r.status == o.status
+            continue
+        assert (r.status, r.count, r.rgs, r.objective, r.z, r.optimal) == \
+            (0, o.count, o.rgs, o.objective, o.z, o.optimal), pb
+    assert 2 in engines
