@@ -314,7 +314,8 @@ def run_b200(args):
                 "traffic_unit": "bytes/launch (ncu dram__bytes_read+write, profiles/r1_traffic.json)",
                 "ops_per_launch": model_ops, "int32_peak_gops": i32.value / 1e9,
                 "peak_source": "measured (hpk_measure_issue_peaks: DMUL+DADD chains, this GPU)",
-                "note": "fp64-op model of SURVEY.md 8(d) (reference ops), whole plan search"}
+                "note": "fp64-op model of SURVEY.md 8(d) (reference ops), whole plan search",
+                "issue": _issue_roofline("cfg4")}
 
     cpu = cpu_baseline(w)
     cpu_line = None
@@ -487,6 +488,27 @@ def run_b200_cfg5(args):
     k = min(4, len(svis))
     ct = [_ref_plan_one(i) for i in range(k)]
     cpu_value = sum(svis[:k]) / sum(ct)
+    # roofline: fp64-op model ops per visit from the oracle on the sampled
+    # snapshots, scaled to the sweep's visits; measured peak
+    import ctypes as C
+    f64, i32 = C.c_double(), C.c_double()
+    eng.lib.hpk_measure_issue_peaks.argtypes = [C.c_int, C.POINTER(C.c_double),
+                                                C.POINTER(C.c_double)]
+    eng.lib.hpk_measure_issue_peaks(local, C.byref(f64), C.byref(i32))
+    sv = so = 0.0
+    for w in configs.cfg5_snapshots(k):
+        v, o = visits_of(w)
+        sv += v
+        so += o
+    ops = total_visits * (so / sv) if sv else 0.0
+    achieved = ops / (dev_max * 1e-3) / 1e9 if dev_max > 0 else 0.0
+    roofline = {"bound": "fp64-issue", "achieved": achieved, "peak": f64.value / 1e9,
+                "unit": "GFLOP/s", "frac": achieved * 1e9 / f64.value if f64.value else None,
+                "traffic": None, "ops_per_launch": ops,
+                "peak_source": "measured (hpk_measure_issue_peaks: DMUL+DADD chains, this GPU)",
+                "note": f"fp64-op model of SURVEY.md 8(d), ops per visit sampled on snapshots "
+                        f"0..{k - 1} ({so / sv if sv else 0:.2f})",
+                "issue": _issue_roofline("cfg5")}
     line = {
         "metric": METRIC, "value": total_visits / (dev_max * 1e-3), "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": e2e_max,
@@ -503,6 +525,7 @@ def run_b200_cfg5(args):
         "cpu_baseline": {"value": cpu_value, "unit": UNIT, "cores": 1, "kind": "reference",
                          "sample": f"snapshots 0..{k - 1}, hp_plan_compute on 1 host core",
                          "host_cores": os.cpu_count()},
+        "roofline": roofline,
         "clocks": cs.summary(),
         "gpu_launches": launches,
     }
@@ -510,6 +533,19 @@ def run_b200_cfg5(args):
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _issue_roofline(workload):
+    """The instruction-issue roofline of the search kernel (the bound that applies
+    to this control-heavy tree search): ncu's issue-slot utilization of the same
+    workload, from the committed capture (profiles/r1_issue.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_issue.json")) as f:
+            rec = json.load(f)["hpk_wave_kernel"][workload]
+        return {"bound": "instruction-issue", "frac": rec["issue_active_pct"] / 100.0,
+                "fp64_pipe_frac": rec["fp64_pipe_pct"] / 100.0, "source": rec["source"]}
+    except Exception:
+        return None
 
 
 def _cpu_model():
