@@ -53,6 +53,22 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
+// 64-bit unsigned warp min / max with two 32-bit redux.sync (high word, then
+// the low word among the lanes holding the extreme high word). Used on the bit
+// patterns of non-negative doubles, which order like the values.
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+  const unsigned hi = (unsigned)(v >> 32);
+  const unsigned mh = __reduce_min_sync(HPK_FULL_MASK, hi);
+  const unsigned ml = __reduce_min_sync(HPK_FULL_MASK, hi == mh ? (unsigned)v : 0xffffffffu);
+  return ((unsigned long long)mh << 32) | ml;
+}
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+  const unsigned hi = (unsigned)(v >> 32);
+  const unsigned mh = __reduce_max_sync(HPK_FULL_MASK, hi);
+  const unsigned ml = __reduce_max_sync(HPK_FULL_MASK, hi == mh ? (unsigned)v : 0u);
+  return ((unsigned long long)mh << 32) | ml;
+}
+
 // Candidate ranking of P/src/grouping.cpp:112-115 (higher objective, then fewer
 // groups); `ia < ib` breaks remaining ties toward the earlier enumeration.
 __device__ __forceinline__ bool key_better(double ao, int ag, int ia, double bo, int bg, int ib) {

@@ -715,24 +715,19 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
           }
           const int n_inf = __popc(__ballot_sync(HPK_FULL_MASK, inf_k[0])) +
                             __popc(__ballot_sync(HPK_FULL_MASK, inf_k[1]));
-          // min1 / idx1 / min2 over existing groups
-          const bool s0 = eff_k[0] <= eff_k[1];
-          double m1 = s0 ? eff_k[0] : eff_k[1];
-          double m2 = s0 ? eff_k[1] : eff_k[0];
-          int i1 = s0 ? lane : lane + 32;
-          // reductions only span the lanes that own groups/children: width W =
-          // next power of two >= G+1 (the full warp once slot 1 is in use)
-          const int W = G + 1 > 32 ? 32 : (G + 1 <= 1 ? 1 : 1 << (32 - __clz(G)));
-          for (int off = W >> 1; off > 0; off >>= 1) {
-            const double om1 = __shfl_xor_sync(HPK_FULL_MASK, m1, off);
-            const int oi1 = __shfl_xor_sync(HPK_FULL_MASK, i1, off);
-            const double om2 = __shfl_xor_sync(HPK_FULL_MASK, m2, off);
-            const bool take = om1 < m1 || (om1 == m1 && oi1 < i1);
-            const double lo2 = take ? m1 : om1;
-            m2 = lo2 < (take ? om2 : m2) ? lo2 : (take ? om2 : m2);
-            m1 = take ? om1 : m1;
-            i1 = take ? oi1 : i1;
-          }
+          // min1 / idx1 / min2 over existing groups. Effective powers are
+          // non-negative doubles (empty slots: +inf), whose bit patterns order
+          // like the values: two 32-bit redux.sync per 64-bit min, exact.
+          const unsigned long long eb0 = (unsigned long long)__double_as_longlong(eff_k[0]);
+          const unsigned long long eb1 = (unsigned long long)__double_as_longlong(eff_k[1]);
+          const unsigned long long m1b = warp_min_u64(eb0 < eb1 ? eb0 : eb1);
+          const double m1 = __longlong_as_double((long long)m1b);
+          const unsigned bz0 = __ballot_sync(HPK_FULL_MASK, eb0 == m1b);
+          const unsigned bz1 = __ballot_sync(HPK_FULL_MASK, eb1 == m1b);
+          const int i1 = bz0 ? __ffs(bz0) - 1 : 31 + __ffs(bz1);  // lowest index attaining it
+          const unsigned long long x0 = lane == i1 ? ~0ull : eb0;
+          const unsigned long long x1 = lane + 32 == i1 ? ~0ull : eb1;
+          const double m2 = __longlong_as_double((long long)warp_min_u64(x0 < x1 ? x0 : x1));
           // each lane evaluates the children it owns (c = lane, lane+32)
           double obj_s[2];
           int gc_s[2];
@@ -752,12 +747,15 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
           }
           o.visits += count;
           if (TOPK) {
-            double mx = obj_s[0] > obj_s[1] ? obj_s[0] : obj_s[1];
-            for (int off = W >> 1; off > 0; off >>= 1) {
-              const double om = __shfl_xor_sync(HPK_FULL_MASK, mx, off);
-              mx = om > mx ? om : mx;
+            // max objective of the batch (objectives >= 0; none feasible: -1)
+            const bool anyf = __any_sync(HPK_FULL_MASK, fe_s[0] || fe_s[1]);
+            double mx = -1.0;
+            if (anyf) {
+              const double lm = obj_s[0] > obj_s[1] ? obj_s[0] : obj_s[1];
+              const unsigned long long lb =
+                  lm >= 0 ? (unsigned long long)__double_as_longlong(lm) : 0ull;
+              mx = __longlong_as_double((long long)warp_max_u64(lb));
             }
-            if (W < 32) mx = shfl(mx, 0);
             if (mx >= 0) {
               o.m = mx > o.m ? mx : o.m;
               if (mx > cut) {  // the cutoff state takes every leaf above the cutoff
@@ -798,40 +796,30 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
               }
             }
           } else {
+          // the batch's best leaf by the reference ranking (objective desc,
+          // #groups asc, enumeration = child order asc): the lane's better child,
+          // then a 64-bit max of the objective bits and a min of (G, child)
+          // among the lanes attaining it; mx (max objective) is its objective
           double best_o = -1.0;
           int best_Gc = 0, best_c = 1 << 30;
-          double mx = -1.0;
-#pragma unroll
-          for (int k = 0; k < 2; ++k) {
-            const int ch = lane + 32 * k;
-            if (fe_s[k]) {
-              const double obj = obj_s[k];
-              const int Gc = gc_s[k];
-              mx = obj > mx ? obj : mx;
-              if (best_o < 0 || key_better(obj, Gc, ch, best_o, best_Gc, best_c)) {
-                best_o = obj;
-                best_Gc = Gc;
-                best_c = ch;
-              }
+          {
+            const bool t0 = fe_s[0] && (!fe_s[1] || key_better(obj_s[0], gc_s[0], lane, obj_s[1],
+                                                               gc_s[1], lane + 32));
+            const bool has = fe_s[0] || fe_s[1];
+            const double lo_ = t0 ? obj_s[0] : obj_s[1];
+            const int lg = t0 ? gc_s[0] : gc_s[1];
+            const int lc = t0 ? lane : lane + 32;
+            if (__any_sync(HPK_FULL_MASK, has)) {
+              const unsigned long long lb = has ? (unsigned long long)__double_as_longlong(lo_) : 0ull;
+              const unsigned long long bb = warp_max_u64(lb);
+              const unsigned key = (has && lb == bb) ? (unsigned)(lg << 7 | lc) : 0xffffffffu;
+              const unsigned kmin = __reduce_min_sync(HPK_FULL_MASK, key);
+              best_o = __longlong_as_double((long long)bb);
+              best_Gc = (int)(kmin >> 7);
+              best_c = (int)(kmin & 127);
             }
           }
-          for (int off = W >> 1; off > 0; off >>= 1) {
-            const double oo = __shfl_xor_sync(HPK_FULL_MASK, best_o, off);
-            const int og = __shfl_xor_sync(HPK_FULL_MASK, best_Gc, off);
-            const int oc = __shfl_xor_sync(HPK_FULL_MASK, best_c, off);
-            const double om = __shfl_xor_sync(HPK_FULL_MASK, mx, off);
-            const bool take = oo >= 0 && (best_o < 0 || key_better(oo, og, oc, best_o, best_Gc, best_c));
-            best_o = take ? oo : best_o;
-            best_Gc = take ? og : best_Gc;
-            best_c = take ? oc : best_c;
-            mx = om > mx ? om : mx;
-          }
-          if (W < 32) {  // make the block-[0,W) result warp-uniform
-            best_o = shfl(best_o, 0);
-            best_Gc = shfl(best_Gc, 0);
-            best_c = shfl(best_c, 0);
-            mx = shfl(mx, 0);
-          }
+          const double mx = best_o;
           if (best_o >= 0) {
             if (!o.has_best || best_o > o.best_obj ||
                 (best_o == o.best_obj && best_Gc < o.best_G)) {
