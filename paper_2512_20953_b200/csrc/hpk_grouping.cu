@@ -692,7 +692,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
         const int lim = d == dtop && hil < G ? hil : G;  // last child of this node in the segment
         int count = lim + 1 - c0;
         bool end_hit = false;
-        if (prefix && match == d) {  // dend == n here
+        if (match == d) {  // dend == n here
           if (ec - c0 < count) {
             count = ec - c0 > 0 ? ec - c0 : 0;
             end_hit = true;
@@ -872,11 +872,11 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
         remove_unit(P, g, lane, grp, up, um);
         sums_ok = false;
         if (match > d) match = d;
-        if (prefix && match == d) ec = sm->endp[d];
+        if (match == d) ec = sm->endp[d];
         HPK_PC(6, 1);
         continue;
       }
-      if (prefix && match == d) {
+      if (match == d) {
         if (c > ec || (c == ec && d + 1 == dend)) {
           o.finished = true;
           break;
@@ -932,7 +932,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
         const int lim = d == dtop && hil < G ? hil : G;
         if (k > lim + 1 - c) k = lim + 1 - c;
         if ((long long)k > cap - o.visits) k = (int)(cap - o.visits);
-        if (prefix && match == d) {
+        if (match == d) {
           // the end node (d+1 == dend) is not visited; the end path's child is,
           // and its prune is the ancestor prune a* (grouping.cpp:162,169)
           const int kl = (d + 1 == dend) ? ec - c : ec - c + 1;
@@ -954,7 +954,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
         const bool pass = exact_passes(P, g, Gc, d + 1, cut);
         remove_unit(P, g, lane, c, up, um);
         if (!pass) {
-          if (prefix && match == d && c == ec && o.a_star < 0) o.a_star = d + 1;
+          if (match == d && c == ec && o.a_star < 0) o.a_star = d + 1;
           ++c;
           continue;
         }
@@ -987,7 +987,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
       }
       add_unit(P, g, lane, c, up, um);
       if (c == G) ++G;
-      if (prefix && match == d && c == ec) match = d + 1;
+      if (match == d && c == ec) match = d + 1;
       ++d;
       Sd = Sn;
       Dd = Dn;
@@ -996,7 +996,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
       sums_ok = false;
       up = P.p[d];
       um = P.m[d];
-      if (prefix && match == d) ec = sm->endp[d];
+      if (match == d) ec = sm->endp[d];
       HPK_PC(5, 1);
     }
   }
