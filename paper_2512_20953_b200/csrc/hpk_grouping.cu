@@ -110,6 +110,7 @@ struct GState {
   // parallel push (schedule step S4): published by the problem's commit CTA,
   // valid when pp_wave == the current wave
   int pp_wave, pp_mode, pp_head, pp_len, pp_ashift, pp_qmax, pp_ntile;
+  int n_units;  // the problem's TP units (its weight in the run-queue share)
   long long pp_bl;
   double pp_C;
   int nT, nbest;
@@ -190,6 +191,7 @@ struct KParams {
   int n_problems;
   int lcap, pcap, qcap, qmax, reserve;
   int qmax_one;       // cap of one problem's share (a lone search floods its list past it)
+  int unit_share;     // 1: a problem's share of run slots is proportional to its units
   long long seg_cap;
   int ramp;           // first-wave visit cap, doubled every wave up to seg_cap (0: off)
   int max_waves;
@@ -1203,6 +1205,7 @@ __device__ __forceinline__ bool same_state(const CandRec& r, const GState& S) {
 __device__ void finish_problem(const KParams& kp, GState& S) {
   S.done = 1;
   atomicSub(kp.active, 1);
+  atomicSub(kp.active + 62, S.n_units);  // units of the active problems (queue weights)
 }
 
 // Queue the first qmax positions (list order) whose run is missing or used a
@@ -2465,6 +2468,7 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
     // schedule phase (the live count drops as problems finish mid-phase; using it
     // let late schedulers over-push past qcap, starving problems)
     const int act = max(1, *((volatile int*)kp.active + 6));
+    const int act_units = max(1, *((volatile int*)kp.active + 63));
     // ... throttled by the list's headroom: each queued run may split, adding
     // about as many pieces as this wave's runs did on average; a full list
     // would revert splits (wasted runs) every wave
@@ -2472,7 +2476,12 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
     const long long dr = runs_now - S.runs_prev;
     const int est = (int)min((long long)kp.reserve, max(1LL, (etot + dr - 1) / max(1LL, dr)));
     const int headroom = kp.lcap - kp.reserve - nlen;
-    const int qmax = max(1, min(min(max(32, kp.qmax / act), kp.qmax_one), headroom / est));
+    // the share: by the problem's units when kp.unit_share (deeper searches need
+    // more runs per wave to move their commit front), else equal
+    const int fair = kp.unit_share
+                         ? (int)((long long)kp.qmax * S.n_units / act_units)
+                         : kp.qmax / act;
+    const int qmax = max(1, min(min(max(32, fair), kp.qmax_one), headroom / est));
     const long long bl = P.budget < 0 ? -1 : P.budget - S.V;
     if (kp.par_push && P.top_k <= 1 && nagg > 0) {
       // the tiles of the list are pushed by every CTA after the commits (S4)
@@ -2643,6 +2652,7 @@ __device__ void init_problem(const KParams& kp, int p) {
     S.nbest = 0;
     S.pp_wave = -1;
     S.pp_mode = 0;
+    S.n_units = n;
     for (int t = 0; t < KW; ++t) S.T[t] = -1.0;
     S.V = 0;
     S.has_best = 0;
@@ -2671,6 +2681,7 @@ __device__ void init_problem(const KParams& kp, int p) {
       S.len = 0;
       S.done = 1;
       atomicSub(kp.active, 1);
+      atomicSub(kp.active + 62, n);
     } else {
       Entry& e = pool_ptr(kp, p, 0)[0];
       e.u[0] = 0;  // root has no groups: its only child is [0]
@@ -2772,6 +2783,7 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
       kp.queues[cur ^ 1].len = 0;
       kp.queues[cur ^ 1].head = 0;
       kp.active[6] = *((volatile int*)kp.active);  // active-count snapshot for the schedule
+      kp.active[63] = *((volatile int*)kp.active + 62);  // ... and of their units
     }
     RunQueue* q = kp.queues + cur;
     RunItem* items = kp.items + (size_t)cur * kp.qcap;
@@ -3863,6 +3875,12 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     HPK_CUDA(cudaMemsetAsync(c.queues, 0, sizeof(RunQueue) * 2, c.stream));
     int init_flags[64] = {0};  // [0] active [1] err [2:4) deadline [4:6) barrier
     init_flags[0] = P;         // [6] active snapshot [7] stop [8:60) trace counters
+    {
+      int units = 0;  // [62] units of the active problems, [63] its snapshot
+      for (int k = 0; k < P; ++k) units += problems[wave_ix[k]].n;
+      init_flags[62] = units;
+      init_flags[63] = units;
+    }
                                // [60:62) expansion work counts
     HPK_CUDA(cudaMemcpyAsync(c.active, init_flags, sizeof(int) * 64, cudaMemcpyHostToDevice,
                              c.stream));
@@ -3902,6 +3920,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     kp.qcap = qcap;
     kp.qmax = qmax;
     kp.qmax_one = (int)((getenv("HPK_QONE") ? atof(getenv("HPK_QONE")) : 1.7) * nwarps);
+    kp.unit_share = getenv("HPK_UNIT_SHARE") ? atoi(getenv("HPK_UNIT_SHARE")) : 0;
     kp.seg_cap = seg_cap;
     kp.ramp = getenv("HPK_RAMP") ? atoi(getenv("HPK_RAMP")) : 64;  // measured: -0.7 ms cfg4, -1.3 ms tp1 alone
     kp.max_waves = cfg.max_waves > 0 ? cfg.max_waves : 1000000;  // watchdog
