@@ -113,7 +113,16 @@ class HetplanLib:
         L.hp_profile_write_file.restype = C.c_int
         L.hp_plan_write_file.argtypes = [_VP, C.c_char_p]
         L.hp_plan_write_file.restype = C.c_int
-        for name in ("hp_cluster_free", "hp_model_free", "hp_profile_free", "hp_plan_free"):
+        # checkpoint / recovery (c_api.h:123-136): the reference's own engines
+        L.hp_checkpoint_save.argtypes = [_VP, C.c_char_p, C.c_ulonglong, C.c_int, C.c_ulonglong,
+                                         C.c_int]
+        L.hp_checkpoint_save.restype = C.c_int
+        L.hp_recovery_compute.argtypes = [_VP, _VP, C.c_char_p, _VP, C.POINTER(_VP)]
+        L.hp_recovery_compute.restype = C.c_int
+        L.hp_recovery_to_json.argtypes = [_VP, C.POINTER(C.c_void_p)]
+        L.hp_recovery_to_json.restype = C.c_int
+        for name in ("hp_cluster_free", "hp_model_free", "hp_profile_free", "hp_plan_free",
+                     "hp_recovery_free"):
             getattr(L, name).argtypes = [_VP]
             getattr(L, name).restype = None
 
@@ -238,6 +247,24 @@ class HetplanLib:
         self._check(self.lib.hp_estimate_to_json(plan.ptr, cluster.ptr, model.ptr, profile.ptr,
                                                  C.byref(p)))
         return self._take_string(p)
+
+    def checkpoint_save(self, plan: "Handle", root: str, step: int, hidden_dim: int = 8,
+                        seed: int = 2512, zero_optimizer: bool = False) -> None:
+        """hp_checkpoint_save (c_api.h:123-125): writes root/manifest.json,
+        root/bitmap.json and the per-device layer shards."""
+        self._check(self.lib.hp_checkpoint_save(plan.ptr, root.encode(), step, hidden_dim, seed,
+                                                int(zero_optimizer)))
+
+    def recovery_json(self, old_plan: "Handle", new_plan: "Handle", bitmap_path: str,
+                      cluster: "Handle") -> str:
+        """hp_recovery_compute + hp_recovery_to_json (c_api.h:127-132)."""
+        out = C.c_void_p()
+        self._check(self.lib.hp_recovery_compute(old_plan.ptr, new_plan.ptr, bitmap_path.encode(),
+                                                 cluster.ptr, C.byref(out)))
+        h = Handle(self, out, "hp_recovery_free")
+        js = C.c_void_p()
+        self._check(self.lib.hp_recovery_to_json(h.ptr, C.byref(js)))
+        return self._take_string(js)
 
     def plan_json(self, cluster_text: str, model_text: str, max_layers: int,
                   options: Optional[PlanOptions] = None, base_seconds: float = 0.05) -> str:
