@@ -58,3 +58,39 @@ def test_batch_equals_single_calls(product_lib):
                  snaps[0].max_layers, threads=1)
     for s, g in zip(snaps, got):
         assert g == _single(product_lib, s.cluster_json(), s.model_json(), s.max_layers)
+
+
+def test_full_cfg5_sweep_searches_match_golden(engine):
+    """All 1167 grouping searches of the 1000-snapshot sweep in ONE wave-kernel
+    launch (range pieces, pool compaction and the parallel queue step at full
+    load): every search's visits, optimal flag, winner objective and RGS equal
+    the pinned oracle's (tests/golden/cfg5_search.json, tools/make_cfg5_search.py)."""
+    import math
+    import os
+
+    from oracle.binding import min_mem_for, units_for
+    from paper_2512_20953_b200.engine import GroupingProblem
+    with open(os.path.join(os.path.dirname(__file__), "golden", "cfg5_search.json")) as f:
+        golden = json.load(f)
+    probs = []
+    for w in configs.cfg5_snapshots(1000):
+        g = 0
+        for nd in w.cluster["nodes"]:
+            g = math.gcd(g, nd["count"])
+        for tp in [t for t in range(1, g + 1) if g % t == 0]:
+            P, M, T, N = units_for(w.cluster, tp)
+            probs.append(GroupingProblem(P, M, w.model["n_microbatches"], min_mem_for(w.model),
+                                         T, N))
+    assert len(probs) == len(golden)
+    res = engine.grouping_search(probs, max_seconds=120)
+    bad = []
+    for g, r in zip(golden, res):
+        if r.status != g["status"]:
+            bad.append(g)
+            continue
+        if g["status"] != 0:
+            continue
+        if (r.visited, r.optimal, r.objective[0].hex(), "".join(chr(48 + x) for x in r.rgs[0])) \
+                != (g["visited"], g["optimal"], g["objective"], g["rgs"]):
+            bad.append(g)
+    assert not bad, (len(bad), bad[:3])
