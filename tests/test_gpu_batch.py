@@ -94,3 +94,39 @@ def test_full_cfg5_sweep_searches_match_golden(engine):
                 != (g["visited"], g["optimal"], g["objective"], g["rgs"]):
             bad.append(g)
     assert not bad, (len(bad), bad[:3])
+
+
+def _oracle_topk(args):
+    from oracle.binding import Oracle
+    P, M, K, MIN, T, N, k = args
+    r = Oracle().solve_grouping(P, M, K, MIN, T, N, top_k=k)
+    return (r.status, r.count, r.visited, r.optimal, [x.hex() for x in r.objective], r.rgs)
+
+
+def test_cfg5_sweep_top_k_matches_oracle(engine):
+    """top_k = 3 on 200 sweep snapshots in one launch (the top-k state at scale:
+    range pieces, compaction, sequential queue scans with improvers)."""
+    import math
+    import os
+    from multiprocessing import get_context
+
+    from oracle.binding import min_mem_for, units_for
+    from paper_2512_20953_b200.engine import GroupingProblem
+    args, probs = [], []
+    for w in configs.cfg5_snapshots(200):
+        g = 0
+        for nd in w.cluster["nodes"]:
+            g = math.gcd(g, nd["count"])
+        for tp in [t for t in range(1, g + 1) if g % t == 0]:
+            P, M, T, N = units_for(w.cluster, tp)
+            K, MIN = w.model["n_microbatches"], min_mem_for(w.model)
+            probs.append(GroupingProblem(P, M, K, MIN, T, N, top_k=3))
+            args.append((P, M, K, MIN, T, N, 3))
+    res = engine.grouping_search(probs, max_seconds=120)
+    with get_context("spawn").Pool(os.cpu_count()) as pool:
+        want = pool.map(_oracle_topk, args, chunksize=2)
+    got = [(r.status, r.count, r.visited, r.optimal, [x.hex() for x in r.objective], r.rgs)
+           if r.status == 0 else (r.status,) for r in res]
+    want = [w if w[0] == 0 else (w[0],) for w in want]
+    bad = [i for i, (a, b) in enumerate(zip(got, want)) if a != b]
+    assert not bad, (len(bad), [(got[i], want[i]) for i in bad[:2]])
