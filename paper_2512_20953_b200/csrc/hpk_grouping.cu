@@ -194,6 +194,7 @@ struct KParams {
   int unit_share;     // 1: a problem's share of run slots is proportional to its units
   long long seg_cap;
   int ramp;           // first-wave visit cap, doubled every wave up to seg_cap (0: off)
+  long long front_cap;  // visit cap of the list head's run (the time slice stops it)
   int max_waves;
   unsigned long long deadline_ns;  // %globaltimer watchdog (relative at launch)
   unsigned long long* deadline_slot;
@@ -1413,7 +1414,9 @@ __device__ void push_items(const KParams& kp, int queue, int p, const int* ids, 
             it.front = (j == 0);
             // an uncapped (list-full) run is the head's: under a budget it
             // needs at most budget_left + 1 visits to show the overflow
-            it.cap = !pool[id].uncapped ? wave_cap
+            // the list head is the commit front's critical path: only the time
+            // slice bounds its run (kp.front_cap), the others take the segment cap
+            it.cap = !pool[id].uncapped ? (j == 0 ? kp.front_cap : wave_cap)
                      : budget_left < 0  ? 0x3fffffffffffffffLL
                                         : budget_left + 1;
             it.cut = chat[k];
@@ -1650,7 +1653,7 @@ __device__ void push_tile(const KParams& kp, int p, int t, int queue, int wave, 
             it.pos = j;
             it.id = id;
             it.front = (j == head);
-            it.cap = !pool[id].uncapped ? kp.seg_cap
+            it.cap = !pool[id].uncapped ? (j == head ? kp.front_cap : kp.seg_cap)
                      : bl < 0           ? 0x3fffffffffffffffLL
                                         : bl + 1;
             it.cut = chat[k];
@@ -3922,6 +3925,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     kp.qmax_one = (int)((getenv("HPK_QONE") ? atof(getenv("HPK_QONE")) : 1.7) * nwarps);
     kp.unit_share = getenv("HPK_UNIT_SHARE") ? atoi(getenv("HPK_UNIT_SHARE")) : 0;
     kp.seg_cap = seg_cap;
+    kp.front_cap = getenv("HPK_FRONT_CAP") ? atoll(getenv("HPK_FRONT_CAP")) : seg_cap;
     kp.ramp = getenv("HPK_RAMP") ? atoi(getenv("HPK_RAMP")) : 64;  // measured: -0.7 ms cfg4, -1.3 ms tp1 alone
     kp.max_waves = cfg.max_waves > 0 ? cfg.max_waves : 1000000;  // watchdog
     kp.deadline_ns = (unsigned long long)(cfg.max_seconds > 0 ? cfg.max_seconds : 120.0) * 1000000000ull;
