@@ -188,6 +188,7 @@ struct KParams {
   unsigned long long wave_ns;  // run-phase time slice (0: none): later runs stop and split
   int runners;        // warps per CTA that run segments (experiment knob; default all)
   int ranges;         // split pieces are sibling ranges (1) or single siblings (0)
+  int eager;          // eager split of a stop subtree with >= this many units left (0: off)
   int n_problems;
   int lcap, pcap, qcap, qmax, reserve;
   int qmax_one;       // cap of one problem's share (a lone search floods its list past it)
@@ -1061,6 +1062,18 @@ __device__ int split_run(const KParams& kp, int p, GState& S, Entry* E, const Ru
     const int w = lim(lev) - (int)sm->path[lev];
     count += rng ? (w > 0 ? 1 : 0) : w;
   }
+  // Eager split (kp.eager > 0, single-sibling pieces): the stop node s starts a
+  // big subtree (>= kp.eager units left) that would be the next list head and
+  // cost one wave per level; it becomes an entry record [s, s.0) — a PREFIX
+  // that visits and checks s only — followed by one piece per child of s, run
+  // in parallel. If s turns out pruned, the entry's run reports a* = depth(s)
+  // and the commit walk deletes the children (the PREFIX deletion rule).
+  const int n = S.n_units;
+  const int gs = (int)((sm->lvl[d] >> 16) & 255);  // groups at the stop node's parent
+  const int Gs = gs + (o.stop_c == gs ? 1 : 0);     // groups at the stop node
+  const bool eager = !rng && kp.eager > 0 && d + 1 < n && n - (d + 1) >= kp.eager;
+  const int nk = eager ? 1 + (Gs + 1) : 0;          // entry + children
+  if (eager) count += nk - 1;                       // (they replace piece 0)
   int first = 0;
   if (lane == 0) {  // CAS bump allocation: a failed attempt leaves no hole, and the
     // list head alone may use the last `reserve` slots (progress guarantee)
@@ -1083,6 +1096,32 @@ __device__ int split_run(const KParams& kp, int p, GState& S, Entry* E, const Ru
   if (first < 0) return 0;
   Entry* pool = pool_ptr(kp, p, S.pool_cur);
   for (int k = lane; k < count; k += 32) {
+    Entry& qe = pool[first + k];
+    if (k < nk) {  // the eager entry record and the stop node's children
+      for (int i = 0; i < d; ++i) qe.u[i] = sm->path[i];
+      qe.u[d] = (uint8_t)o.stop_c;
+      if (k == 0) {
+        for (int i = 0; i <= d; ++i) qe.end[i] = qe.u[i];
+        qe.end[d + 1] = 0;
+        qe.du = (uint8_t)(d + 1);
+        qe.dend = (uint8_t)(d + 2);
+        qe.hi = (uint8_t)o.stop_c;
+        qe.kind = KIND_PREFIX;
+      } else {
+        qe.u[d + 1] = (uint8_t)(k - 1);
+        qe.du = (uint8_t)(d + 2);
+        qe.hi = (uint8_t)(k - 1);
+        qe.kind = KIND_FULL;
+      }
+      qe.cver = -1;
+      qe.finished = 0;
+      qe.capped = 0;
+      qe.uncapped = 0;
+      qe.has_best = 0;
+      qe.a_star = -1;
+      continue;
+    }
+    const int kk = eager ? k - nk + 1 : k;  // index in the plain enumeration
     int lev = d, child = o.stop_c, last;
     if (rng) {
       for (int idx = k; idx > 0;) {  // the k-th non-empty level below d
@@ -1094,7 +1133,7 @@ __device__ int split_run(const KParams& kp, int p, GState& S, Entry* E, const Ru
       }
       last = lim(lev);
     } else {  // the k-th sibling piece, level by level (deepest first)
-      int idx = k, base = o.stop_c - 1, cnt = lim(d) - base;
+      int idx = kk, base = o.stop_c - 1, cnt = lim(d) - base;
       while (idx >= cnt) {
         idx -= cnt;
         --lev;
@@ -3827,7 +3866,8 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     // parallel pieces near one search's commit front); HPK_RANGES overrides
     const int ranges = getenv("HPK_RANGES") ? atoi(getenv("HPK_RANGES")) : (P > 16 ? 1 : 0);
     const int reserve = ranges ? max_n + 64                          // one piece per level
-                               : max_n * (max_n + 1) / 2 + 32;  // one per sibling, worst case
+                               : max_n * (max_n + 1) / 2 + 32 + 66;  // one per sibling,
+                                                                      // + an eager split
     if (pcap < 4 * reserve) pcap = 4 * reserve;
     std::vector<GProb> hp(P);
     for (int k = 0; k < P; ++k) {
@@ -3914,6 +3954,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     kp.minq = getenv("HPK_MINQ") ? atoll(getenv("HPK_MINQ")) : 0;
     kp.runners = getenv("HPK_RUNNERS") ? atoi(getenv("HPK_RUNNERS")) : WARPS_PER_BLOCK;
     kp.ranges = ranges;
+    kp.eager = getenv("HPK_EAGER") ? atoi(getenv("HPK_EAGER")) : 0;
     // run-phase time slice: 300 us (HPK_WAVE_US overrides; 0 = none)
     kp.wave_ns = (unsigned long long)((getenv("HPK_WAVE_US") ? atof(getenv("HPK_WAVE_US")) : 300.0) * 1000.0);
     kp.n_problems = P;
