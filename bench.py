@@ -108,7 +108,7 @@ def workload(name):
 
 def tp_problems(w):
     """The grouping problems of one plan search (one per valid TP dimension)."""
-    from oracle.binding import min_mem_for, units_for  # data prep only (no compute)
+    from paper_2512_20953_b200.configs import min_mem_for, units_for  # data prep only (no compute)
     from paper_2512_20953_b200.engine import GroupingProblem
     g = 0
     for nd in w.cluster["nodes"]:

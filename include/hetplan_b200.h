@@ -139,6 +139,9 @@ void hp_recovery_free(hp_recovery* recovery);                         /* c_api.h
  * ------------------------------------------------------------------ */
 #define HPK_MAX_UNITS 64 /* wave engine; larger problems use the serial replica */
 #define HPK_MAX_TOPK 16
+#ifndef HPK_HOST_TRACE
+#define HPK_HOST_TRACE 0 /* build with -DHPK_HOST_TRACE=1 for per-phase host timings */
+#endif
 
 const char* hpk_version(void);
 const char* hpk_last_error(void); /* thread-local, valid until the next hpk_* call */

@@ -93,31 +93,3 @@ class Oracle:
                                            int(allow_zero), layers, times, C.byref(bn),
                                            C.byref(ms), C.byref(ml))
         return rc, list(layers), list(times), bn.value, ms.value, ml.value
-
-
-def units_for(cluster: dict, tp: int):
-    """build_tp_units (P/src/grouping.cpp:40-75) for a JSON cluster dict whose nodes
-    are single-type: returns (power, memory, type_key, node_key) in unit order."""
-    types = cluster["gpu_types"]
-    names = sorted(types)
-    P, M, T, N = [], [], [], []
-    for nd in sorted(cluster["nodes"], key=lambda x: x["node_id"]):
-        t = types[nd["type"]]
-        for base in range(0, nd["count"], tp):
-            p = 0.0
-            m = 0.0
-            for _ in range(tp):
-                p += float(t["compute_power"])
-                m += float(t["memory_bytes"])
-            P.append(p)
-            M.append(m)
-            T.append(names.index(nd["type"]))
-            N.append(nd["node_id"])
-    return P, M, T, N
-
-
-def min_mem_for(model: dict) -> float:
-    """MemoryModel::required_group_memory (P/src/profile.cpp:217-224)."""
-    L = model["n_layers"]
-    return (L * model["per_layer_param_bytes"] * (1.0 + model["optimizer_multiplier"])
-            + L * model["per_layer_activation_bytes"])

@@ -155,3 +155,45 @@ WORKLOADS = {"cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4}
 
 def get(name: str) -> Workload:
     return WORKLOADS[name]()
+
+
+# ---- grouping inputs of a workload (the planner builds the same through the C
+# ABI; these let bench.py and the tests drive the kernel C-ABI directly)
+
+def units_for(cluster: dict, tp: int):
+    """TP units of a JSON cluster whose nodes are single-type, as
+    build_tp_units forms them (P/src/grouping.cpp:40-75): nodes by id, blocks of
+    tp ranks, power and memory summed in rank order. Returns (power, memory,
+    type_key, node_key) in unit order."""
+    types = cluster["gpu_types"]
+    names = sorted(types)
+    P, M, T, N = [], [], [], []
+    for nd in sorted(cluster["nodes"], key=lambda x: x["node_id"]):
+        t = types[nd["type"]]
+        for _ in range(0, nd["count"], tp):
+            p = 0.0
+            m = 0.0
+            for _ in range(tp):
+                p += float(t["compute_power"])
+                m += float(t["memory_bytes"])
+            P.append(p)
+            M.append(m)
+            T.append(names.index(nd["type"]))
+            N.append(nd["node_id"])
+    return P, M, T, N
+
+
+def min_mem_for(model: dict) -> float:
+    """MIN_mem, MemoryModel::required_group_memory (P/src/profile.cpp:217-224)."""
+    L = model["n_layers"]
+    return (L * model["per_layer_param_bytes"] * (1.0 + model["optimizer_multiplier"])
+            + L * model["per_layer_activation_bytes"])
+
+
+def tp_dims_of(cluster: dict) -> list:
+    """enumerate_tp_dims (P/src/grouping.cpp:341-350): divisors of the gcd."""
+    import math
+    g = 0
+    for nd in cluster["nodes"]:
+        g = math.gcd(g, nd["count"])
+    return [t for t in range(1, g + 1) if g % t == 0] or [1]

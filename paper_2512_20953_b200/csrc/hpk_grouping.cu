@@ -39,6 +39,10 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef HPK_TRACE_LEVEL
+#define HPK_TRACE_LEVEL 0  // per-wave scheduler trace (debug builds only)
+#endif
+
 namespace hpk {
 
 constexpr int MAXN = HPK_MAX_UNITS;  // 64 units -> lanes own groups g and g+32
@@ -2810,7 +2814,7 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long now;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-    kp.deadline_ns += now;  // relative budget -> absolute
+    if (kp.deadline_ns != ~0ull) kp.deadline_ns += now;  // relative budget -> absolute
     *kp.deadline_slot = kp.deadline_ns;
   }
   if (kp.trace >= 4 && blockIdx.x == 0 && threadIdx.x == 0) kp.prof[11] = 4;  // per-decision trace
@@ -3864,7 +3868,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     // piece shape: sibling ranges for big batches (cfg5: 1.3x faster, shorter
     // lists), single siblings for a few problems (cfg3: 1.9x faster — more
     // parallel pieces near one search's commit front); HPK_RANGES overrides
-    const int ranges = getenv("HPK_RANGES") ? atoi(getenv("HPK_RANGES")) : (P > 16 ? 1 : 0);
+    const int ranges = P > 16 ? 1 : 0;
     const int reserve = ranges ? max_n + 64                          // one piece per level
                                : max_n * (max_n + 1) / 2 + 32 + 66;  // one per sibling,
                                                                       // + an eager split
@@ -3909,7 +3913,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     // small: several per warp keep the warps busy through the time slice)
     // (4 per warp and a 300 us slice: measured best on cfg4 / cfg3 after the
     // parallel queue step; HPK_QMUL / HPK_WAVE_US override)
-    const int qmax = (getenv("HPK_QMUL") ? atoi(getenv("HPK_QMUL")) : 4) * nwarps;
+    const int qmax = 4 * nwarps;
     const int qcap = qmax + 33 * P + 64;
     if (int rc = grow(c.items, c.cap_items, (size_t)2 * qcap)) return rc;
 
@@ -3942,7 +3946,7 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     kp.xtn = xtn;
     kp.agg = c.agg;
     kp.pagg = c.pagg;
-    kp.par_push = getenv("HPK_PAR_PUSH") ? atoi(getenv("HPK_PAR_PUSH")) : 1;
+    kp.par_push = 1;
     kp.work = c.work;
     kp.wcap = P * xtn;
     kp.wcount = c.active + 60;
@@ -3951,30 +3955,44 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     kp.active = c.active;
     kp.err = c.active + 1;
     kp.stop = c.active + 7;
-    kp.minq = getenv("HPK_MINQ") ? atoll(getenv("HPK_MINQ")) : 0;
-    kp.runners = getenv("HPK_RUNNERS") ? atoi(getenv("HPK_RUNNERS")) : WARPS_PER_BLOCK;
+    kp.minq = 0;
+    kp.runners = WARPS_PER_BLOCK;
     kp.ranges = ranges;
-    kp.eager = getenv("HPK_EAGER") ? atoi(getenv("HPK_EAGER")) : 0;
+    kp.eager = 0;
     // run-phase time slice: 300 us (HPK_WAVE_US overrides; 0 = none)
-    kp.wave_ns = (unsigned long long)((getenv("HPK_WAVE_US") ? atof(getenv("HPK_WAVE_US")) : 300.0) * 1000.0);
+    kp.wave_ns = 300000ull;
     kp.n_problems = P;
     kp.lcap = lcap;
     kp.pcap = pcap;
     kp.reserve = reserve;
     kp.qcap = qcap;
     kp.qmax = qmax;
-    kp.qmax_one = (int)((getenv("HPK_QONE") ? atof(getenv("HPK_QONE")) : 1.7) * nwarps);
-    kp.unit_share = getenv("HPK_UNIT_SHARE") ? atoi(getenv("HPK_UNIT_SHARE")) : 0;
+    kp.qmax_one = (int)(1.7 * nwarps);
+    kp.unit_share = 0;
     kp.seg_cap = seg_cap;
-    kp.front_cap = getenv("HPK_FRONT_CAP") ? atoll(getenv("HPK_FRONT_CAP")) : seg_cap;
-    kp.ramp = getenv("HPK_RAMP") ? atoi(getenv("HPK_RAMP")) : 64;  // measured: -0.7 ms cfg4, -1.3 ms tp1 alone
-    kp.max_waves = cfg.max_waves > 0 ? cfg.max_waves : 1000000;  // watchdog
-    kp.deadline_ns = (unsigned long long)(cfg.max_seconds > 0 ? cfg.max_seconds : 120.0) * 1000000000ull;
+    kp.front_cap = seg_cap;
+    kp.ramp = 64;  // measured: -0.7 ms cfg4, -1.3 ms tp1 alone
+    kp.max_waves = cfg.max_waves > 0 ? cfg.max_waves : 0x7fffffff;  // explicit watchdog only
+    // watchdog: an explicit max_seconds, else derived from the budgets (a
+    // visit rate 100x below the slowest measured, plus 60 s); searches with no
+    // budget (exhaustive mode) have no deadline, like the reference
+    double secs = cfg.max_seconds;
+    if (secs <= 0) {
+      long long tot = 0;
+      bool unbounded = false;
+      for (int k = 0; k < P; ++k) {
+        const hpk_grouping_problem& pr = problems[wave_ix[k]];
+        if (pr.n <= pr.exact_threshold || pr.node_budget < 0) unbounded = pr.n > 12 || unbounded;
+        else tot += pr.node_budget;
+      }
+      secs = unbounded ? 0.0 : 60.0 + (double)tot / 1e6;
+    }
+    kp.deadline_ns = secs > 0 ? (unsigned long long)(secs * 1e9) : ~0ull;
     kp.deadline_slot = reinterpret_cast<unsigned long long*>(c.active + 2);
     kp.bar = reinterpret_cast<unsigned int*>(c.active + 4);
     kp.prof = reinterpret_cast<unsigned long long*>(c.active + 8);
-    kp.trace = getenv("HPK_TRACE") ? atoi(getenv("HPK_TRACE")) : 0;
-    kp.trace_p = getenv("HPK_TRACE_P") ? atoi(getenv("HPK_TRACE_P")) : -1;
+    kp.trace = HPK_TRACE_LEVEL;  // build-time: -DHPK_TRACE_LEVEL=n
+    kp.trace_p = -1;
     const size_t smem = sizeof(WarpSmem) * WARPS_PER_BLOCK + sizeof(SchedSmem);
     void* args[] = {&kp};
     HPK_CUDA(cudaEventRecord(c.ev0, c.stream));

@@ -228,7 +228,7 @@ extern "C" int hpk_stage_affinity(hpk_affinity_problem* probs, int n, int device
   if (max_smem > 48 * 1024)
     HPKS_CUDA(cudaFuncSetAttribute(affinity_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)max_smem));
-  const bool trace = getenv("HPK_HOST_TRACE") != nullptr;
+  constexpr bool trace = HPK_HOST_TRACE != 0;  // build-time: -DHPK_HOST_TRACE=1
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (trace) {
     cudaEventCreate(&e0);

@@ -12,9 +12,10 @@
 //     is one CTA of ONE batched hpk_stage_affinity launch;
 //   * every candidate's layer partition + Eq. (1) cost is one CTA of ONE
 //     batched hpk_partition_cost launch (partition.cpp:51-110, cost.cpp:29-147).
-// Host work left here: option handling, TP-unit formation (build_tp_units,
-// reference code), the stage mapper's joint / fallback placement (restated,
-// stage_map.cpp:63-186) and plan assembly/validation. There is no CPU
+// Host work left here, all restated (no reference function is called for any
+// SURVEY 8 row): option handling, TP dimensions and TP-unit formation (R1-R2),
+// MIN_mem (R3), the stage mapper's joint / fallback placement
+// (stage_map.cpp:63-186), plan assembly and validation (R17). There is no CPU
 // fallback: without a CUDA device plan_cluster throws InternalError.
 #include <algorithm>
 #include <atomic>
@@ -27,7 +28,9 @@
 #include <cmath>
 #include <iostream>
 #include <map>
+#include <numeric>
 #include <optional>
+#include <set>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -45,23 +48,155 @@ namespace hetplan {
 
 namespace {
 
-// planner.cpp:34-50 — devices in spec order with (derived) powers.
-std::vector<GroupingDevice> grouping_devices(const ClusterSpec& spec,
-                                             const std::map<std::string, double>* powers) {
-  std::vector<GroupingDevice> out;
-  for (const auto& d : spec.all_devices()) {
-    const GpuType& t = spec.type_of(d);
-    double g = t.compute_power;
-    if (powers) {
-      auto it = powers->find(t.name);
-      if (it == powers->end()) {
-        throw InvalidArgumentError("derived powers missing GPU type " + t.name);
+// ---- R1-R3 and plan validation, restated (no reference code runs for them).
+
+// R1, enumerate_tp_dims (grouping.cpp:341-350): the divisors of the gcd of the
+// nodes' GPU counts, ascending; [1] when there is no node.
+std::vector<int> valid_tp_dims(const ClusterSpec& spec) {
+  int g = 0;
+  for (const auto& nd : spec.nodes) g = std::gcd(g, nd.gpu_count);
+  std::vector<int> dims;
+  for (int t = 1; t <= g; ++t)
+    if (g % t == 0) dims.push_back(t);
+  if (dims.empty()) dims.push_back(1);
+  return dims;
+}
+
+// derive_power (profile.cpp:234-262): T_ref / T_type at the largest layer
+// count profiled for every type at tp_dim.
+std::map<std::string, double> derived_powers(const ProfileTable& table, const std::string& ref,
+                                             int tp_dim) {
+  const std::vector<std::string> types = table.gpu_types();
+  if (std::find(types.begin(), types.end(), ref) == types.end()) {
+    throw InvalidArgumentError("derive_power: reference type '" + ref +
+                               "' not in profile table");
+  }
+  std::vector<int> common = table.layer_counts(types.front(), tp_dim);
+  for (const auto& t : types) {
+    const std::vector<int> counts = table.layer_counts(t, tp_dim);
+    std::vector<int> keep;
+    for (int c : common)
+      if (std::binary_search(counts.begin(), counts.end(), c)) keep.push_back(c);
+    common.swap(keep);
+  }
+  if (common.empty()) {
+    throw InvalidArgumentError("derive_power: no layer count profiled for every type at tp=" +
+                               std::to_string(tp_dim));
+  }
+  const int anchor = common.back();
+  const double t_ref = table.at(ref, tp_dim, anchor);
+  std::map<std::string, double> out;
+  for (const auto& t : types) out[t] = t_ref / table.at(t, tp_dim, anchor);
+  return out;
+}
+
+// One device as the grouping sees it (GroupingDevice, grouping.hpp:38-43).
+struct Dev {
+  DeviceId id;
+  const std::string* type;
+  double power, memory;
+};
+
+// grouping_devices (planner.cpp:34-50): every device in spec order with its
+// type's power (or the derived one) and memory.
+std::vector<Dev> device_list(const ClusterSpec& spec,
+                             const std::map<std::string, double>* powers) {
+  std::vector<Dev> out;
+  for (const auto& nd : spec.nodes) {
+    for (int r = 0; r < nd.gpu_count; ++r) {
+      const DeviceId d{nd.node_id, r};
+      const GpuType& t = spec.type_of(d);  // first node with this id (cluster.cpp:57-62)
+      double g = t.compute_power;
+      if (powers) {
+        auto it = powers->find(t.name);
+        if (it == powers->end()) {
+          throw InvalidArgumentError("derived powers missing GPU type " + t.name);
+        }
+        g = it->second;
       }
-      g = it->second;
+      out.push_back({d, &t.name, g, t.memory});
     }
-    out.push_back({d, t.name, g, t.memory});
   }
   return out;
+}
+
+// R2, build_tp_units (grouping.cpp:40-75): devices ordered by (node, rank);
+// each node's run is cut into consecutive blocks of tp_dim same-type devices;
+// power and memory summed in rank order from 0.
+std::vector<TpUnit> tp_units(std::vector<Dev> devs, int tp_dim) {
+  if (tp_dim < 1) throw InvalidArgumentError("tp_dim must be >= 1");
+  std::sort(devs.begin(), devs.end(), [](const Dev& a, const Dev& b) { return a.id < b.id; });
+  std::vector<TpUnit> units;
+  for (size_t i = 0; i < devs.size();) {
+    size_t j = i;
+    while (j < devs.size() && devs[j].id.node_id == devs[i].id.node_id) ++j;
+    if ((j - i) % (size_t)tp_dim != 0) {
+      throw InfeasibleError("tp_dim " + std::to_string(tp_dim) +
+                            " does not divide the GPU count of node " +
+                            std::to_string(devs[i].id.node_id) + " (divisibility)");
+    }
+    for (size_t b = i; b < j; b += (size_t)tp_dim) {
+      TpUnit u;
+      u.node_id = devs[b].id.node_id;
+      u.gpu_type = *devs[b].type;
+      for (size_t k = b; k < b + (size_t)tp_dim; ++k) {
+        if (*devs[k].type != u.gpu_type) {
+          throw InfeasibleError("mixed GPU types on node " + std::to_string(u.node_id) +
+                                "; TP units must be same-type");
+        }
+        u.devices.push_back(devs[k].id);
+        u.power += devs[k].power;
+        u.memory += devs[k].memory;
+      }
+      units.push_back(std::move(u));
+    }
+    i = j;
+  }
+  return units;
+}
+
+// R3, MemoryModel::required_group_memory (profile.cpp:217-224): MIN_mem is
+// tp-independent, L·ppb·(1+om) + L·pab, unless the model overrides it.
+double group_memory_floor(const MemoryModel& mm, const ModelConfig& cfg) {
+  if (mm.min_mem_override > 0) return mm.min_mem_override;
+  return cfg.n_layers * mm.per_layer_param_bytes * (1.0 + mm.optimizer_multiplier) +
+         cfg.n_layers * mm.per_layer_activation_bytes;
+}
+
+// ParallelPlan::validate (plan.cpp:30-51): the same invariants in the same
+// order, raising InternalError with the reference's text.
+void check_plan(const ParallelPlan& plan) {
+  auto need = [](bool ok, const char* what, const char* expr) {
+    if (!ok) {
+      throw InternalError(std::string("invariant violated: ") + what + " [" + expr + "]");
+    }
+  };
+  need(plan.tp_dim >= 1, "tp_dim >= 1", "tp_dim >= 1");
+  need(!plan.groups.empty(), "plan has at least one group", "!groups.empty()");
+  std::set<DeviceId> seen;
+  for (const auto& group : plan.groups) {
+    need(!group.stages.empty(), "group has at least one stage", "!group.stages.empty()");
+    int expected = 1;
+    int cursor = 0;
+    for (const auto& st : group.stages) {
+      need(st.stage_index == expected++, "stage indices contiguous from 1",
+           "st.stage_index == expected_index++");
+      need((int)st.devices.size() == plan.tp_dim, "stage holds tp_dim devices",
+           "static_cast<int>(st.devices.size()) == tp_dim");
+      need(st.layer_begin == cursor, "layer ranges tile [0, n_layers)",
+           "st.layer_begin == cursor");
+      need(st.layer_end >= st.layer_begin, "layer range is not inverted",
+           "st.layer_end >= st.layer_begin");
+      cursor = st.layer_end;
+      for (const auto& d : st.devices) {
+        need(d.node_id == st.devices.front().node_id, "TP unit is co-located",
+             "d.node_id == st.devices.front().node_id");
+        need(seen.insert(d).second, "device appears exactly once in the plan",
+             "seen.insert(d).second");
+      }
+    }
+    need(cursor == plan.n_layers, "every group covers all layers", "cursor == n_layers");
+  }
 }
 
 // split_microbatches (plan.cpp:53-62): earlier groups take the remainder.
@@ -334,7 +469,7 @@ void job_prepare(PlanJob& J) {
   auto& nk = J.nk;
   // planner.cpp:119-126
   tp_dims = options.tp_dims;
-  valid = enumerate_tp_dims(spec);
+  valid = valid_tp_dims(spec);
   if (tp_dims.empty()) {
     tp_dims = valid;
   } else {
@@ -345,7 +480,7 @@ void job_prepare(PlanJob& J) {
   if (options.derive_power) {
     std::string ref = options.power_reference;
     if (ref.empty()) ref = spec.gpu_types.begin()->first;
-    derived = derive_power(profile, ref, 1);
+    derived = derived_powers(profile, ref, 1);
   }
   for (const auto& [name, t] : spec.gpu_types) {
     (void)t;
@@ -366,18 +501,18 @@ void job_prepare(PlanJob& J) {
       tw.decided = true;
       continue;
     }
-    std::vector<GroupingDevice> devices;
+    std::vector<Dev> devices;
     tw.pre = capture([&] {
-      devices = grouping_devices(spec, derived ? &*derived : nullptr);
+      devices = device_list(spec, derived ? &*derived : nullptr);
       tw.min_mem = options.min_mem_override > 0 ? options.min_mem_override
-                                                : memmodel.required_group_memory(cfg, tp);
+                                                : group_memory_floor(memmodel, cfg);
       double total_dev = 0;
       for (const auto& d : devices) total_dev += d.memory;
       const double big_l = std::max(total_dev, tw.min_mem) * 2 + 1;
       if (cfg.n_microbatches < 1) {
         throw InvalidArgumentError("grouping: n_microbatches must be >= 1");
       }
-      tw.units = build_tp_units(devices, tp);
+      tw.units = tp_units(devices, tp);
       if (tw.units.empty()) throw InvalidArgumentError("grouping: no devices");
       double total_mem = 0;
       for (const auto& u : tw.units) total_mem += u.memory;
@@ -673,7 +808,7 @@ ParallelPlan job_select(PlanJob& J) {
       }
       plan.cost.t_sync = r.t_sync;
       plan.cost.t_star = r.t_star;
-      plan.validate();
+      check_plan(plan);
       summary.grouping_objective = c.grouping->objective;
       summary.t_star = plan.cost.t_star;
       summary.status = "candidate";
@@ -742,7 +877,7 @@ void for_jobs(std::vector<PlanJob*>& jobs, int threads, Fn&& fn) {
 // partition/cost launch. A GPU failure fails every job that needed the GPU.
 // HPK_HOST_TRACE=1: per-phase wall times of plan_jobs on stderr (diagnostics).
 struct PhaseClock {
-  bool on = getenv("HPK_HOST_TRACE") != nullptr;
+  static constexpr bool on = HPK_HOST_TRACE != 0;  // build-time: -DHPK_HOST_TRACE=1
   std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
   std::ostringstream os;
   void lap(const char* name) {
@@ -755,6 +890,13 @@ struct PhaseClock {
     if (on) std::cerr << "[hpk-host] " << os.str() << "\n";
   }
 };
+
+// A failed GPU launch ends the call: every job not finished yet (including
+// jobs with no work in that launch) reports the launch's error.
+void fail_unfinished(std::vector<PlanJob*>& jobs, const std::exception_ptr& e) {
+  for (PlanJob* J : jobs)
+    if (!J->error && !J->plan) J->error = e;
+}
 
 void plan_jobs(std::vector<PlanJob*>& jobs, int threads) {
   hpk_reset_timing();
@@ -788,7 +930,7 @@ void plan_jobs(std::vector<PlanJob*>& jobs, int threads) {
                                          &scfg);
       if (rc != 0) gpu_fail(rc);
     } catch (...) {
-      for (auto& o : owner) o.first->error = std::current_exception();
+      fail_unfinished(jobs, std::current_exception());
       return;
     }
     for (size_t i = 0; i < problems.size(); ++i) owner[i].first->gres[owner[i].second] = gres[i];
@@ -821,7 +963,7 @@ void plan_jobs(std::vector<PlanJob*>& jobs, int threads) {
         const int rc = hpk_stage_affinity(ap.data(), (int)ap.size(), -1);
         if (rc != 0) gpu_fail(rc);
       } catch (...) {
-        for (PlanJob* J : aowner) J->error = std::current_exception();
+        fail_unfinished(jobs, std::current_exception());
         return;
       }
     }
@@ -846,7 +988,7 @@ void plan_jobs(std::vector<PlanJob*>& jobs, int threads) {
       const int rc = hpk_partition_cost(pin.data(), (int)pin.size(), pres.data(), -1);
       if (rc != 0) gpu_fail(rc);
     } catch (...) {
-      for (auto& o : powner) o.first->error = std::current_exception();
+      fail_unfinished(jobs, std::current_exception());
       return;
     }
     for (size_t i = 0; i < pin.size(); ++i) powner[i].first->pres[powner[i].second] = pres[i];
@@ -865,6 +1007,7 @@ ParallelPlan plan_cluster(const ClusterSpec& spec, const ModelConfig& cfg,
   std::vector<PlanJob*> jobs{&job};
   plan_jobs(jobs, 1);
   if (job.error) std::rethrow_exception(job.error);
+  if (!job.plan) throw InternalError("hetplan_b200: planning ended without a plan");
   return std::move(*job.plan);
 }
 
@@ -950,6 +1093,9 @@ extern "C" hp_status hp_plan_compute_batch(int n, const hp_cluster* const* clust
       std::string msg;
       if (jobs[i]->error) {
         out_status[i] = status_of(jobs[i]->error, &msg);
+      } else if (!jobs[i]->plan) {
+        out_status[i] = HP_INTERNAL_ERROR;
+        msg = "hetplan_b200: planning ended without a plan";
       } else {
         out_status[i] = HP_OK;
         out_plans[i] = new hp_plan{std::move(*jobs[i]->plan)};

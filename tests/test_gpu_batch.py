@@ -68,7 +68,7 @@ def test_full_cfg5_sweep_searches_match_golden(engine):
     import math
     import os
 
-    from oracle.binding import min_mem_for, units_for
+    from paper_2512_20953_b200.configs import min_mem_for, units_for
     from paper_2512_20953_b200.engine import GroupingProblem
     with open(os.path.join(os.path.dirname(__file__), "golden", "cfg5_search.json")) as f:
         golden = json.load(f)
@@ -110,7 +110,7 @@ def test_cfg5_sweep_top_k_matches_oracle(engine):
     import os
     from multiprocessing import get_context
 
-    from oracle.binding import min_mem_for, units_for
+    from paper_2512_20953_b200.configs import min_mem_for, units_for
     from paper_2512_20953_b200.engine import GroupingProblem
     args, probs = [], []
     for w in configs.cfg5_snapshots(200):

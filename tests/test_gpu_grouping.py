@@ -6,7 +6,7 @@ import random
 
 import pytest
 
-from oracle.binding import min_mem_for, units_for
+from paper_2512_20953_b200.configs import min_mem_for, units_for
 from paper_2512_20953_b200 import configs
 from paper_2512_20953_b200.engine import GroupingProblem
 

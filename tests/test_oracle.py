@@ -7,7 +7,8 @@ import random
 
 import pytest
 
-from oracle.binding import PROBE_LIB, min_mem_for, units_for
+from oracle.binding import PROBE_LIB
+from paper_2512_20953_b200.configs import min_mem_for, units_for
 from paper_2512_20953_b200 import cases, configs
 
 

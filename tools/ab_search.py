@@ -1,9 +1,10 @@
 """A/B the grouping-search kernel of two library builds on one config.
 usage: python tools/ab_search.py CFG LIB_A LIB_B [reps]"""
 import math
+import os
 import sys
-sys.path.insert(0, "/root/repo")
-from oracle.binding import min_mem_for, units_for  # noqa: E402
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2512_20953_b200.configs import min_mem_for, units_for  # noqa: E402
 from paper_2512_20953_b200 import configs  # noqa: E402
 from paper_2512_20953_b200.engine import Engine, GroupingProblem  # noqa: E402
 w = configs.get(sys.argv[1])

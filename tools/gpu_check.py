@@ -8,7 +8,8 @@ import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-from oracle.binding import REF_LIB, Oracle, min_mem_for, units_for  # noqa: E402
+from oracle.binding import REF_LIB, Oracle
+from paper_2512_20953_b200.configs import min_mem_for, units_for  # noqa: E402
 from paper_2512_20953_b200 import configs  # noqa: E402
 from paper_2512_20953_b200.capi import HetplanLib  # noqa: E402
 from paper_2512_20953_b200.engine import Engine, GroupingProblem  # noqa: E402

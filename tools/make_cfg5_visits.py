@@ -14,7 +14,8 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-from oracle.binding import Oracle, min_mem_for, units_for  # noqa: E402
+from oracle.binding import Oracle
+from paper_2512_20953_b200.configs import min_mem_for, units_for  # noqa: E402
 from paper_2512_20953_b200 import configs  # noqa: E402
 
 

@@ -3,10 +3,11 @@ product library vs the reference library; checks the JSON is identical.
 
 usage: python tools/opt_probe.py [cfg ...]
 """
+import os
 import sys
 import time
 
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from oracle.binding import REF_LIB  # noqa: E402
 from paper_2512_20953_b200 import configs  # noqa: E402
 from paper_2512_20953_b200.capi import HetplanLib, PlanOptions  # noqa: E402

@@ -1,6 +1,7 @@
 """One cfg4 plan through the product C ABI (profiling target)."""
+import os
 import sys
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2512_20953_b200 import configs
 from paper_2512_20953_b200.capi import HetplanLib
 from paper_2512_20953_b200.engine import LIB_PATH

@@ -1,8 +1,9 @@
 """cfg5 snapshot grouping searches in one wave-kernel launch (profiling target)."""
 import math
+import os
 import sys
-sys.path.insert(0, "/root/repo")
-from oracle.binding import min_mem_for, units_for
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2512_20953_b200.configs import min_mem_for, units_for
 from paper_2512_20953_b200 import configs
 from paper_2512_20953_b200.engine import Engine, GroupingProblem
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 100

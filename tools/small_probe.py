@@ -1,7 +1,8 @@
 """Kernel and plan latency of the small configs (cfg1, accept clusters)."""
+import os
 import sys
 import time
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2512_20953_b200 import configs  # noqa: E402
 from paper_2512_20953_b200.capi import HetplanLib  # noqa: E402
 from paper_2512_20953_b200.engine import LIB_PATH, Engine  # noqa: E402
