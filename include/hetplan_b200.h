@@ -236,6 +236,14 @@ typedef struct hpk_plan_result {
 int hpk_partition_cost(const hpk_plan_candidate* cands, int n_cands, hpk_plan_result* results,
                        int device);
 
+/* Same, with test hooks that force the kernel's slow branches on any input:
+ * the DP's best tables in global memory instead of shared memory, and the
+ * per-layer-count memory check instead of the feasible-prefix fast path. */
+#define HPK_PART_GMEM_TABLES 1
+#define HPK_PART_PER_L_MEMORY 2
+int hpk_partition_cost_ex(const hpk_plan_candidate* cands, int n_cands,
+                          hpk_plan_result* results, int device, int flags);
+
 /* The DP-affinity pass of the stage mapper (map_nodes_and_stages,
  * P/src/stage_map.cpp:188-214) for one candidate plan: slots in stage order
  * per group after the joint / fallback placement (:94-186), each holding the
@@ -254,6 +262,18 @@ typedef struct hpk_affinity_problem {
 
 /* All problems in one launch (one CTA each). */
 int hpk_stage_affinity(hpk_affinity_problem* problems, int n_problems, int device);
+
+/* The planner's whole stage mapping (map_nodes_and_stages,
+ * P/src/stage_map.cpp:63-216) for n_groupings groupings of one cluster's TP
+ * units at tp, exactly as hp_plan_compute runs it: the joint / fallback
+ * placement on the host, then ONE hpk_stage_affinity launch for all of them.
+ * Units are the planner's own (R2) at the GPU types' powers; grouping g puts
+ * unit u in group rgs[g*U + u]. Writes the unit index of every stage slot
+ * (groups in order, stages in order) to out_unit[g*U + s]. Returns U (> 0), or
+ * -(hp_status) on an error (text in hpk_last_error()). Used by the parity tests
+ * against the reference mapper. */
+int hpk_map_stages(const hp_cluster* cluster, int tp, int n_groupings, const int* rgs,
+                   int* out_unit);
 
 /* Device-side timing of this thread's last hpk_grouping_search /
  * hpk_partition_cost calls (CUDA events on the launching stream). */

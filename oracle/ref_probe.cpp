@@ -9,9 +9,11 @@
 #include <string>
 #include <vector>
 
+#include "hetplan/cluster.hpp"
 #include "hetplan/grouping.hpp"
 #include "hetplan/partition.hpp"
 #include "hetplan/profile.hpp"
+#include "hetplan/stage_map.hpp"
 
 using namespace hetplan;
 
@@ -115,6 +117,55 @@ int ref_balance_workload(int n_layers, int P, int n_bits, const double* prof,
     return 6;
   } catch (...) {
     return 5;
+  }
+}
+
+// map_nodes_and_stages (P/src/stage_map.cpp:63-216) of n_groupings groupings of
+// one cluster's TP units: units = build_tp_units over the spec's devices at
+// their type powers (planner.cpp:34-50, grouping.cpp:40-75), grouping g puts
+// unit u in group rgs[g*U + u]. Writes, per grouping, the unit index held by
+// each stage slot (groups in order, stages in order) into out_unit[g*U + s].
+// Returns the unit count U (> 0), or -3 / -6 / -5 on Infeasible /
+// InvalidArgument / other errors.
+int ref_map_stages(const char* cluster_json, int tp, int n_groupings, const int* rgs,
+                   int* out_unit) {
+  try {
+    const ClusterSpec spec = load_cluster_spec(cluster_json);
+    std::vector<GroupingDevice> devs;
+    for (const auto& d : spec.all_devices()) {
+      const GpuType& t = spec.type_of(d);
+      devs.push_back({d, t.name, t.compute_power, t.memory});
+    }
+    const std::vector<TpUnit> units = build_tp_units(devs, tp);
+    const int U = static_cast<int>(units.size());
+    for (int g = 0; g < n_groupings; ++g) {
+      GroupingSolution sol;
+      const int* r = rgs + static_cast<size_t>(g) * U;
+      int m = 0;
+      for (int u = 0; u < U; ++u) m = std::max(m, r[u] + 1);
+      sol.groups.assign(m, {});
+      for (int u = 0; u < U; ++u) {
+        sol.groups[r[u]].push_back(units[u]);
+        for (const auto& d : units[u].devices) sol.assignment[d] = r[u];
+      }
+      const StageMapping mp = map_nodes_and_stages(spec, sol, tp);
+      int s = 0;
+      for (const auto& grp : mp.groups) {
+        for (const auto& slot : grp.stages) {
+          int ix = -1;
+          for (int u = 0; u < U && ix < 0; ++u)
+            if (units[u].devices.front() == slot.unit.devices.front()) ix = u;
+          out_unit[static_cast<size_t>(g) * U + s++] = ix;
+        }
+      }
+    }
+    return U;
+  } catch (const InfeasibleError&) {
+    return -3;
+  } catch (const InvalidArgumentError&) {
+    return -6;
+  } catch (...) {
+    return -5;
   }
 }
 

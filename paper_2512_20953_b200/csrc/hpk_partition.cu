@@ -47,6 +47,7 @@ struct Cand {
   int tt_base;     // offset into the time-table scratch
   int best_base;   // offset into global best scratch (when it does not fit smem)
   int use_gmem;
+  int per_l_memory;  // 1: skip the feasible-prefix fast path (test hook)
 };
 
 struct Outs {
@@ -93,6 +94,7 @@ __global__ void __launch_bounds__(THREADS) partition_cost_kernel(Args a) {
   __shared__ int s_first_missing;
   __shared__ double s_bottleneck;
   __shared__ int s_status;
+  __shared__ int s_zero;  // first group with a zero-layer stage (allow_zero only)
   __shared__ int s_lmax[MAXS], s_lcnt[MAXS];  // per stage: largest / number of feasible l >= 1
   __shared__ int s_prefix;                    // every stage's feasible set is [1, lmax]
   const int ci = blockIdx.x;
@@ -122,7 +124,10 @@ __global__ void __launch_bounds__(THREADS) partition_cost_kernel(Args a) {
     tt[x] = total;
     tm[x] = (unsigned char)miss;
   }
-  if (tid == 0) s_status = 0;
+  if (tid == 0) {
+    s_status = 0;
+    s_zero = -1;
+  }
   __syncthreads();
 
   const int* goff = a.group_stage_off + c.group_base + ci;  // n_groups+1 entries
@@ -176,7 +181,7 @@ __global__ void __launch_bounds__(THREADS) partition_cost_kernel(Args a) {
     // so the l passing `bytes <= capacity` (partition.cpp:66) form a prefix
     // [1, lmax]: the DP loop then needs no per-l memory model. Checked, not
     // assumed: a non-prefix stage falls back to the per-l test.
-    const bool fast = P <= MAXS;
+    const bool fast = P <= MAXS && !c.per_l_memory;
     if (fast) {
       for (int i = tid; i < P; i += blockDim.x) {
         s_lmax[i] = 0;
@@ -322,17 +327,24 @@ __global__ void __launch_bounds__(THREADS) partition_cost_kernel(Args a) {
       a.out_total[gix] = a.out_fill[gix] + a.out_steady[gix];
       a.out_bubble[gix] = (double)(P - 1) / (double)(Kj + P - 1);
       worst = worst < a.out_total[gix] ? a.out_total[gix] : worst;
-      if (zero_layers) {  // estimate_stage_time rejects n_layers < 1 (profile.cpp:181)
-        a.outs[ci].status = 6;
-        a.outs[ci].fail_group = j;
-        a.outs[ci].missing_layers = 0;
-        s_status = 6;
-      }
+      // estimate_stage_time rejects n_layers < 1 (profile.cpp:181), but only in
+      // estimate_iteration, after balance_workload ran for EVERY group
+      // (planner.cpp:72-108 then :110): a later group's InfeasibleError or
+      // missing profile entry wins, so the zero-layer group is only recorded
+      if (zero_layers && s_zero < 0) s_zero = j;
     }
     __syncthreads();
     if (s_status) break;
   }
   if (s_status) return;
+  if (s_zero >= 0) {
+    if (tid == 0) {
+      a.outs[ci].status = 6;
+      a.outs[ci].fail_group = s_zero;
+      a.outs[ci].missing_layers = 0;
+    }
+    return;
+  }
 
   // T_sync (cost.cpp:73-120): per layer, holders = first stage holding it in
   // each group, ring over their representatives sorted by global rank.
@@ -421,8 +433,16 @@ using namespace hpkp;
 
 void hpkp_fail(const std::string& msg);
 
+extern "C" int hpk_partition_cost_ex(const hpk_plan_candidate* cands, int n_cands,
+                                     hpk_plan_result* results, int device, int flags);
+
 extern "C" int hpk_partition_cost(const hpk_plan_candidate* cands, int n_cands,
                                   hpk_plan_result* results, int device) {
+  return hpk_partition_cost_ex(cands, n_cands, results, device, 0);
+}
+
+extern "C" int hpk_partition_cost_ex(const hpk_plan_candidate* cands, int n_cands,
+                                     hpk_plan_result* results, int device, int flags) {
   if (n_cands <= 0) return 0;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0) {
@@ -496,7 +516,12 @@ extern "C" int hpk_partition_cost(const hpk_plan_candidate* cands, int n_cands,
     prof.insert(prof.end(), in.prof, in.prof + (size_t)in.n_types * in.n_bits);
     const size_t need = (size_t)(maxP + 1) * W;
     c.best_base = (int)gbest_total;
-    if (need * sizeof(double) > smem_limit) {
+    c.per_l_memory = (flags & HPK_PART_PER_L_MEMORY) ? 1 : 0;
+    if (in.n_groups > 256) {
+      hpkp_fail("hetplan_b200: more than 256 DP groups in one candidate unsupported");
+      return 6;
+    }
+    if (need * sizeof(double) > smem_limit || (flags & HPK_PART_GMEM_TABLES)) {
       c.use_gmem = 1;
       gbest_total += need;
     } else {

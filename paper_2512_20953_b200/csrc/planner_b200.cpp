@@ -1055,6 +1055,65 @@ hp_status status_of(const std::exception_ptr& e, std::string* msg) {
 }
 }  // namespace
 
+void hpkp_fail(const std::string& msg);  // hpk_last_error() text (hpk_grouping.cu)
+
+extern "C" int hpk_map_stages(const hp_cluster* cluster, int tp, int n_groupings,
+                              const int* rgs, int* out_unit) {
+  using namespace hetplan;
+  if (!cluster || tp < 1 || n_groupings < 0 || (n_groupings > 0 && (!rgs || !out_unit))) {
+    hpkp_fail("hpk_map_stages: bad arguments");
+    return -HP_INVALID_ARGUMENT;
+  }
+  try {
+    const ClusterSpec& spec = cluster->spec;
+    const std::vector<TpUnit> units = tp_units(device_list(spec, nullptr), tp);
+    const int U = (int)units.size();
+    std::vector<GroupingSolution> sols(n_groupings);
+    std::vector<StageMapping> maps(n_groupings);
+    std::vector<AffinityIn> aff(n_groupings);
+    std::vector<hpk_affinity_problem> ap(n_groupings);
+    for (int g = 0; g < n_groupings; ++g) {
+      const int* r = rgs + (size_t)g * U;
+      const int m = U ? *std::max_element(r, r + U) + 1 : 0;
+      sols[g].groups.assign(m, {});
+      for (int u = 0; u < U; ++u) {
+        sols[g].groups[r[u]].push_back(units[u]);
+        for (const auto& d : units[u].devices) sols[g].assignment[d] = r[u];
+      }
+      maps[g] = premap_stages(spec, sols[g]);
+      aff[g] = affinity_inputs(maps[g]);
+      ap[g].n_groups = (int)aff[g].goff.size() - 1;
+      ap[g].n_slots = (int)aff[g].type.size();
+      ap[g].group_off = aff[g].goff.data();
+      ap[g].slot_type = aff[g].type.data();
+      ap[g].slot_node = aff[g].node.data();
+      ap[g].slot_perm = aff[g].perm.data();
+      ap[g].swaps = 0;
+    }
+    if (n_groupings > 0) {
+      const int rc = hpk_stage_affinity(ap.data(), n_groupings, -1);
+      if (rc != 0) gpu_fail(rc);
+    }
+    for (int g = 0; g < n_groupings; ++g) {
+      apply_affinity(maps[g], aff[g]);
+      int s = 0;
+      for (const auto& grp : maps[g].groups)
+        for (const auto& slot : grp.stages) {
+          int ix = -1;
+          for (int u = 0; u < U && ix < 0; ++u)
+            if (units[u].devices.front() == slot.unit.devices.front()) ix = u;
+          out_unit[(size_t)g * U + s++] = ix;
+        }
+    }
+    return U;
+  } catch (...) {
+    std::string msg;
+    const hp_status st = status_of(std::current_exception(), &msg);
+    hpkp_fail(msg);
+    return -(int)st;
+  }
+}
+
 extern "C" hp_status hp_plan_compute_batch(int n, const hp_cluster* const* clusters,
                                            const hp_model* model,
                                            const hp_profile* const* profiles,

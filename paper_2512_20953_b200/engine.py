@@ -77,6 +77,87 @@ class hpk_timing(C.Structure):
     ]
 
 
+class hpk_plan_candidate(C.Structure):
+    _fields_ = [
+        ("n_layers", C.c_int), ("tp", C.c_int), ("k_total", C.c_int), ("n_groups", C.c_int),
+        ("ppb", C.c_double), ("pab", C.c_double), ("opt_mult", C.c_double),
+        ("cost_ppb", C.c_double), ("cost_pab", C.c_double),
+        ("intra_bw", C.c_double), ("inter_bw", C.c_double),
+        ("sync_max", C.c_int), ("allow_zero", C.c_int),
+        ("group_stage_off", C.POINTER(C.c_int)), ("microbatches", C.POINTER(C.c_int)),
+        ("stage_type", C.POINTER(C.c_int)), ("stage_index", C.POINTER(C.c_int)),
+        ("stage_mem_capacity", C.POINTER(C.c_double)), ("stage_node", C.POINTER(C.c_int)),
+        ("stage_rank0", C.POINTER(C.c_int)),
+        ("n_types", C.c_int), ("n_bits", C.c_int),
+        ("prof", C.POINTER(C.c_double)),
+    ]
+
+
+class hpk_plan_result(C.Structure):
+    _fields_ = [
+        ("status", C.c_int), ("fail_group", C.c_int), ("fail_kind", C.c_int),
+        ("missing_stage", C.c_int), ("missing_layers", C.c_int),
+        ("stage_layers", C.POINTER(C.c_int)), ("stage_time", C.POINTER(C.c_double)),
+        ("stage_mem", C.POINTER(C.c_double)), ("group_fill", C.POINTER(C.c_double)),
+        ("group_steady", C.POINTER(C.c_double)), ("group_total", C.POINTER(C.c_double)),
+        ("group_bubble", C.POINTER(C.c_double)),
+        ("t_sync", C.c_double), ("t_star", C.c_double),
+    ]
+
+
+class hpk_affinity_problem(C.Structure):
+    _fields_ = [
+        ("n_groups", C.c_int), ("n_slots", C.c_int),
+        ("group_off", C.POINTER(C.c_int)), ("slot_type", C.POINTER(C.c_int)),
+        ("slot_node", C.POINTER(C.c_int)), ("slot_perm", C.POINTER(C.c_int)),
+        ("swaps", C.c_int),
+    ]
+
+
+HPK_PART_GMEM_TABLES = 1
+HPK_PART_PER_L_MEMORY = 2
+
+
+@dataclass
+class PlanCandidate:
+    """One candidate plan for hpk_partition_cost (include/hetplan_b200.h):
+    groups of stages, each stage = (type row, stage_index, capacity, node, rank0)."""
+
+    n_layers: int
+    tp: int
+    k_total: int
+    groups: Sequence[Sequence[tuple]]
+    microbatches: Sequence[int]
+    prof: Sequence[Sequence[float]]  # [type][bit] seconds for 2**bit layers (<= 0: missing)
+    ppb: float
+    pab: float
+    opt_mult: float = 3.0
+    cost_ppb: Optional[float] = None
+    cost_pab: Optional[float] = None
+    intra_bw: float = 600e9
+    inter_bw: float = 50e9
+    sync_max: bool = False
+    allow_zero: bool = False
+
+
+@dataclass
+class PlanResult:
+    status: int
+    fail_group: int
+    fail_kind: int
+    missing_stage: int
+    missing_layers: int
+    layers: List[int]
+    stage_time: List[float]
+    stage_mem: List[float]
+    fill: List[float]
+    steady: List[float]
+    total: List[float]
+    bubble: List[float]
+    t_sync: float
+    t_star: float
+
+
 @dataclass
 class GroupingProblem:
     """Mirror of GroupingProblem (P/include/hetplan/grouping.hpp:49-59) over units."""
@@ -135,6 +216,11 @@ class Engine:
                                           C.POINTER(hpk_grouping_result),
                                           C.POINTER(hpk_search_config)]
         L.hpk_grouping_search.restype = C.c_int
+        L.hpk_partition_cost_ex.argtypes = [C.POINTER(hpk_plan_candidate), C.c_int,
+                                            C.POINTER(hpk_plan_result), C.c_int, C.c_int]
+        L.hpk_partition_cost_ex.restype = C.c_int
+        L.hpk_stage_affinity.argtypes = [C.POINTER(hpk_affinity_problem), C.c_int, C.c_int]
+        L.hpk_stage_affinity.restype = C.c_int
         L.hpk_last_timing.argtypes = [C.POINTER(hpk_timing)]
         L.hpk_reset_timing.argtypes = []
 
@@ -193,3 +279,80 @@ class Engine:
                                       r.waves, r.segment_runs, r.segment_visits, r.max_list,
                                       r.exact_checks))
         return out
+
+    def partition_cost(self, cands: Sequence[PlanCandidate], *, device: int = -1,
+                       flags: int = 0) -> List[PlanResult]:
+        """hpk_partition_cost_ex: layer partition + Eq. (1) cost of every
+        candidate in one launch (one CTA per candidate)."""
+        n = len(cands)
+        arr = (hpk_plan_candidate * n)()
+        res = (hpk_plan_result * n)()
+        keep = []
+        shapes = []
+        for i, c in enumerate(cands):
+            goff = [0]
+            st, si, cap, nd, rk = [], [], [], [], []
+            for g in c.groups:
+                for (ty, idx, cp, node, r0) in g:
+                    st.append(ty)
+                    si.append(idx)
+                    cap.append(cp)
+                    nd.append(node)
+                    rk.append(r0)
+                goff.append(len(st))
+            S, G = len(st), len(c.groups)
+            n_bits = len(c.prof[0]) if c.prof else 0
+            flat = [v for row in c.prof for v in row]
+            bufs = [(C.c_int * len(goff))(*goff), (C.c_int * G)(*c.microbatches),
+                    (C.c_int * S)(*st), (C.c_int * S)(*si), (C.c_double * S)(*cap),
+                    (C.c_int * S)(*nd), (C.c_int * S)(*rk), (C.c_double * max(1, len(flat)))(*flat)]
+            outs = [(C.c_int * S)(), (C.c_double * S)(), (C.c_double * S)(), (C.c_double * G)(),
+                    (C.c_double * G)(), (C.c_double * G)(), (C.c_double * G)()]
+            keep += bufs + outs
+            shapes.append((S, G, outs))
+            arr[i] = hpk_plan_candidate(
+                c.n_layers, c.tp, c.k_total, G, c.ppb, c.pab, c.opt_mult,
+                c.ppb if c.cost_ppb is None else c.cost_ppb,
+                c.pab if c.cost_pab is None else c.cost_pab, c.intra_bw, c.inter_bw,
+                int(c.sync_max), int(c.allow_zero), bufs[0], bufs[1], bufs[2], bufs[3], bufs[4],
+                bufs[5], bufs[6], len(c.prof), n_bits, bufs[7])
+            r = res[i]
+            (r.stage_layers, r.stage_time, r.stage_mem, r.group_fill, r.group_steady,
+             r.group_total, r.group_bubble) = outs
+        rc = self.lib.hpk_partition_cost_ex(arr, n, res, device, flags)
+        if rc != 0:
+            raise EngineError(rc, self.lib.hpk_last_error().decode())
+        out = []
+        for i in range(n):
+            S, G, o = shapes[i]
+            r = res[i]
+            out.append(PlanResult(r.status, r.fail_group, r.fail_kind, r.missing_stage,
+                                  r.missing_layers, list(o[0]), list(o[1]), list(o[2]),
+                                  list(o[3]), list(o[4]), list(o[5]), list(o[6]), r.t_sync,
+                                  r.t_star))
+        return out
+
+    def stage_affinity(self, problems: Sequence[tuple], *, device: int = -1):
+        """hpk_stage_affinity: the stage mapper's DP-affinity pass for every
+        problem (groups: list of [(type, node), ...] slots in stage order).
+        Returns (perm, swaps) per problem: slot s now holds original slot perm[s]."""
+        n = len(problems)
+        arr = (hpk_affinity_problem * n)()
+        keep, perms = [], []
+        for i, groups in enumerate(problems):
+            goff, ty, nd = [0], [], []
+            for g in groups:
+                for (t, v) in g:
+                    ty.append(t)
+                    nd.append(v)
+                goff.append(len(ty))
+            S = len(ty)
+            b = [(C.c_int * len(goff))(*goff), (C.c_int * S)(*ty), (C.c_int * S)(*nd),
+                 (C.c_int * S)()]
+            keep += b
+            perms.append(b[3])
+            arr[i] = hpk_affinity_problem(len(groups), S, b[0], b[1], b[2], b[3], 0)
+        rc = self.lib.hpk_stage_affinity(arr, n, device)
+        if rc != 0:
+            raise EngineError(rc, self.lib.hpk_last_error().decode())
+        return [(list(perms[i]), arr[i].swaps) for i in range(n)]

@@ -38,6 +38,23 @@ def test_batch_cfg5_sweep_matches_golden(product_lib, golden_plans):
         assert out == (g["json"] if st == 0 else g["error"]), case.name
 
 
+def test_batch_full_cfg5_sweep_plans_match_reference(product_lib):
+    """All 1000 snapshots of the sweep in ONE hp_plan_compute_batch call: every
+    plan JSON hashes to the reference planner's (tests/golden/cfg5_plans.json,
+    tools/make_cfg5_plans.py, oracle/_ref/libhetplan.so at default options)."""
+    import hashlib
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "cfg5_plans.json")) as f:
+        golden = json.load(f)
+    snaps = configs.cfg5_snapshots(1000)
+    got = _batch(product_lib, [s.cluster_json() for s in snaps], snaps[0].model_json(),
+                 snaps[0].max_layers)
+    assert len(got) == len(golden) == 1000
+    bad = [g["snapshot"] for g, (st, out) in zip(golden, got)
+           if (st, hashlib.sha256(out.encode()).hexdigest()) != (g["status"], g["sha256"])]
+    assert not bad, (len(bad), bad[:10])
+
+
 def test_batch_with_failing_clusters_matches_reference(product_lib, ref_lib):
     w = configs.cfg3()
     tiny = json.loads(w.cluster_json())

@@ -1,0 +1,263 @@
+"""Direct GPU parity of the small kernels and of the planner's host rows.
+
+* hpk_partition_cost (hpk_partition.cu) on every reference-generated partition
+  vector (tests/golden/partition.json, from P/src/partition.cpp:51-110 through
+  the reference probe), with each slow branch forced on: global-memory DP
+  tables and the per-layer-count memory check.
+* the stage mapper (host joint / fallback placement + hpk_stage_affinity) on
+  random groupings of random clusters against the reference
+  map_nodes_and_stages (P/src/stage_map.cpp:63-216) via the probe.
+* R1-R3 restated in planner_b200.cpp: random clusters (uneven node counts,
+  requested TP dimensions that do not divide) through both libraries give the
+  same status and message, or the same plan.
+"""
+import ctypes as C
+import json
+import os
+import random
+
+import pytest
+
+from oracle.binding import PROBE_LIB
+from paper_2512_20953_b200 import configs
+from paper_2512_20953_b200.capi import HetplanError, PlanOptions
+from paper_2512_20953_b200.engine import (HPK_PART_GMEM_TABLES, HPK_PART_PER_L_MEMORY,
+                                          PlanCandidate)
+
+pytestmark = pytest.mark.gpu
+
+TYPES = {"A100": {"compute_power": 1.0, "memory_bytes": 80e9},
+         "H800": {"compute_power": 2.0, "memory_bytes": 80e9},
+         "H20": {"compute_power": 1.5, "memory_bytes": 100e9}}
+
+
+def _vector_candidate(rec):
+    P = len(rec["prof"])
+    stages = [(s, rec["stage_index"][s], rec["mem_capacity"][s], 0, s) for s in range(P)]
+    return PlanCandidate(n_layers=rec["n_layers"], tp=rec["tp"], k_total=rec["k_total"],
+                         groups=[stages], microbatches=[rec["k_total"]], prof=rec["prof"],
+                         ppb=rec["ppb"], pab=rec["pab"], opt_mult=rec["opt_mult"])
+
+
+@pytest.mark.parametrize("flags", [0, HPK_PART_GMEM_TABLES, HPK_PART_PER_L_MEMORY,
+                                   HPK_PART_GMEM_TABLES | HPK_PART_PER_L_MEMORY])
+def test_partition_kernel_matches_reference_vectors(engine, golden_partition, flags):
+    assert len(golden_partition) >= 200
+    res = engine.partition_cost([_vector_candidate(r) for r in golden_partition], flags=flags)
+    seen = {0: 0, 3: 0, 6: 0}
+    for rec, r in zip(golden_partition, res):
+        assert r.status == rec["status"], rec
+        seen[r.status] += 1
+        if r.status != 0:
+            continue
+        assert r.layers == rec["layers"], rec
+        assert [t.hex() for t in r.stage_time] == rec["times"], rec
+        assert max(r.stage_time).hex() == rec["bottleneck"]
+    assert seen[0] > 50 and seen[3] > 10  # the vectors cover both outcomes
+
+
+def test_partition_kernel_multi_group_batch(engine, golden_partition):
+    # several groups per candidate and many candidates per launch: every group
+    # must equal its single-group vector (the DP is per group)
+    ok = [r for r in golden_partition if r["status"] == 0]
+    rng = random.Random(7)
+    cands, parts = [], []
+    for _ in range(40):
+        # groups of one candidate share n_layers / model constants
+        base = rng.choice(ok)
+        same = [r for r in ok if all(r[k] == base[k] for k in
+                                     ("n_layers", "ppb", "pab", "opt_mult", "k_total", "tp"))]
+        grp = [rng.choice(same) for _ in range(rng.randint(1, 3))]
+        prof, groups = [], []
+        for g in grp:
+            P = len(g["prof"])
+            groups.append([(len(prof) + s, g["stage_index"][s], g["mem_capacity"][s], 0, s)
+                           for s in range(P)])
+            prof += g["prof"]
+        nb = max(len(p) for p in prof)
+        prof = [p + [0.0] * (nb - len(p)) for p in prof]
+        cands.append(PlanCandidate(n_layers=base["n_layers"], tp=base["tp"],
+                                   k_total=base["k_total"], groups=groups,
+                                   microbatches=[1] * len(groups), prof=prof, ppb=base["ppb"],
+                                   pab=base["pab"], opt_mult=base["opt_mult"]))
+        parts.append(grp)
+    for flags in (0, HPK_PART_GMEM_TABLES):
+        res = engine.partition_cost(cands, flags=flags)
+        for grp, r in zip(parts, res):
+            assert r.status == 0
+            want = [x for g in grp for x in g["layers"]]
+            assert r.layers == want
+            assert [t.hex() for t in r.stage_time] == [x for g in grp for x in g["times"]]
+
+
+def _rand_cluster(rng, max_nodes=6):
+    nodes = []
+    for i in range(rng.randint(1, max_nodes)):
+        nodes.append({"node_id": i, "count": rng.choice([1, 2, 2, 4, 4, 8]),
+                      "type": rng.choice(sorted(TYPES))})
+    return {"gpu_types": TYPES, "nodes": nodes, "bandwidths": dict(configs.BANDWIDTHS)}
+
+
+def _rand_rgs(rng, n):
+    rgs, m = [], 0
+    for _ in range(n):
+        g = rng.randint(0, m) if rng.random() < 0.8 else m  # m opens a new group
+        rgs.append(g)
+        m = max(m, g + 1)
+    return rgs
+
+
+@pytest.fixture(scope="module")
+def probe():
+    if not os.path.exists(PROBE_LIB):
+        pytest.skip("reference probe not built")
+    lib = C.CDLL(PROBE_LIB)
+    lib.ref_map_stages.argtypes = [C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_int),
+                                   C.POINTER(C.c_int)]
+    return lib
+
+
+def test_stage_mapper_matches_reference_on_random_groupings(product_lib, probe):
+    lib = product_lib.lib
+    lib.hpk_map_stages.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int),
+                                   C.POINTER(C.c_int)]
+    rng = random.Random(2512)
+    total = swapped = 0
+    while total < 500:
+        cl = _rand_cluster(rng)
+        tp = rng.choice(configs.tp_dims_of(cl))
+        U = sum(nd["count"] for nd in cl["nodes"]) // tp
+        k = 25
+        rgs = [x for _ in range(k) for x in _rand_rgs(rng, U)]
+        arr = (C.c_int * len(rgs))(*rgs)
+        want = (C.c_int * len(rgs))()
+        got = (C.c_int * len(rgs))()
+        text = json.dumps(cl)
+        assert probe.ref_map_stages(text.encode(), tp, k, arr, want) == U
+        h = product_lib.cluster_parse(text)
+        rc = lib.hpk_map_stages(h.ptr, tp, k, arr, got)
+        assert rc == U, product_lib.lib.hp_last_error()
+        for j in range(k):
+            a = list(want[j * U:(j + 1) * U])
+            b = list(got[j * U:(j + 1) * U])
+            assert a == b, (cl, tp, rgs[j * U:(j + 1) * U])
+            # count groupings where the affinity pass changed the placement order
+            swapped += a != sorted(a)
+        total += k
+    assert swapped > 50
+
+
+def test_planner_host_rows_match_reference_on_random_clusters(product_lib, ref_lib):
+    """R1 (tp dims + divisibility status), R2 (units), R3 (MIN_mem) through whole
+    plans: same status + message, or byte-identical plan JSON."""
+    rng = random.Random(99)
+    model = {"n_layers": 8, "per_layer_param_bytes": 1e8, "per_layer_activation_bytes": 5e7,
+             "optimizer_multiplier": 3.0, "n_microbatches": 8, "global_batch_tokens": 1 << 20}
+    outcomes = set()
+    for it in range(60):
+        cl = _rand_cluster(rng, max_nodes=4)
+        nodes = cl["nodes"]
+        if rng.random() < 0.4:  # an uneven node: only tp=1 divides every count
+            nodes[rng.randrange(len(nodes))]["count"] = rng.choice([3, 5, 6])
+        md = dict(model, n_layers=rng.choice([4, 8, 16]),
+                  per_layer_param_bytes=rng.choice([1e8, 2e9, 2e10]))
+        opts = PlanOptions(tp_dims=rng.choice([None, [1], [2], [1, 2, 4], [4, 2, 8, 2]]),
+                           exact_threshold=12, node_budget=20000)
+        res = []
+        for lib in (ref_lib, product_lib):
+            c = lib.cluster_parse(json.dumps(cl))
+            m = lib.model_parse(json.dumps(md))
+            p = lib.profile_synth(c, 0.05, 16)
+            try:
+                res.append(("ok", lib.plan_to_json(lib.plan_compute(c, m, p, opts))))
+            except HetplanError as e:
+                res.append((e.status, e.message))
+        assert res[0] == res[1], (cl, md, opts)
+        outcomes.add(res[0][0] if res[0][0] != "ok" else "ok")
+        if "divisibility" in str(res[0][1]):
+            outcomes.add("divisibility")
+    assert "ok" in outcomes and len(outcomes) >= 3, outcomes
+
+
+def test_reference_acceptance_suite_on_the_product():
+    """P/tests/acceptance.cpp compiled unchanged and linked against
+    libhetplan_b200.so (oracle/Makefile accept_b200): C6 (plan shape), C10
+    (determinism / byte-identical plans, 24 GPUs of 3 types) and C11 (planning
+    overhead) call the B200 plan_cluster through the reference's own harness."""
+    import subprocess
+    exe = os.path.join(os.path.dirname(PROBE_LIB), "hetplan_acceptance_b200")
+    if not os.path.exists(exe):
+        pytest.fail("oracle/_ref/hetplan_acceptance_b200 missing: run __graft_entry__.build()")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("[")]
+    assert len(lines) == 11, out.stdout + out.stderr
+    assert all(ln.startswith("[PASS]") for ln in lines), out.stdout
+    assert out.returncode == 0
+
+
+# ---- the reference's own known answers, on the GPU path (the oracle versions
+# live in tests/test_oracle.py; P/tests/test_grouping.cpp, acceptance.cpp C4/C9)
+def _gp(*a, **k):
+    from paper_2512_20953_b200.engine import GroupingProblem
+    return GroupingProblem(*a, **k)
+
+
+@pytest.mark.parametrize("enumeration", [False, True])
+def test_gpu_known_answer_two_a100_one_h800(engine, enumeration):
+    # test_grouping.cpp:87-104: objective 32/9, z 16/9, the A100s together
+    r = engine.grouping_search([_gp([1.0, 1.0, 2.0], [10.0] * 3, 8, 5.0, [0, 0, 1], [0, 0, 1])],
+                               enumeration=enumeration)[0]
+    assert r.count == 1 and r.optimal
+    assert r.rgs[0][0] == r.rgs[0][1] != r.rgs[0][2]
+    assert abs(r.objective[0] - 32.0 / 9.0) < 1e-12 and abs(r.z[0] - 16.0 / 9.0) < 1e-12
+
+
+def test_gpu_known_answer_budget_abort(engine):
+    # test_grouping.cpp:222-247: 12 identical units, threshold 4, budget 50 ->
+    # optimal = false after exactly 50 visits, deterministic across runs
+    pb = _gp([1.0] * 12, [8.0] * 12, 8, 4.0, [0] * 12, list(range(12)), exact_threshold=4,
+             node_budget=50)
+    a, b = engine.grouping_search([pb, pb])
+    assert not a.optimal and a.visited == 50 and a.objective[0] > 0
+    assert (a.rgs, a.objective, a.visited) == (b.rgs, b.objective, b.visited)
+    full = engine.grouping_search([_gp([1.0] * 12, [8.0] * 12, 8, 4.0, [0] * 12,
+                                       list(range(12)), exact_threshold=12)])[0]
+    assert full.optimal and full.objective[0] >= a.objective[0]
+
+
+@pytest.mark.parametrize("enumeration", [False, True])
+def test_gpu_known_answer_tie_break(engine, enumeration):
+    # test_grouping.cpp:202-220: K = 1, two identical devices -> two singletons
+    r = engine.grouping_search([_gp([1.0, 1.0], [4.0, 4.0], 1, 2.0, [0, 0], [0, 0])],
+                               enumeration=enumeration)[0]
+    assert r.rgs[0] == [0, 1] and r.objective[0] == 2.0
+
+
+def test_gpu_known_answer_proportional_partition(engine):
+    # acceptance.cpp C4 tail: powers (1,1,2,2), 24 layers -> (4,4,8,8), equal times
+    rows = [[(1 << b) / pw for b in range(5)] for pw in (1.0, 1.0, 2.0, 2.0)]
+    c = PlanCandidate(n_layers=24, tp=1, k_total=8, groups=[[(s, s + 1, 1e300, 0, s)
+                                                             for s in range(4)]],
+                      microbatches=[8], prof=rows, ppb=0.0, pab=0.0, opt_mult=0.0)
+    for flags in (0, HPK_PART_GMEM_TABLES | HPK_PART_PER_L_MEMORY):
+        r = engine.partition_cost([c], flags=flags)[0]
+        assert r.status == 0 and r.layers == [4, 4, 8, 8] and len(set(r.stage_time)) == 1
+
+
+def test_gpu_binary_decomposition_exact(engine):
+    # acceptance.cpp C9: T(n) == c*n exactly for c = 0.25, n in 1..64 (the
+    # kernel's stage-time table is the ascending-bit sum, profile.cpp:180-190)
+    row = [0.25 * (1 << b) for b in range(7)]
+    cands = [PlanCandidate(n_layers=n, tp=1, k_total=1, groups=[[(0, 1, 1e300, 0, 0)]],
+                           microbatches=[1], prof=[row], ppb=0.0, pab=0.0, opt_mult=0.0)
+             for n in range(1, 65)]
+    for n, r in zip(range(1, 65), engine.partition_cost(cands)):
+        assert r.status == 0 and r.layers == [n] and r.stage_time[0] == 0.25 * n
+
+
+def test_gpu_stage_time_ascending_bits(engine):
+    # test_profile.cpp:51-66 style: 7 layers = (T1 + T2) + T4, in that order
+    row = [0.1, 0.7, 5.0]
+    c = PlanCandidate(n_layers=7, tp=1, k_total=1, groups=[[(0, 1, 1e300, 0, 0)]],
+                      microbatches=[1], prof=[row], ppb=0.0, pab=0.0, opt_mult=0.0)
+    assert engine.partition_cost([c])[0].stage_time[0] == (0.1 + 0.7) + 5.0

@@ -1,7 +1,7 @@
 """Golden grouping-search results of the whole cfg5 sweep (tests/golden/cfg5_search.json):
 for every snapshot and valid TP dimension, the reference's nodes_visited, optimal flag,
-winner objective (hex) and winner RGS, from the pinned C restatement
-(oracle/_ref/libhpo.so, checked against the reference probe by tests/test_oracle.py).
+winner objective (hex) and winner RGS, from the REFERENCE itself: solve_grouping_topk
+(P/src/grouping.cpp:269-335) through the probe oracle/_ref/libhetplan_probe.so.
 The GPU test runs all 1167 searches in one batch and compares each.
 Run: python tools/make_cfg5_search.py   (~1 min on 8 cores)"""
 import json
@@ -13,7 +13,9 @@ from multiprocessing import Pool
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-from oracle.binding import Oracle
+import ctypes as C
+
+from oracle.binding import PROBE_LIB
 from paper_2512_20953_b200.configs import min_mem_for, units_for  # noqa: E402
 from paper_2512_20953_b200 import configs  # noqa: E402
 
@@ -32,12 +34,19 @@ def problems(count=1000):
 
 def solve(pb):
     si, tp, P, M, K, MIN, T, N = pb
-    r = Oracle().solve_grouping(P, M, K, MIN, T, N)
-    rec = {"snapshot": si, "tp": tp, "status": r.status}
-    if r.status == 0:
-        rec.update({"visited": r.visited, "optimal": r.optimal,
-                    "objective": r.objective[0].hex(),
-                    "rgs": "".join(chr(48 + x) for x in r.rgs[0])})
+    probe = C.CDLL(PROBE_LIB)
+    n = len(P)
+    D = lambda a: (C.c_double * len(a))(*a)  # noqa: E731
+    I = lambda a: (C.c_int * len(a))(*a)  # noqa: E731
+    cnt, opt, vis = C.c_int(), C.c_int(), C.c_longlong()
+    rgs, obj, z = (C.c_int * n)(), (C.c_double * 1)(), (C.c_double * 1)()
+    rc = probe.ref_solve_grouping(n, D(P), D(M), I(T), I(N), K, C.c_double(MIN), 8,
+                                  C.c_longlong(5_000_000), 1, C.byref(cnt), rgs, obj, z,
+                                  C.byref(opt), C.byref(vis))
+    rec = {"snapshot": si, "tp": tp, "status": rc}
+    if rc == 0:
+        rec.update({"visited": vis.value, "optimal": bool(opt.value), "objective": obj[0].hex(),
+                    "rgs": "".join(chr(48 + x) for x in rgs)})
     return rec
 
 
