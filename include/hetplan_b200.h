@@ -179,8 +179,10 @@ typedef struct hpk_grouping_result {
   long long exact_checks;            /* child checks inside the filter margin (exact path) */
 } hpk_grouping_result;
 
+#define HPK_ALL_DEVICES (-2)
 typedef struct hpk_search_config {
-  int device;            /* CUDA ordinal (-1: current) */
+  int device;            /* CUDA ordinal (-1: current; HPK_ALL_DEVICES: every visible
+                            device, problems longest-first to the least-loaded one) */
   long long segment_cap; /* visits per segment run per wave (0: default) */
   int max_list;          /* segment list capacity per problem (0: default) */
   int force_serial;      /* 1: use the serial replica kernel for every problem */
@@ -284,6 +286,8 @@ typedef struct hpk_timing {
   double h2d_ms, d2h_ms;
   long long h2d_bytes, d2h_bytes;
   int kernel_launches;
+  int devices_used;     /* GPUs the grouping search ran on */
+  double affinity_ms;   /* stage-mapper affinity kernel */
 } hpk_timing;
 void hpk_last_timing(hpk_timing* out);
 void hpk_reset_timing(void);

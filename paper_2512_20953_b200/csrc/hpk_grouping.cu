@@ -31,6 +31,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -3619,7 +3620,8 @@ double seed_floor(const hpk_grouping_problem& pr) {
 // Hooks shared with hpk_partition.cu (same thread-local error / timing).
 void hpkp_fail(const std::string& msg) { t_err = msg; }
 namespace hpk_timing_bridge {
-void add_launch(long long h2d, long long d2h) {
+void add_affinity(double ms, long long h2d, long long d2h) {
+  t_timing.affinity_ms += ms;
   t_timing.kernel_launches += 1;
   t_timing.h2d_bytes += h2d;
   t_timing.d2h_bytes += d2h;
@@ -3685,6 +3687,100 @@ void hpk_last_timing(hpk_timing* out) {
 
 void hpk_reset_timing(void) { t_timing = hpk_timing{}; }
 
+}  // extern "C"
+
+namespace hpk {
+
+int search_device(const hpk_grouping_problem* problems, int n_problems,
+                  hpk_grouping_result* results, const hpk_search_config& cfg);
+
+// Relative cost of one search for the device assignment: a budgeted search
+// runs node_budget visits, an exhaustive one Bell(n); deeper searches cost more
+// per visit (more groups per node check), hence the unit-count weight.
+double search_cost(const hpk_grouping_problem& pr) {
+  double bell = 1;  // Bell(n) by the Bell triangle, capped
+  {
+    std::vector<double> row{1.0};
+    for (int i = 1; i < pr.n && bell < 1e18; ++i) {
+      std::vector<double> next{row.back()};
+      for (double x : row) next.push_back(next.back() + x);
+      row.swap(next);
+      bell = row.back();
+    }
+  }
+  const bool budgeted = pr.n > pr.exact_threshold && pr.node_budget >= 0;
+  const double visits = budgeted ? std::min<double>((double)pr.node_budget, bell) : bell;
+  return visits * (double)(pr.n + 8);
+}
+
+// hpk_grouping_search over every visible device: problems go longest-first to
+// the least-loaded device (one host thread and one persistent kernel per
+// device, each on its own context and stream); results land in the caller's
+// slots. Device time is the max over devices (they run concurrently).
+int search_all_devices(const hpk_grouping_problem* problems, int n_problems,
+                       hpk_grouping_result* results, const hpk_search_config& cfg, int ndev) {
+  const int D = std::min(ndev, 16);
+  std::vector<int> order(n_problems);
+  std::vector<double> cost(n_problems);
+  for (int i = 0; i < n_problems; ++i) {
+    order[i] = i;
+    cost[i] = search_cost(problems[i]);
+  }
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+  std::vector<double> load(D, 0.0);
+  std::vector<std::vector<int>> mine(D);
+  for (int i : order) {
+    int d = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+    load[d] += cost[i];
+    mine[d].push_back(i);
+  }
+  for (auto& m : mine) std::sort(m.begin(), m.end());  // batch in caller order
+  std::vector<int> rc(D, 0);
+  std::vector<hpk_timing> tim(D);
+  std::vector<std::string> err(D);
+  auto run = [&](int d) {
+    if (mine[d].empty()) return;
+    std::vector<hpk_grouping_problem> pb;
+    std::vector<hpk_grouping_result> rs;
+    for (int i : mine[d]) {
+      pb.push_back(problems[i]);
+      rs.push_back(results[i]);
+    }
+    hpk_search_config c = cfg;
+    c.device = d;
+    t_timing = hpk_timing{};
+    rc[d] = search_device(pb.data(), (int)pb.size(), rs.data(), c);
+    tim[d] = t_timing;
+    err[d] = t_err;
+    for (size_t k = 0; k < mine[d].size(); ++k) results[mine[d][k]] = rs[k];
+  };
+  std::vector<std::thread> workers;
+  for (int d = 1; d < D; ++d) workers.emplace_back(run, d);
+  const hpk_timing before = t_timing;
+  run(0);
+  for (auto& w : workers) w.join();
+  t_timing = before;
+  for (int d = 0; d < D; ++d) {
+    t_timing.search_ms = std::max(t_timing.search_ms, before.search_ms + tim[d].search_ms);
+    t_timing.serial_ms = std::max(t_timing.serial_ms, before.serial_ms + tim[d].serial_ms);
+    t_timing.h2d_bytes += tim[d].h2d_bytes;
+    t_timing.d2h_bytes += tim[d].d2h_bytes;
+    t_timing.kernel_launches += tim[d].kernel_launches;
+  }
+  t_timing.devices_used = 0;
+  for (int d = 0; d < D; ++d) t_timing.devices_used += mine[d].empty() ? 0 : 1;
+  for (int d = 0; d < D; ++d)
+    if (rc[d] != 0) {
+      t_err = err[d];
+      return rc[d];
+    }
+  return 0;
+}
+
+}  // namespace hpk
+
+extern "C" {
+
 int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
                         hpk_grouping_result* results, const hpk_search_config* cfg_in) {
   t_err.clear();
@@ -3696,6 +3792,27 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
   if (ndev <= 0)
     return fail(5, "hetplan_b200: no CUDA device visible; the B200 planner has no CPU "
                    "fallback");
+  if (cfg.device == HPK_ALL_DEVICES) {
+    if (ndev > 1) return search_all_devices(problems, n_problems, results, cfg, ndev);
+    cfg.device = 0;
+  }
+  if (cfg.device < 0) {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess) d = 0;
+    cfg.device = d;
+  }
+  const int rc = search_device(problems, n_problems, results, cfg);
+  t_timing.devices_used = std::max(t_timing.devices_used, 1);
+  return rc;
+}
+
+}  // extern "C"
+
+namespace hpk {
+
+int search_device(const hpk_grouping_problem* problems, int n_problems,
+                  hpk_grouping_result* results, const hpk_search_config& cfg) {
+  const int ndev = hpk_device_count();
   int device = cfg.device;
   if (device < 0) {
     if (cudaGetDevice(&device) != cudaSuccess) device = 0;
@@ -4203,4 +4320,4 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
   return 0;
 }
 
-}  // extern "C"
+}  // namespace hpk

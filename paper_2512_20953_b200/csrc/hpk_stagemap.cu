@@ -34,7 +34,7 @@
 
 void hpkp_fail(const std::string& msg);  // thread-local error of the hpk_* layer
 namespace hpk_timing_bridge {
-void add_launch(long long h2d, long long d2h);  // this thread's hpk_timing
+void add_affinity(double ms, long long h2d, long long d2h);  // this thread's hpk_timing
 }
 
 namespace hpks {
@@ -130,6 +130,7 @@ __global__ void __launch_bounds__(THREADS) affinity_kernel(Prob* probs, const in
 struct Ctx {
   int device = -1;
   cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   HpkArena arena;
   std::mutex mu;
 };
@@ -166,6 +167,8 @@ extern "C" int hpk_stage_affinity(hpk_affinity_problem* probs, int n, int device
   HPKS_CUDA(cudaSetDevice(device));
   if (cx.device != device) {
     HPKS_CUDA(cudaStreamCreateWithFlags(&cx.stream, cudaStreamNonBlocking));
+    HPKS_CUDA(cudaEventCreate(&cx.ev0));
+    HPKS_CUDA(cudaEventCreate(&cx.ev1));
     cx.device = device;
   }
   std::vector<Prob> hp(n);
@@ -229,15 +232,10 @@ extern "C" int hpk_stage_affinity(hpk_affinity_problem* probs, int n, int device
     HPKS_CUDA(cudaFuncSetAttribute(affinity_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)max_smem));
   constexpr bool trace = HPK_HOST_TRACE != 0;  // build-time: -DHPK_HOST_TRACE=1
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (trace) {
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    cudaEventRecord(e0, cx.stream);
-  }
+  HPKS_CUDA(cudaEventRecord(cx.ev0, cx.stream));
   affinity_kernel<<<n, THREADS, max_smem, cx.stream>>>(d_probs, d_goff, d_type, d_node, d_perm);
   HPKS_CUDA(cudaGetLastError());
-  if (trace) cudaEventRecord(e1, cx.stream);
+  HPKS_CUDA(cudaEventRecord(cx.ev1, cx.stream));
   // outputs: the permutation, and the problem records (swap counts) again
   HPKS_CUDA(cudaMemcpyAsync(ar.h + o_perm, ar.d + o_perm, out_end - o_perm, cudaMemcpyDeviceToHost,
                             cx.stream));
@@ -245,21 +243,20 @@ extern "C" int hpk_stage_affinity(hpk_affinity_problem* probs, int n, int device
                             cudaMemcpyDeviceToHost, cx.stream));
   HPKS_CUDA(cudaStreamSynchronize(cx.stream));
   const int* perm = ar.hp<int>(o_perm);
-  hpk_timing_bridge::add_launch((long long)in_end, (long long)(out_end - o_perm + sizeof(Prob) * n));
+  float kms = 0;
+  HPKS_CUDA(cudaEventElapsedTime(&kms, cx.ev0, cx.ev1));
+  hpk_timing_bridge::add_affinity(kms, (long long)in_end,
+                                  (long long)(out_end - o_perm + sizeof(Prob) * n));
   std::memcpy(hp.data(), ar.h + o_probs, sizeof(Prob) * n);
   for (int k = 0; k < n; ++k) {
     for (int s = 0; s < probs[k].n_slots; ++s) probs[k].slot_perm[s] = perm[hp[k].in_off + s];
     probs[k].swaps = hp[k].swaps;
   }
   if (trace) {
-    float ms = 0;
-    cudaEventElapsedTime(&ms, e0, e1);
-    fprintf(stderr, "[hpk-affinity] %d problems, kernel %.3f ms, swaps:", n, ms);
+    fprintf(stderr, "[hpk-affinity] %d problems, kernel %.3f ms, swaps:", n, kms);
     for (int k = 0; k < n && k < 16; ++k)
       fprintf(stderr, " %d(S=%d,G=%d)", hp[k].swaps, hp[k].n_slots, hp[k].n_groups);
     fprintf(stderr, "\n");
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
   }
   return 0;
 }

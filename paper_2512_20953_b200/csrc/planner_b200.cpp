@@ -926,6 +926,9 @@ void plan_jobs(std::vector<PlanJob*>& jobs, int threads) {
       hpk_search_config scfg;
       hpk_search_config_init(&scfg);
       scfg.enumerate = 1;
+      // every visible GPU: the TP-dimension searches of a plan (and the
+      // snapshots of a sweep) go longest-first to the least-loaded device
+      scfg.device = HPK_ALL_DEVICES;
       const int rc = hpk_grouping_search(problems.data(), (int)problems.size(), gres.data(),
                                          &scfg);
       if (rc != 0) gpu_fail(rc);

@@ -14,6 +14,7 @@ from typing import List, Optional, Sequence
 
 HPK_MAX_UNITS = 64
 HPK_MAX_TOPK = 16
+HPK_ALL_DEVICES = -2
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("HPK_LIB") or os.path.join(PKG_DIR, "libhetplan_b200.so")
@@ -74,6 +75,8 @@ class hpk_timing(C.Structure):
         ("h2d_bytes", C.c_longlong),
         ("d2h_bytes", C.c_longlong),
         ("kernel_launches", C.c_int),
+        ("devices_used", C.c_int),
+        ("affinity_ms", C.c_double),
     ]
 
 
