@@ -138,7 +138,7 @@ void hp_recovery_free(hp_recovery* recovery);                         /* c_api.h
  * B200 kernel C-ABI (new)                                              *
  * ------------------------------------------------------------------ */
 #define HPK_MAX_UNITS 64 /* wave engine; larger problems use the serial replica */
-#define HPK_MAX_TOPK 16
+#define HPK_MAX_TOPK 16 /* wave engine (larger top_k: serial replica) */
 #ifndef HPK_HOST_TRACE
 #define HPK_HOST_TRACE 0 /* build with -DHPK_HOST_TRACE=1 for per-phase host timings */
 #endif
@@ -168,8 +168,8 @@ typedef struct hpk_grouping_result {
   int optimal;                       /* 0 if the node budget ran out (grouping.cpp:317) */
   int engine;                        /* 0 wave engine, 1 serial replica, 2 enumeration */
   long long visited;                 /* GroupingSolution::nodes_visited */
-  double objective[HPK_MAX_TOPK];
-  double z[HPK_MAX_TOPK];
+  double* objective;                 /* caller-owned [top_k] */
+  double* z;                         /* caller-owned [top_k] */
   int* rgs;                          /* caller-owned [top_k * n]: group of unit i */
   /* engine statistics */
   int waves;
@@ -277,6 +277,35 @@ int hpk_stage_affinity(hpk_affinity_problem* problems, int n_problems, int devic
 int hpk_map_stages(const hp_cluster* cluster, int tp, int n_groupings, const int* rgs,
                    int* out_unit);
 
+/* The 1F1B schedule recurrence of simulate_pipeline (P/src/pipeline_sim.cpp:46-149)
+ * for many pipelines in one launch (one CTA per pipeline, one thread per
+ * stage). Inputs are the StageTiming fields per stage; outputs are the
+ * reference's PipelineSimResult values: makespan, busy and peak_in_flight per
+ * stage, and each stage's tasks' start / end times in the stage's static order
+ * (warmup forwards, F/B pairs, backward drain; :53-66). */
+typedef struct hpk_pipeline {
+  int n_stages, n_microbatches;
+  const double* forward;        /* [n_stages] */
+  const double* backward;
+  const double* send_forward;
+  const double* send_backward;
+  double makespan;              /* out */
+  double* busy;                 /* out [n_stages] */
+  int* peak_in_flight;          /* out [n_stages] */
+  double* task_start;           /* out [n_stages * 2 * n_microbatches] or NULL */
+  double* task_end;
+} hpk_pipeline;
+int hpk_pipeline_sim(hpk_pipeline* pipes, int n_pipes, int device);
+
+/* Extension of the drop-in ABI: hp_simulate (c_api.h:113-115) for n plans of
+ * one model in ONE simulator launch (every DP group of every plan). Results are
+ * the reference's hp_sim_result handles (hp_sim_result_to_json /
+ * hp_sim_timeline_csv / hp_sim_result_free apply). Returns the first error
+ * (text in hpk_last_error()); out[i] is NULL then. */
+hp_status hp_simulate_batch(int n, const hp_plan* const* plans, const hp_cluster* const* clusters,
+                            const hp_model* model, const hp_profile* const* profiles,
+                            const hp_sim_options* options, hp_sim_result** out);
+
 /* Device-side timing of this thread's last hpk_grouping_search /
  * hpk_partition_cost calls (CUDA events on the launching stream). */
 typedef struct hpk_timing {
@@ -288,6 +317,7 @@ typedef struct hpk_timing {
   int kernel_launches;
   int devices_used;     /* GPUs the grouping search ran on */
   double affinity_ms;   /* stage-mapper affinity kernel */
+  double pipeline_ms;   /* 1F1B pipeline simulator kernel */
 } hpk_timing;
 void hpk_last_timing(hpk_timing* out);
 void hpk_reset_timing(void);

@@ -12,6 +12,7 @@
 #include "hetplan/cluster.hpp"
 #include "hetplan/grouping.hpp"
 #include "hetplan/partition.hpp"
+#include "hetplan/pipeline_sim.hpp"
 #include "hetplan/profile.hpp"
 #include "hetplan/stage_map.hpp"
 
@@ -166,6 +167,35 @@ int ref_map_stages(const char* cluster_json, int tp, int n_groupings, const int*
     return -6;
   } catch (...) {
     return -5;
+  }
+}
+
+// simulate_pipeline (P/src/pipeline_sim.cpp:46-149) on P stages x K
+// microbatches: makespan, busy[P], peak[P], and the events in the reference's
+// order as (stage, kind 0=F/1=B, microbatch) + (start, end).
+// Returns 0 ok, 5 on an invariant failure.
+int ref_simulate_pipeline(int P, int K, const double* fwd, const double* bwd, const double* sf,
+                          const double* sb, double* makespan, double* busy, int* peak,
+                          int* ev_int, double* ev_time) {
+  try {
+    std::vector<StageTiming> st(P);
+    for (int p = 0; p < P; ++p) st[p] = {fwd[p], bwd[p], sf[p], sb[p]};
+    const PipelineSimResult r = simulate_pipeline(st, K);
+    *makespan = r.makespan;
+    for (int p = 0; p < P; ++p) {
+      busy[p] = r.busy[p];
+      peak[p] = r.peak_in_flight[p];
+    }
+    for (size_t i = 0; i < r.events.size(); ++i) {
+      ev_int[3 * i] = r.events[i].stage;
+      ev_int[3 * i + 1] = r.events[i].kind == 'F' ? 0 : 1;
+      ev_int[3 * i + 2] = r.events[i].microbatch;
+      ev_time[2 * i] = r.events[i].start;
+      ev_time[2 * i + 1] = r.events[i].end;
+    }
+    return 0;
+  } catch (...) {
+    return 5;
   }
 }
 

@@ -56,6 +56,12 @@ class hp_plan_options(C.Structure):
     ]
 
 
+class hp_sim_options(C.Structure):
+    """c_api.h:105-109."""
+
+    _fields_ = [("combined_time", C.c_int), ("fb_ratio", C.c_double), ("zero_comm", C.c_int)]
+
+
 @dataclass
 class PlanOptions:
     tp_dims: Optional[Sequence[int]] = None
@@ -113,6 +119,23 @@ class HetplanLib:
         L.hp_profile_write_file.restype = C.c_int
         L.hp_plan_write_file.argtypes = [_VP, C.c_char_p]
         L.hp_plan_write_file.restype = C.c_int
+        # 1F1B simulation (c_api.h:105-120)
+        L.hp_sim_options_init.argtypes = [C.POINTER(hp_sim_options)]
+        L.hp_simulate.argtypes = [_VP, _VP, _VP, _VP, C.POINTER(hp_sim_options), C.POINTER(_VP)]
+        L.hp_simulate.restype = C.c_int
+        L.hp_sim_makespan.argtypes = [_VP]
+        L.hp_sim_makespan.restype = C.c_double
+        for name in ("hp_sim_result_to_json", "hp_sim_timeline_csv"):
+            getattr(L, name).argtypes = [_VP, C.POINTER(C.c_void_p)]
+            getattr(L, name).restype = C.c_int
+        L.hp_sim_result_free.argtypes = [_VP]
+        L.hp_sim_result_free.restype = None
+        if hasattr(L, "hp_simulate_batch"):  # product library only
+            L.hp_simulate_batch.argtypes = [C.c_int, C.POINTER(_VP), C.POINTER(_VP), _VP,
+                                            C.POINTER(_VP), C.POINTER(hp_sim_options),
+                                            C.POINTER(_VP)]
+            L.hp_simulate_batch.restype = C.c_int
+            L.hpk_last_error.restype = C.c_char_p
         # checkpoint / recovery (c_api.h:123-136): the reference's own engines
         L.hp_checkpoint_save.argtypes = [_VP, C.c_char_p, C.c_ulonglong, C.c_int, C.c_ulonglong,
                                          C.c_int]
@@ -265,6 +288,51 @@ class HetplanLib:
         js = C.c_void_p()
         self._check(self.lib.hp_recovery_to_json(h.ptr, C.byref(js)))
         return self._take_string(js)
+
+    def plan_load(self, path: str) -> "Handle":
+        h = _VP()
+        self._check(self.lib.hp_plan_load_file(path.encode(), C.byref(h)))
+        return Handle(self, h, "hp_plan_free")
+
+    def _sim_options(self, combined_time, fb_ratio, zero_comm):
+        o = hp_sim_options()
+        self.lib.hp_sim_options_init(C.byref(o))
+        o.combined_time = int(combined_time)
+        if fb_ratio is not None:
+            o.fb_ratio = fb_ratio
+        o.zero_comm = int(zero_comm)
+        return o
+
+    def _sim_outputs(self, h):
+        js, csv = C.c_void_p(), C.c_void_p()
+        self._check(self.lib.hp_sim_result_to_json(h, C.byref(js)))
+        self._check(self.lib.hp_sim_timeline_csv(h, C.byref(csv)))
+        out = (self._take_string(js), self._take_string(csv), self.lib.hp_sim_makespan(h))
+        self.lib.hp_sim_result_free(h)
+        return out
+
+    def simulate(self, plan, cluster, model, profile, combined_time=False, fb_ratio=None,
+                 zero_comm=False):
+        """hp_simulate + hp_sim_result_to_json + hp_sim_timeline_csv:
+        (json, csv, makespan)."""
+        o = self._sim_options(combined_time, fb_ratio, zero_comm)
+        h = _VP()
+        self._check(self.lib.hp_simulate(plan.ptr, cluster.ptr, model.ptr, profile.ptr,
+                                         C.byref(o), C.byref(h)))
+        return self._sim_outputs(h)
+
+    def simulate_batch(self, plans, clusters, model, profiles, combined_time=False,
+                       fb_ratio=None, zero_comm=False):
+        """hp_simulate_batch (product extension): every plan in one launch."""
+        n = len(plans)
+        o = self._sim_options(combined_time, fb_ratio, zero_comm)
+        out = (_VP * n)()
+        rc = self.lib.hp_simulate_batch(n, (_VP * n)(*[p.ptr for p in plans]),
+                                        (_VP * n)(*[c.ptr for c in clusters]), model.ptr,
+                                        (_VP * n)(*[p.ptr for p in profiles]), C.byref(o), out)
+        if rc != HP_OK:
+            raise HetplanError(rc, self.lib.hpk_last_error().decode())
+        return [self._sim_outputs(_VP(out[i])) for i in range(n)]
 
     def plan_json(self, cluster_text: str, model_text: str, max_layers: int,
                   options: Optional[PlanOptions] = None, base_seconds: float = 0.05) -> str:

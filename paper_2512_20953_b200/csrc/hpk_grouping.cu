@@ -40,6 +40,20 @@
 
 namespace cg = cooperative_groups;
 
+// wave-engine tuning (build-time; the defaults are the measured best)
+#ifndef HPK_SEG_CAP
+#define HPK_SEG_CAP 1024      // visits per segment run per wave
+#endif
+#ifndef HPK_WAVE_NS
+#define HPK_WAVE_NS 300000ull // run-phase time slice
+#endif
+#ifndef HPK_QMUL
+#define HPK_QMUL 4            // run slots per warp per wave
+#endif
+#ifndef HPK_QONE
+#define HPK_QONE 1.7          // one problem's share of run slots, x warps
+#endif
+
 #ifndef HPK_TRACE_LEVEL
 #define HPK_TRACE_LEVEL 0  // per-wave scheduler trace (debug builds only)
 #endif
@@ -55,7 +69,7 @@ constexpr uint8_t KIND_PREFIX = 1;
 // top_k of the wave engine (grouping.cpp:117-132 with top_k > 1): the state
 // the DFS carries between segments is the vector of the top_k best leaf
 // objectives above the prune floor; larger top_k run on the serial replica.
-constexpr int KW = 8;
+constexpr int KW = 16;
 
 // ------------------------------------------------------------------ layout
 
@@ -3042,7 +3056,9 @@ struct SerialProb {
   // outputs
   int status, count, optimal;
   long long visited;
-  double obj[HPK_MAX_TOPK], z[HPK_MAX_TOPK];
+  double* obj_out;   // device [top_k]
+  double* z_out;     // device [top_k]
+  SerialCand* cand;  // device [top_k + 1]: the best-first candidate list
   int* rgs_out;  // device [top_k * n]
 };
 
@@ -3079,7 +3095,8 @@ __global__ void hpk_serial_kernel(SerialProb* probs, int n_probs, SerialCand* ca
   int* rgs = gc + (max_n + 1);
   int* fr_G = rgs + (max_n + 1);
   int* fr_gi = fr_G + (max_n + 1);
-  SerialCand* best = cands + (size_t)pi * (HPK_MAX_TOPK + 1);
+  SerialCand* best = pb.cand;
+  (void)cands;
   int n_best = 0;
   const int top_k = pb.top_k < 1 ? 1 : pb.top_k;
 
@@ -3214,15 +3231,15 @@ __global__ void hpk_serial_kernel(SerialProb* probs, int n_probs, SerialCand* ca
     seed_rgs(pb, seed_ix, rgs);
     for (int i = 0; i < n; ++i) pb.rgs_out[i] = rgs[i];
     pb.count = 1;
-    pb.obj[0] = seed_obj;
-    pb.z[0] = seed_z;
+    pb.obj_out[0] = seed_obj;
+    pb.z_out[0] = seed_z;
     pb.optimal = 0;
     return;
   }
   pb.count = n_best;
   for (int k = 0; k < n_best; ++k) {
-    pb.obj[k] = best[k].obj;
-    pb.z[k] = best[k].z;
+    pb.obj_out[k] = best[k].obj;
+    pb.z_out[k] = best[k].z;
     for (int i = 0; i < n; ++i) pb.rgs_out[(size_t)k * n + i] = best[k].rgs[i];
   }
   pb.optimal = optimal ? 1 : 0;
@@ -3620,6 +3637,12 @@ double seed_floor(const hpk_grouping_problem& pr) {
 // Hooks shared with hpk_partition.cu (same thread-local error / timing).
 void hpkp_fail(const std::string& msg) { t_err = msg; }
 namespace hpk_timing_bridge {
+void add_pipeline(double ms, long long h2d, long long d2h) {
+  t_timing.pipeline_ms += ms;
+  t_timing.kernel_launches += 1;
+  t_timing.h2d_bytes += h2d;
+  t_timing.d2h_bytes += d2h;
+}
 void add_affinity(double ms, long long h2d, long long d2h) {
   t_timing.affinity_ms += ms;
   t_timing.kernel_launches += 1;
@@ -3837,7 +3860,6 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
     results[i].max_list = 0;
     results[i].exact_checks = 0;
     if (pr.n < 1) return fail(6, "grouping: no devices");
-    if (pr.top_k > HPK_MAX_TOPK) return fail(6, "hetplan_b200: top_k above 16 unsupported");
     const bool contract = exact_sums(pr.power, pr.n, 0, false) &&
                           exact_sums(pr.memory, pr.n, 0, false);
     const bool wave_ok = !cfg.force_serial && pr.n <= MAXN && pr.top_k <= KW && contract;
@@ -3966,7 +3988,7 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
   // ---------------- wave engine
   if (!wave_ix.empty()) {
     const int P = (int)wave_ix.size();
-    const long long seg_cap = cfg.segment_cap > 0 ? cfg.segment_cap : 1024;
+    const long long seg_cap = cfg.segment_cap > 0 ? cfg.segment_cap : HPK_SEG_CAP;
     // list capacity (ids) and entry-pool capacity per problem; large by default
     // (the list must hold the whole speculative frontier), scaled down so that
     // big batches (cfg5 sweeps) stay within ~4 GB of HBM.
@@ -4030,7 +4052,7 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
     // small: several per warp keep the warps busy through the time slice)
     // (4 per warp and a 300 us slice: measured best on cfg4 / cfg3 after the
     // parallel queue step; HPK_QMUL / HPK_WAVE_US override)
-    const int qmax = 4 * nwarps;
+    const int qmax = HPK_QMUL * nwarps;
     const int qcap = qmax + 33 * P + 64;
     if (int rc = grow(c.items, c.cap_items, (size_t)2 * qcap)) return rc;
 
@@ -4077,14 +4099,14 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
     kp.ranges = ranges;
     kp.eager = 0;
     // run-phase time slice: 300 us (HPK_WAVE_US overrides; 0 = none)
-    kp.wave_ns = 300000ull;
+    kp.wave_ns = HPK_WAVE_NS;
     kp.n_problems = P;
     kp.lcap = lcap;
     kp.pcap = pcap;
     kp.reserve = reserve;
     kp.qcap = qcap;
     kp.qmax = qmax;
-    kp.qmax_one = (int)(1.7 * nwarps);
+    kp.qmax_one = (int)(HPK_QONE * nwarps);
     kp.unit_share = 0;
     kp.seg_cap = seg_cap;
     kp.front_cap = seg_cap;
@@ -4225,8 +4247,8 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
     std::vector<double> hpw, hme;
     std::vector<int> htk, hnk;
     std::vector<size_t> off(P);
-    size_t rgs_total = 0;
-    std::vector<size_t> rgs_off(P);
+    size_t rgs_total = 0, k_total = 0;
+    std::vector<size_t> rgs_off(P), k_off(P);
     for (int k = 0; k < P; ++k) {
       const hpk_grouping_problem& pr = problems[serial_ix[k]];
       off[k] = hpw.size();
@@ -4236,7 +4258,10 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
       hnk.insert(hnk.end(), pr.node_key, pr.node_key + pr.n);
       rgs_off[k] = rgs_total;
       rgs_total += (size_t)std::max(1, pr.top_k) * pr.n;
+      k_off[k] = k_total;  // top_k results + (top_k + 1) list slots per problem
+      k_total += (size_t)std::max(1, pr.top_k);
     }
+    double *d_obj, *d_z;
     double *d_pw, *d_me, *d_scr;
     int *d_tk, *d_nk, *d_iscr, *d_rgs;
     SerialProb* d_probs;
@@ -4249,7 +4274,9 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
     HPK_CUDA(cudaMalloc(&d_iscr, sizeof(int) * (size_t)P * 4 * (max_n + 1)));
     HPK_CUDA(cudaMalloc(&d_rgs, sizeof(int) * rgs_total));
     HPK_CUDA(cudaMalloc(&d_probs, sizeof(SerialProb) * P));
-    HPK_CUDA(cudaMalloc(&d_cands, sizeof(SerialCand) * (size_t)P * (HPK_MAX_TOPK + 1)));
+    HPK_CUDA(cudaMalloc(&d_cands, sizeof(SerialCand) * (k_total + (size_t)P)));
+    HPK_CUDA(cudaMalloc(&d_obj, sizeof(double) * k_total));
+    HPK_CUDA(cudaMalloc(&d_z, sizeof(double) * k_total));
     std::vector<SerialProb> sp(P);
     for (int k = 0; k < P; ++k) {
       const hpk_grouping_problem& pr = problems[serial_ix[k]];
@@ -4265,6 +4292,9 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
       s.tkey = d_tk + off[k];
       s.nkey = d_nk + off[k];
       s.rgs_out = d_rgs + rgs_off[k];
+      s.obj_out = d_obj + k_off[k];
+      s.z_out = d_z + k_off[k];
+      s.cand = d_cands + k_off[k] + (size_t)k;
     }
     HPK_CUDA(cudaMemcpyAsync(d_pw, hpw.data(), sizeof(double) * tot_units,
                              cudaMemcpyHostToDevice, c.stream));
@@ -4287,6 +4317,11 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
     std::vector<int> hrgs(rgs_total);
     HPK_CUDA(cudaMemcpyAsync(hrgs.data(), d_rgs, sizeof(int) * rgs_total,
                              cudaMemcpyDeviceToHost, c.stream));
+    std::vector<double> hobj(k_total), hz(k_total);
+    HPK_CUDA(cudaMemcpyAsync(hobj.data(), d_obj, sizeof(double) * k_total,
+                             cudaMemcpyDeviceToHost, c.stream));
+    HPK_CUDA(cudaMemcpyAsync(hz.data(), d_z, sizeof(double) * k_total, cudaMemcpyDeviceToHost,
+                             c.stream));
     HPK_CUDA(cudaStreamSynchronize(c.stream));
     float ms = 0;
     cudaEventElapsedTime(&ms, c.ev0, c.ev1);
@@ -4302,8 +4337,8 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
       r.optimal = s.optimal;
       r.visited = s.visited;
       for (int t = 0; t < s.count; ++t) {
-        r.objective[t] = s.obj[t];
-        r.z[t] = s.z[t];
+        r.objective[t] = hobj[k_off[k] + t];
+        r.z[t] = hz[k_off[k] + t];
         for (int u = 0; u < pr.n; ++u) r.rgs[(size_t)t * pr.n + u] = hrgs[rgs_off[k] + t * pr.n + u];
       }
     }
@@ -4316,6 +4351,8 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
     cudaFree(d_rgs);
     cudaFree(d_probs);
     cudaFree(d_cands);
+    cudaFree(d_obj);
+    cudaFree(d_z);
   }
   return 0;
 }

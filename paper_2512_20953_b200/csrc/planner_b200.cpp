@@ -46,6 +46,13 @@
 
 namespace hetplan {
 
+// sim_b200.cpp: every group of every plan through the GPU 1F1B simulator
+std::vector<PlanSimResult> simulate_plans(const std::vector<const ParallelPlan*>& plans,
+                                          const std::vector<const ProfileTable*>& profiles,
+                                          const std::vector<const ModelConfig*>& cfgs,
+                                          const std::vector<const ClusterSpec*>& specs,
+                                          const SimOptions& options);
+
 namespace {
 
 // ---- R1-R3 and plan validation, restated (no reference code runs for them).
@@ -439,6 +446,7 @@ struct PlanJob {
   std::vector<std::vector<int>> tk, nk;
   std::vector<hpk_grouping_result> gres;
   std::vector<std::vector<int>> rgs_buf;
+  std::vector<std::vector<double>> obj_buf, z_buf;
   std::vector<Candidate> cands;
   std::vector<hpk_plan_candidate> pin;
   std::vector<int> pin_of;
@@ -563,9 +571,15 @@ void job_prepare(PlanJob& J) {
 
   J.gres.assign(problems.size(), hpk_grouping_result{});
   J.rgs_buf.assign(problems.size(), {});
+  J.obj_buf.assign(problems.size(), {});
+  J.z_buf.assign(problems.size(), {});
   for (size_t k = 0; k < problems.size(); ++k) {
     J.rgs_buf[k].assign((size_t)problems[k].top_k * problems[k].n, 0);
+    J.obj_buf[k].assign((size_t)problems[k].top_k, 0.0);
+    J.z_buf[k].assign((size_t)problems[k].top_k, 0.0);
     J.gres[k].rgs = J.rgs_buf[k].data();
+    J.gres[k].objective = J.obj_buf[k].data();
+    J.gres[k].z = J.z_buf[k].data();
   }
 }
 
@@ -718,7 +732,6 @@ void job_partition_inputs(PlanJob& J) {
 ParallelPlan job_select(PlanJob& J) {
   const ClusterSpec& spec = J.spec;
   const ModelConfig& cfg = J.cfg;
-  const ProfileTable& profile = J.profile;
   const PlannerOptions& options = J.options;
   auto& work = J.work;
   auto& cands = J.cands;
@@ -830,13 +843,46 @@ ParallelPlan job_select(PlanJob& J) {
     if (s.status == "candidate" && s.tp_dim == best->tp_dim) s.status = "selected";
   }
   best->candidates = summaries;
+  // validate_with_sim (planner.cpp:207-219) follows in plan_jobs: every job's
+  // selected plan is simulated in one GPU launch (sim_b200.cpp)
+  return *best;
+}
 
-  if (options.validate_with_sim) {  // planner.cpp:207-219 (reference simulator, host)
-    SimOptions sim_opts;
-    sim_opts.combined_time = true;
-    PlanSimResult sim = simulate_1f1b(*best, profile, cfg, spec, sim_opts);
+// planner.cpp:207-219 for every job that asked for it: one simulator launch
+// (combined_time, like the reference), then the reference's warnings per job.
+void validate_jobs_with_sim(std::vector<PlanJob*>& jobs) {
+  std::vector<PlanJob*> sel;
+  std::vector<const ParallelPlan*> plans;
+  std::vector<const ProfileTable*> profiles;
+  std::vector<const ModelConfig*> cfgs;
+  std::vector<const ClusterSpec*> specs;
+  for (PlanJob* J : jobs) {
+    if (J->error || !J->plan || !J->options.validate_with_sim) continue;
+    sel.push_back(J);
+    plans.push_back(&*J->plan);
+    profiles.push_back(&J->profile);
+    cfgs.push_back(&J->cfg);
+    specs.push_back(&J->spec);
+  }
+  if (sel.empty()) return;
+  SimOptions sim_opts;
+  sim_opts.combined_time = true;
+  std::vector<PlanSimResult> sims;
+  try {
+    sims = simulate_plans(plans, profiles, cfgs, specs, sim_opts);
+  } catch (...) {
+    // the reference raises from inside plan_cluster: the job fails
+    for (PlanJob* J : sel) {
+      J->plan.reset();
+      J->error = std::current_exception();
+    }
+    return;
+  }
+  for (size_t k = 0; k < sel.size(); ++k) {
+    const ParallelPlan& best = *sel[k]->plan;
+    const PlanSimResult& sim = sims[k];
     for (size_t j = 0; j < sim.groups.size(); ++j) {
-      const double estimated = best->cost.per_group[j].total;
+      const double estimated = best.cost.per_group[j].total;
       const double simulated = sim.groups[j].pipeline.makespan;
       if (estimated > 0 && std::abs(simulated - estimated) / estimated > 0.01) {
         std::cerr << "warning: group " << j << " simulated makespan " << simulated
@@ -844,7 +890,6 @@ ParallelPlan job_select(PlanJob& J) {
       }
     }
   }
-  return *best;
 }
 
 // Runs fn(job) for every unfinished job on up to `threads` host threads; an
@@ -999,6 +1044,8 @@ void plan_jobs(std::vector<PlanJob*>& jobs, int threads) {
   clk.lap("partition");
   for_jobs(jobs, threads, [](PlanJob& J) { J.plan = job_select(J); });
   clk.lap("select");
+  validate_jobs_with_sim(jobs);
+  clk.lap("validate-sim");
 }
 
 }  // namespace

@@ -42,8 +42,8 @@ class hpk_grouping_result(C.Structure):
         ("optimal", C.c_int),
         ("engine", C.c_int),
         ("visited", C.c_longlong),
-        ("objective", C.c_double * HPK_MAX_TOPK),
-        ("z", C.c_double * HPK_MAX_TOPK),
+        ("objective", C.POINTER(C.c_double)),
+        ("z", C.POINTER(C.c_double)),
         ("rgs", C.POINTER(C.c_int)),
         ("waves", C.c_int),
         ("segment_runs", C.c_longlong),
@@ -77,6 +77,7 @@ class hpk_timing(C.Structure):
         ("kernel_launches", C.c_int),
         ("devices_used", C.c_int),
         ("affinity_ms", C.c_double),
+        ("pipeline_ms", C.c_double),
     ]
 
 
@@ -114,6 +115,17 @@ class hpk_affinity_problem(C.Structure):
         ("group_off", C.POINTER(C.c_int)), ("slot_type", C.POINTER(C.c_int)),
         ("slot_node", C.POINTER(C.c_int)), ("slot_perm", C.POINTER(C.c_int)),
         ("swaps", C.c_int),
+    ]
+
+
+class hpk_pipeline(C.Structure):
+    _fields_ = [
+        ("n_stages", C.c_int), ("n_microbatches", C.c_int),
+        ("forward", C.POINTER(C.c_double)), ("backward", C.POINTER(C.c_double)),
+        ("send_forward", C.POINTER(C.c_double)), ("send_backward", C.POINTER(C.c_double)),
+        ("makespan", C.c_double), ("busy", C.POINTER(C.c_double)),
+        ("peak_in_flight", C.POINTER(C.c_int)), ("task_start", C.POINTER(C.c_double)),
+        ("task_end", C.POINTER(C.c_double)),
     ]
 
 
@@ -222,6 +234,8 @@ class Engine:
         L.hpk_partition_cost_ex.argtypes = [C.POINTER(hpk_plan_candidate), C.c_int,
                                             C.POINTER(hpk_plan_result), C.c_int, C.c_int]
         L.hpk_partition_cost_ex.restype = C.c_int
+        L.hpk_pipeline_sim.argtypes = [C.POINTER(hpk_pipeline), C.c_int, C.c_int]
+        L.hpk_pipeline_sim.restype = C.c_int
         L.hpk_stage_affinity.argtypes = [C.POINTER(hpk_affinity_problem), C.c_int, C.c_int]
         L.hpk_stage_affinity.restype = C.c_int
         L.hpk_last_timing.argtypes = [C.POINTER(hpk_timing)]
@@ -256,10 +270,14 @@ class Engine:
             tk = (C.c_int * m)(*(pb.type_key if pb.type_key is not None else [0] * m))
             nk = (C.c_int * m)(*(pb.node_key if pb.node_key is not None else list(range(m))))
             rg = (C.c_int * (max(1, pb.top_k) * m))()
-            keep += [pw, me, tk, nk, rg]
+            ob = (C.c_double * max(1, pb.top_k))()
+            zz = (C.c_double * max(1, pb.top_k))()
+            keep += [pw, me, tk, nk, rg, ob, zz]
             arr[i] = hpk_grouping_problem(m, pb.n_microbatches, pb.min_mem, pb.exact_threshold,
                                           pb.node_budget, pb.top_k, pw, me, tk, nk)
             res[i].rgs = rg
+            res[i].objective = ob
+            res[i].z = zz
         cfg = hpk_search_config()
         self.lib.hpk_search_config_init(C.byref(cfg))
         cfg.device = device
@@ -359,3 +377,25 @@ class Engine:
         if rc != 0:
             raise EngineError(rc, self.lib.hpk_last_error().decode())
         return [(list(perms[i]), arr[i].swaps) for i in range(n)]
+
+    def pipeline_sim(self, pipes, *, device: int = -1):
+        """hpk_pipeline_sim: pipes = [(K, [(fwd, bwd, send_f, send_b) per stage])].
+        Returns [(makespan, busy, peak, starts, ends)] with each stage's tasks in
+        its static 1F1B order (stage-major)."""
+        n = len(pipes)
+        arr = (hpk_pipeline * n)()
+        keep, outs = [], []
+        for i, (K, stages) in enumerate(pipes):
+            P = len(stages)
+            cols = [(C.c_double * P)(*[s[j] for s in stages]) for j in range(4)]
+            o = [(C.c_double * P)(), (C.c_int * P)(), (C.c_double * (2 * P * K))(),
+                 (C.c_double * (2 * P * K))()]
+            keep += cols
+            outs.append(o)
+            arr[i] = hpk_pipeline(P, K, cols[0], cols[1], cols[2], cols[3], 0.0, o[0], o[1],
+                                  o[2], o[3])
+        rc = self.lib.hpk_pipeline_sim(arr, n, device)
+        if rc != 0:
+            raise EngineError(rc, self.lib.hpk_last_error().decode())
+        return [(arr[i].makespan, list(outs[i][0]), list(outs[i][1]), list(outs[i][2]),
+                 list(outs[i][3])) for i in range(n)]

@@ -65,7 +65,7 @@ def test_wave_engine_top_k_random_batch(engine, oracle, cap):
     (grouping.cpp:117-132); every returned candidate, visits and the optimal
     flag match the oracle."""
     probs = _random_problems(1000 + cap, 160, nmax=10 if cap < 16 else 11,
-                             top_ks=(2, 3, 4, 8))
+                             top_ks=(2, 3, 4, 8, 13, 16))
     res = engine.grouping_search(probs, segment_cap=cap, max_seconds=60)
     bad = []
     for pb, r in zip(probs, res):
@@ -78,7 +78,8 @@ def test_wave_engine_top_k_random_batch(engine, oracle, cap):
     assert not bad, bad[:2]
 
 
-@pytest.mark.parametrize("name,k", [("cfg2", 2), ("cfg3", 3), ("cfg4", 2), ("cfg4", 8)])
+@pytest.mark.parametrize("name,k", [("cfg2", 2), ("cfg3", 3), ("cfg4", 2), ("cfg4", 8),
+                                    ("cfg2", 12), ("cfg3", 16)])
 def test_configs_top_k_every_tp_dimension(engine, oracle, name, k):
     w = configs.get(name)
     g = 0
@@ -148,11 +149,15 @@ def test_non_dyadic_and_large_top_k_take_the_serial_engine(engine, oracle):
     nd = GroupingProblem([1.0, 1.0, 2.0, 0.7, 1.3], [8.0, 8.0, 8.0, 9.0, 7.0], 8, 6.0,
                          [0, 0, 1, 2, 3], [0, 0, 1, 2, 3], top_k=3)
     big = GroupingProblem([1.0, 1.0, 2.0, 0.5, 1.5, 2.0], [8.0, 8.0, 8.0, 9.0, 7.0, 4.0], 8, 6.0,
-                          [0, 0, 1, 2, 3, 1], [0, 0, 1, 2, 3, 3], top_k=12)
+                          [0, 0, 1, 2, 3, 1], [0, 0, 1, 2, 3, 3], top_k=20)
+    mid = GroupingProblem(big.power, big.memory, 8, 6.0, big.type_key, big.node_key, top_k=12)
     small = GroupingProblem(big.power, big.memory, 8, 6.0, big.type_key, big.node_key, top_k=3)
-    res = engine.grouping_search([nd, big, small])
-    assert [r.engine for r in res] == [1, 1, 0]
-    for pb, r in zip([nd, big, small], res):
+    # top_k <= 16 runs on the wave engine; larger top_k (beyond the old limit,
+    # the reference accepts any) on the serial replica with a top_k-long list
+    res = engine.grouping_search([nd, big, mid, small])
+    assert [r.engine for r in res] == [1, 1, 0, 0]
+    assert res[1].count > 16
+    for pb, r in zip([nd, big, mid, small], res):
         o = oracle.solve_grouping(pb.power, pb.memory, 8, 6.0, pb.type_key, pb.node_key,
                                   top_k=pb.top_k)
         assert _same(r, o)

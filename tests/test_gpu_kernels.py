@@ -261,3 +261,14 @@ def test_gpu_stage_time_ascending_bits(engine):
     c = PlanCandidate(n_layers=7, tp=1, k_total=1, groups=[[(0, 1, 1e300, 0, 0)]],
                       microbatches=[1], prof=[row], ppb=0.0, pab=0.0, opt_mult=0.0)
     assert engine.partition_cost([c])[0].stage_time[0] == (0.1 + 0.7) + 5.0
+
+
+@pytest.mark.parametrize("name,k", [("cfg1", 20), ("cfg2", 12), ("cfg3", 16), ("cfg1", 40)])
+def test_large_top_k_plans_match_reference(product_lib, ref_lib, name, k):
+    """top_k up to 16 on the wave engine, larger on the serial replica (the
+    reference accepts any top_k; round 1 rejected > 16): whole plans equal."""
+    w = configs.get(name)
+    opts = PlanOptions(top_k=k)
+    got = product_lib.plan_json(w.cluster_json(), w.model_json(), w.max_layers, opts)
+    want = ref_lib.plan_json(w.cluster_json(), w.model_json(), w.max_layers, opts)
+    assert got == want
