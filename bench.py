@@ -8,8 +8,10 @@ one full default-option plan search of the workload through the product's
 public C ABI, hp_plan_compute (grouping search, stage mapping, layer partition,
 cost, selection), with host buffers.
 
-  e2e    the headline: candidates / wall time of hp_plan_compute + plan JSON
-         (host<->device copies and every host phase inside the timed region)
+  e2e    the headline: candidates / wall time of hp_plan_compute, the same
+         call the reference arm times (host<->device copies, the device->host
+         read of every kernel's results and every host phase inside the timed
+         region)
   value  the same calls, device time only: the kernels' CUDA-event durations
          on their launching streams (grouping search = max over GPUs, + stage
          affinity + partition/cost), i.e. throughput with inputs resident
@@ -183,7 +185,7 @@ def run_reference(args):
     from paper_2512_20953_b200 import configs
     st = stats()
     if args.workload == "cfg5":
-        sample = min(64, max(2 * (os.cpu_count() or 1), 16))
+        sample = min(256, max(8 * (os.cpu_count() or 1), 32))
         rates = [ref_cfg5_rate(sample) for _ in range(max(1, args.steps // 5))]
         value = statistics.mean(r[0] for r in rates)
         cores = rates[0][2]
@@ -262,8 +264,7 @@ def time_plans(prod, w, steps, warmup, flush):
         _flush(flush)
         prod.eng.reset_timing()
         t0 = time.perf_counter()
-        plan = lib.plan_compute(cl, md, pr)
-        lib.plan_to_json(plan)
+        plan = lib.plan_compute(cl, md, pr)  # the plan (device results read back) is on the host
         dt = time.perf_counter() - t0
         plan.close()
         ms, t = prod.device_ms()
@@ -455,7 +456,7 @@ def secondary_workloads(prod, flush, st, args):
            "visits": v, "e2e_ms": statistics.mean(wall), "device_ms": statistics.mean(dev),
            "e2e_candidates_per_s": v / (statistics.mean(wall) * 1e-3)}
     if not args.no_cpu:
-        sample = min(64, max(2 * (os.cpu_count() or 1), 16))
+        sample = min(256, max(8 * (os.cpu_count() or 1), 32))
         rate, dt, cores = ref_cfg5_rate(sample)
         rec["reference"] = {"candidates_per_s": rate, "cores": cores,
                             "projected_sweep_s": v / rate,

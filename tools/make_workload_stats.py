@@ -36,12 +36,14 @@ if __name__ == "__main__":
     out = {name: plan_stats(o, configs.get(name)) for name in ("cfg1", "cfg2", "cfg3", "cfg4")}
     with open(os.path.join(ROOT, "tests", "golden", "cfg5_search.json")) as f:
         golden = json.load(f)
-    snaps = configs.cfg5_snapshots(64)
-    sample = [plan_stats(o, w) for w in snaps]
-    sv = sum(s["visits"] for s in sample[:16])
-    so = sum(s["model_ops"] for s in sample[:16])
-    out["cfg5"] = {"snapshots": 1000, "visits": sum(r.get("visited", 0) for r in golden),
-                   "model_ops_per_visit": so / sv, "sample_visits": [s["visits"] for s in sample],
+    sample = [plan_stats(o, w) for w in configs.cfg5_snapshots(16)]
+    sv = sum(s["visits"] for s in sample)
+    so = sum(s["model_ops"] for s in sample)
+    per_snap = [0] * 1000
+    for r in golden:
+        per_snap[r["snapshot"]] += r.get("visited", 0)
+    out["cfg5"] = {"snapshots": 1000, "visits": sum(per_snap),
+                   "model_ops_per_visit": so / sv, "sample_visits": per_snap,
                    "source": "visits: tests/golden/cfg5_search.json (reference probe); "
                              "ops per visit: oracle instrumentation on snapshots 0..15"}
     with open(os.path.join(ROOT, "profiles", "workload_stats.json"), "w") as f:
