@@ -137,7 +137,7 @@ void hp_recovery_free(hp_recovery* recovery);                         /* c_api.h
 /* ------------------------------------------------------------------ *
  * B200 kernel C-ABI (new)                                              *
  * ------------------------------------------------------------------ */
-#define HPK_MAX_UNITS 64 /* wave engine; larger problems use the serial replica */
+#define HPK_MAX_UNITS 128 /* wave engine (<= 64 groups per node); larger: serial replica */
 #define HPK_MAX_TOPK 16 /* wave engine (larger top_k: serial replica) */
 #ifndef HPK_HOST_TRACE
 #define HPK_HOST_TRACE 0 /* build with -DHPK_HOST_TRACE=1 for per-phase host timings */

@@ -60,7 +60,7 @@ namespace cg = cooperative_groups;
 
 namespace hpk {
 
-constexpr int MAXN = HPK_MAX_UNITS;  // 64 units -> lanes own groups g and g+32
+constexpr int MAXN = HPK_MAX_UNITS;  // 128 units; lanes own groups g and g+32 (G <= 64)
 constexpr int WARPS_PER_BLOCK = 8;
 constexpr int BLOCK_THREADS = WARPS_PER_BLOCK * 32;
 constexpr int TILE = BLOCK_THREADS * 8;  // list positions per expansion / commit tile
@@ -516,6 +516,8 @@ struct RunOut {
   int dstop;   // unfinished: the stop node is path[0..dstop-1) + [stop_c]
   int exact;   // child checks resolved by the exact serial check
   int stop_c;
+  bool overflow;  // reached an internal node with more than 63 groups (lanes own
+                  // groups g, g+32): the problem goes to the serial replica
 };
 
 // DFS of subtree(E.u) in preorder (PREFIX: stopping before E.end), cap visits.
@@ -575,6 +577,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
   o.dstop = 0;
   o.stop_c = 0;
   o.exact = 0;
+  o.overflow = false;
   if (TOPK && lane == 0) sm->rn = 0;
   if (cap <= 0) {  // budget already exhausted: the reference aborts before entering u
     if (TOPK && lane == 0) rec->n = 0;
@@ -608,6 +611,11 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
   int d = dtop;
   double cut = C;
   double Sd, Dd;
+  if (!single && G > 63) {  // the range's parent has 64 groups (65 children)
+    o.overflow = true;
+    o.finished = true;
+    goto done;
+  }
   if (single) {  // enter the segment root u
     const int i = du - 1;
     const int grp = sm->path[i];
@@ -616,6 +624,11 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
     if (lane == 0) sm->lvl[du] = (unsigned)G << 16;
     o.visits = 1;
     __syncwarp();
+    if (d < n && G > 63) {  // its children would need group slot 64
+      o.overflow = true;
+      o.finished = true;
+      goto done;
+    }
     if (d == n) {  // the root is a leaf (grouping.cpp:138-149)
       bool infeas = false;
       double z = INFINITY;
@@ -1012,6 +1025,11 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
       if (c == G) ++G;
       if (match == d && c == ec) match = d + 1;
       ++d;
+      if (G > 63 && d < n) {  // an internal node with 64 groups: 65 children
+        o.overflow = true;
+        o.finished = true;
+        break;
+      }
       Sd = Sn;
       Dd = Dn;
       c = 0;
@@ -2950,6 +2968,7 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
         atomicAdd((unsigned long long*)&S.runs, 1ull);
         atomicAdd((unsigned long long*)&S.run_visits, (unsigned long long)o.visits);
         if (o.exact) atomicAdd((unsigned long long*)&S.exact_checks, (unsigned long long)o.exact);
+        if (o.overflow) atomicOr(&S.error, 8);  // > 63 groups: the serial replica redoes it
       }
       __syncwarp();
     }
@@ -4165,6 +4184,10 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
       r.max_list = s.max_list;
       r.exact_checks = s.exact_checks;
       r.visited = s.V;
+      if (s.error & 8) {  // a run met more than 63 groups: exact serial replay instead
+        serial_ix.push_back(i);
+        continue;
+      }
       if (!s.done)
         return fail(5, "hetplan_b200: wave engine did not converge within " +
                            std::to_string(kp.max_waves) + " waves (problem " +

@@ -12,7 +12,7 @@ import os
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
-HPK_MAX_UNITS = 64
+HPK_MAX_UNITS = 128
 HPK_MAX_TOPK = 16
 HPK_ALL_DEVICES = -2
 

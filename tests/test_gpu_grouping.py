@@ -232,3 +232,40 @@ def test_enumeration_engine_top_k(engine, oracle):
         assert (r.status, r.count, r.rgs, r.objective, r.z, r.optimal) == \
             (0, o.count, o.rgs, o.objective, o.z, o.optimal), pb
     assert 2 in engines
+
+
+def test_wave_engine_up_to_128_units(engine, oracle):
+    """65..128 TP units run on the wave engine (lanes own groups g and g+32, so a
+    node may hold up to 64 groups); budgeted searches over such clusters match
+    the oracle exactly (visits, optimal flag, winner)."""
+    import random
+    rng = random.Random(72)
+    probs = []
+    for n in (65, 72, 96, 128, 72, 80):
+        P = [rng.choice([1.0, 1.5, 2.0]) for _ in range(n)]
+        M = [rng.choice([40e9, 80e9, 100e9]) for _ in range(n)]
+        T = [int(p * 2) for p in P]
+        N = [i // 8 for i in range(n)]
+        MIN = sum(M) / rng.choice([3, 6, 12])
+        probs.append(GroupingProblem(P, M, rng.choice([16, 64]), MIN, T, N,
+                                     node_budget=rng.choice([20000, 300000])))
+    res = engine.grouping_search(probs, max_seconds=120)
+    for pb, r in zip(probs, res):
+        o = oracle.solve_grouping(pb.power, pb.memory, pb.n_microbatches, pb.min_mem,
+                                  pb.type_key, pb.node_key, pb.exact_threshold, pb.node_budget)
+        assert r.engine == 0, pb.n
+        assert _same(r, o), (pb.n, r.visited, o.visited)
+
+
+def test_more_than_63_groups_falls_back_exactly(engine, oracle):
+    """K = 1 and equal powers: every merge is pruned by the singletons seed, so
+    the DFS walks straight down opening a new group per unit and reaches an
+    internal node with 64 groups (65 children) — beyond the lanes' slots. The
+    wave engine hands such a problem to the serial replica; the result stays
+    the reference's."""
+    n = 70
+    pb = GroupingProblem([1.0] * n, [8.0] * n, 1, 1.0, [0] * n, list(range(n)))
+    r = engine.grouping_search([pb], max_seconds=120)[0]
+    o = oracle.solve_grouping(pb.power, pb.memory, 1, 1.0, pb.type_key, pb.node_key)
+    assert r.engine == 1
+    assert _same(r, o)

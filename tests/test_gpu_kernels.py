@@ -272,3 +272,16 @@ def test_large_top_k_plans_match_reference(product_lib, ref_lib, name, k):
     got = product_lib.plan_json(w.cluster_json(), w.model_json(), w.max_layers, opts)
     want = ref_lib.plan_json(w.cluster_json(), w.model_json(), w.max_layers, opts)
     assert got == want
+
+
+@pytest.mark.parametrize("nodes", [[(8, "A100")] * 3 + [(8, "H800")] * 3 + [(8, "H20")] * 3,
+                                   [(8, "A100")] * 6 + [(8, "H800")] * 4 + [(8, "H20")] * 2])
+def test_more_than_64_gpu_plans_match_reference(product_lib, ref_lib, nodes):
+    """72- and 96-GPU clusters: tp = 1 has more than 64 TP units (the wave
+    engine's old limit); the whole plan equals the reference's."""
+    from paper_2512_20953_b200.configs import _cluster, _model
+    cl = json.dumps(_cluster(TYPES, nodes))
+    md = json.dumps(_model(96, 3.6e9, 8.6e8, 64))
+    got = product_lib.plan_json(cl, md, 64)
+    want = ref_lib.plan_json(cl, md, 64)
+    assert got == want
