@@ -84,6 +84,9 @@ struct GProb {
   double RM[MAXN + 1];  // remaining_mem from d, serial as grouping.cpp:156-160
   double mb_abs;        // absolute error bound of the approximate bound sums
   double md_abs;        // same for the deficit sums (0 when they are exact integers)
+  int check_drift;      // 1: sums outside the exact-sum contract; every += is checked
+                        // for drift (fl(fl(x+p)-p) != x), which sends the problem to
+                        // the serial replica
 };
 
 // A segment of the ordered DFS list, stored in a per-problem entry pool; the
@@ -346,7 +349,7 @@ struct PView {
   const double* f;
   const double* R;
   const double* RM;
-  int n, exact_mem;
+  int n, exact_mem, check_drift;
   double min_mem, mb_abs, md_abs;
 };
 
@@ -379,6 +382,7 @@ __device__ __forceinline__ PView stage_problem(const GProb& G, WarpSmem* sm, int
   v.min_mem = G.min_mem;
   v.mb_abs = G.mb_abs;
   v.md_abs = G.md_abs;
+  v.check_drift = G.check_drift;
   return v;
 }
 
@@ -395,6 +399,7 @@ constexpr double kEps52 = 2.220446049250313e-16;  // 2^-52
 struct Groups {
   double gp[2], gm[2], f0[2], f1[2];
   int gc[2];
+  bool drift;  // check_drift: a += on this lane's groups would not round-trip
 };
 
 __device__ __forceinline__ void add_unit(const PView& P, Groups& g, int lane, int grp, double up,
@@ -402,6 +407,12 @@ __device__ __forceinline__ void add_unit(const PView& P, Groups& g, int lane, in
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     const bool o = grp == lane + 32 * k;
+    if (P.check_drift && o && g.gc[k] > 0) {
+      // the reference's -= after this += must give back the same sum
+      // (grouping.cpp:184-198); a new group (push_back) cannot drift
+      const double yp = g.gp[k] + up, ym = g.gm[k] + um;
+      g.drift = g.drift || (yp - up) != g.gp[k] || (ym - um) != g.gm[k];
+    }
     g.gp[k] += o ? up : 0.0;
     g.gm[k] += o ? um : 0.0;
     g.gc[k] += o ? 1 : 0;
@@ -426,6 +437,7 @@ __device__ __forceinline__ void remove_unit(const PView& P, Groups& g, int lane,
 }
 
 __device__ __forceinline__ void groups_init(const PView& P, Groups& g) {
+  g.drift = false;
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     g.gp[k] = 0;
@@ -518,6 +530,7 @@ struct RunOut {
   int stop_c;
   bool overflow;  // reached an internal node with more than 63 groups (lanes own
                   // groups g, g+32): the problem goes to the serial replica
+  bool drift;     // check_drift problems: some group sum would not round-trip
 };
 
 // DFS of subtree(E.u) in preorder (PREFIX: stopping before E.end), cap visits.
@@ -578,6 +591,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
   o.stop_c = 0;
   o.exact = 0;
   o.overflow = false;
+  o.drift = false;
   if (TOPK && lane == 0) sm->rn = 0;
   if (cap <= 0) {  // budget already exhausted: the reference aborts before entering u
     if (TOPK && lane == 0) rec->n = 0;
@@ -764,6 +778,15 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
           const unsigned long long x0 = lane == i1 ? ~0ull : eb0;
           const unsigned long long x1 = lane + 32 == i1 ? ~0ull : eb1;
           const double m2 = __longlong_as_double((long long)warp_min_u64(x0 < x1 ? x0 : x1));
+          if (P.check_drift) {  // every visited leaf child does += / -= on its group
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const int ch = lane + 32 * k;
+              if (ch >= c0 && ch < c0 + count && ch < G &&
+                  (((g.gp[k] + up) - up) != g.gp[k] || ((g.gm[k] + um) - um) != g.gm[k]))
+                g.drift = true;
+            }
+          }
           // each lane evaluates the children it owns (c = lane, lane+32)
           double obj_s[2];
           int gc_s[2];
@@ -949,6 +972,12 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
           lD[k] = (Dd - def_old) + def_new;
           const double A = lS[k] + Rn;
           const bool valid = ci <= (d == dtop && hil < G ? hil : G);
+          // every visited child, pruned or entered, does += / -= on its group
+          // (grouping.cpp:178-199): a round trip that does not restore the sum
+          // makes the reference's later sums path dependent
+          if (P.check_drift && valid && ci < G &&
+              (((g.gp[k] + up) - up) != g.gp[k] || ((g.gm[k] + um) - um) != g.gm[k]))
+            g.drift = true;
           pr[k] = !valid || (hc && A + mb < cut) || (lD[k] - md > RMn);
           ps[k] = !pr[k] && (!hc || A - mb >= cut) && (lD[k] + md <= RMn);
         }
@@ -1043,6 +1072,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
   }
 done:
   __syncwarp();
+  o.drift = __any_sync(HPK_FULL_MASK, g.drift);
   if (TOPK) {
     const int rn = sm->rn;
     o.has_best = rn > 0;
@@ -2695,6 +2725,7 @@ __device__ void init_problem(const KParams& kp, int p) {
     // quantities <= 2x the total power) plus the reference's own serial sum
     // (<= n roundings): (8n + 64) ulps of the largest magnitude, doubled.
     P.mb_abs = (double)(8 * n + 64) * kEps52 * 2.0 * (P.R[0] > 0 ? P.R[0] : 1.0);
+    if (P.check_drift) P.mb_abs *= 4.0;  // inexact unit sums: a wider filter margin
     if (P.exact_mem) {
       P.md_abs = 0.0;
     } else {
@@ -2969,6 +3000,7 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
         atomicAdd((unsigned long long*)&S.run_visits, (unsigned long long)o.visits);
         if (o.exact) atomicAdd((unsigned long long*)&S.exact_checks, (unsigned long long)o.exact);
         if (o.overflow) atomicOr(&S.error, 8);  // > 63 groups: the serial replica redoes it
+        if (o.drift) atomicOr(&S.error, 16);    // path-dependent sums: the serial replica
       }
       __syncwarp();
     }
@@ -3881,8 +3913,10 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
     if (pr.n < 1) return fail(6, "grouping: no devices");
     const bool contract = exact_sums(pr.power, pr.n, 0, false) &&
                           exact_sums(pr.memory, pr.n, 0, false);
-    const bool wave_ok = !cfg.force_serial && pr.n <= MAXN && pr.top_k <= KW && contract;
-    const bool enum_ok = wave_ok && cfg.enumerate && pr.n <= pr.exact_threshold &&
+    // outside the exact-sum contract the wave engine still runs, checking every
+    // += for drift; the enumeration engine (fresh sums only) needs the contract
+    const bool wave_ok = !cfg.force_serial && pr.n <= MAXN && pr.top_k <= KW;
+    const bool enum_ok = wave_ok && contract && cfg.enumerate && pr.n <= pr.exact_threshold &&
                          pr.n <= ENUM_MAXN;
     (enum_ok ? enum_ix : wave_ok ? wave_ix : serial_ix).push_back(i);
   }
@@ -4042,6 +4076,8 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
       g.min_mem = pr.min_mem;
       g.top_k = std::max(1, pr.top_k);
       g.exact_mem = exact_sums(pr.memory, pr.n, pr.min_mem, true) ? 1 : 0;
+      g.check_drift = exact_sums(pr.power, pr.n, 0, false) && exact_sums(pr.memory, pr.n, 0, false)
+                          ? 0 : 1;
       for (int i = 0; i < pr.n; ++i) {
         g.p[i] = pr.power[i];
         g.m[i] = pr.memory[i];
@@ -4184,7 +4220,7 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
       r.max_list = s.max_list;
       r.exact_checks = s.exact_checks;
       r.visited = s.V;
-      if (s.error & 8) {  // a run met more than 63 groups: exact serial replay instead
+      if (s.error & (8 | 16)) {  // > 63 groups, or drifting sums: exact serial replay
         serial_ix.push_back(i);
         continue;
       }

@@ -17,7 +17,8 @@ prod = HetplanLib(LIB_PATH)
 ref = HetplanLib(REF_LIB)
 names = sys.argv[1:] or ["cfg2", "cfg3", "cfg4"]
 variants = [("default", PlanOptions()), ("top_k=2", PlanOptions(top_k=2)),
-            ("top_k=4", PlanOptions(top_k=4)), ("derive_power", PlanOptions(derive_power=True))]
+            ("top_k=4", PlanOptions(top_k=4)), ("top_k=12", PlanOptions(top_k=12)),
+            ("derive_power", PlanOptions(derive_power=True))]
 
 
 def timed(lib, w, o, reps):
