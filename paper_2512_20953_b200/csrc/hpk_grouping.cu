@@ -60,7 +60,16 @@ namespace cg = cooperative_groups;
 
 namespace hpk {
 
-constexpr int MAXN = HPK_MAX_UNITS;  // 128 units; lanes own groups g and g+32 (G <= 64)
+// Units per problem of this build's wave engine. The library links two builds
+// of this file: the primary one (64 units: lanes own groups g and g+32) and
+// hpk_grouping_wide.cu (128 units, same lane layout, so a node may hold at
+// most 64 groups — more hands the problem to the serial replica). Problems
+// with 65..128 units go to the wide build; the primary build's smaller
+// per-entry paths keep the common case's list traffic low.
+#ifndef HPK_MAXN
+#define HPK_MAXN 64
+#endif
+constexpr int MAXN = HPK_MAXN;
 constexpr int WARPS_PER_BLOCK = 8;
 constexpr int BLOCK_THREADS = WARPS_PER_BLOCK * 32;
 constexpr int TILE = BLOCK_THREADS * 8;  // list positions per expansion / commit tile
@@ -69,7 +78,10 @@ constexpr uint8_t KIND_PREFIX = 1;
 // top_k of the wave engine (grouping.cpp:117-132 with top_k > 1): the state
 // the DFS carries between segments is the vector of the top_k best leaf
 // objectives above the prune floor; larger top_k run on the serial replica.
-constexpr int KW = 16;
+#ifndef HPK_KW
+#define HPK_KW 16
+#endif
+constexpr int KW = HPK_KW;
 
 // ------------------------------------------------------------------ layout
 
@@ -210,11 +222,9 @@ struct KParams {
   unsigned long long wave_ns;  // run-phase time slice (0: none): later runs stop and split
   int runners;        // warps per CTA that run segments (experiment knob; default all)
   int ranges;         // split pieces are sibling ranges (1) or single siblings (0)
-  int eager;          // eager split of a stop subtree with >= this many units left (0: off)
   int n_problems;
   int lcap, pcap, qcap, qmax, reserve;
   int qmax_one;       // cap of one problem's share (a lone search floods its list past it)
-  int unit_share;     // 1: a problem's share of run slots is proportional to its units
   long long seg_cap;
   int ramp;           // first-wave visit cap, doubled every wave up to seg_cap (0: off)
   long long front_cap;  // visit cap of the list head's run (the time slice stops it)
@@ -402,12 +412,13 @@ struct Groups {
   bool drift;  // check_drift: a += on this lane's groups would not round-trip
 };
 
+template <bool DRIFT>
 __device__ __forceinline__ void add_unit(const PView& P, Groups& g, int lane, int grp, double up,
                                          double um) {
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     const bool o = grp == lane + 32 * k;
-    if (P.check_drift && o && g.gc[k] > 0) {
+    if (DRIFT && o && g.gc[k] > 0) {
       // the reference's -= after this += must give back the same sum
       // (grouping.cpp:184-198); a new group (push_back) cannot drift
       const double yp = g.gp[k] + up, ym = g.gm[k] + um;
@@ -552,7 +563,7 @@ struct RunOut {
 // state loaded by the caller; cut = its cutoff) — a feasible leaf above the
 // cutoff joins it — and the run keeps its own top_k candidates in sm->r*,
 // written to rec at the end (grouping.cpp:117-132).
-template <bool TOPK>
+template <bool TOPK, bool DRIFT>
 __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, double C,
                               long long cap, WarpSmem* sm, int lane, int* err,
                               unsigned long long deadline, unsigned long long* prof,
@@ -609,7 +620,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
   if (lane == 0) sm->lvl[0] = 0;
   for (int i = 0; i + 1 < du; ++i) {  // the range's parent node: units 0..du-2
     const int grp = sm->path[i];
-    add_unit(P, g, lane, grp, P.p[i], P.m[i]);
+    add_unit<DRIFT>(P, g, lane, grp, P.p[i], P.m[i]);
     if (grp == G) ++G;
     if (lane == 0) sm->lvl[i + 1] = (unsigned)G << 16;
   }
@@ -633,7 +644,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
   if (single) {  // enter the segment root u
     const int i = du - 1;
     const int grp = sm->path[i];
-    add_unit(P, g, lane, grp, P.p[i], P.m[i]);
+    add_unit<DRIFT>(P, g, lane, grp, P.p[i], P.m[i]);
     if (grp == G) ++G;
     if (lane == 0) sm->lvl[du] = (unsigned)G << 16;
     o.visits = 1;
@@ -778,7 +789,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
           const unsigned long long x0 = lane == i1 ? ~0ull : eb0;
           const unsigned long long x1 = lane + 32 == i1 ? ~0ull : eb1;
           const double m2 = __longlong_as_double((long long)warp_min_u64(x0 < x1 ? x0 : x1));
-          if (P.check_drift) {  // every visited leaf child does += / -= on its group
+          if (DRIFT) {  // every visited leaf child does += / -= on its group
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
               const int ch = lane + 32 * k;
@@ -975,7 +986,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
           // every visited child, pruned or entered, does += / -= on its group
           // (grouping.cpp:178-199): a round trip that does not restore the sum
           // makes the reference's later sums path dependent
-          if (P.check_drift && valid && ci < G &&
+          if (DRIFT && valid && ci < G &&
               (((g.gp[k] + up) - up) != g.gp[k] || ((g.gm[k] + um) - um) != g.gm[k]))
             g.drift = true;
           pr[k] = !valid || (hc && A + mb < cut) || (lD[k] - md > RMn);
@@ -1014,7 +1025,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
       HPK_PC(4, 1);
       if (!(mp & bit)) {  // inside the error margin: the exact serial check
         o.exact += 1;
-        add_unit(P, g, lane, c, up, um);
+        add_unit<DRIFT>(P, g, lane, c, up, um);
         const int Gc = c == G ? G + 1 : G;
         const bool pass = exact_passes(P, g, Gc, d + 1, cut);
         remove_unit(P, g, lane, c, up, um);
@@ -1050,7 +1061,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
         sm->mprune[d] = mr;
         sm->mcut[d] = mc;
       }
-      add_unit(P, g, lane, c, up, um);
+      add_unit<DRIFT>(P, g, lane, c, up, um);
       if (c == G) ++G;
       if (match == d && c == ec) match = d + 1;
       ++d;
@@ -1072,7 +1083,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
   }
 done:
   __syncwarp();
-  o.drift = __any_sync(HPK_FULL_MASK, g.drift);
+  if (DRIFT) o.drift = __any_sync(HPK_FULL_MASK, g.drift);
   if (TOPK) {
     const int rn = sm->rn;
     o.has_best = rn > 0;
@@ -1129,18 +1140,6 @@ __device__ int split_run(const KParams& kp, int p, GState& S, Entry* E, const Ru
     const int w = lim(lev) - (int)sm->path[lev];
     count += rng ? (w > 0 ? 1 : 0) : w;
   }
-  // Eager split (kp.eager > 0, single-sibling pieces): the stop node s starts a
-  // big subtree (>= kp.eager units left) that would be the next list head and
-  // cost one wave per level; it becomes an entry record [s, s.0) — a PREFIX
-  // that visits and checks s only — followed by one piece per child of s, run
-  // in parallel. If s turns out pruned, the entry's run reports a* = depth(s)
-  // and the commit walk deletes the children (the PREFIX deletion rule).
-  const int n = S.n_units;
-  const int gs = (int)((sm->lvl[d] >> 16) & 255);  // groups at the stop node's parent
-  const int Gs = gs + (o.stop_c == gs ? 1 : 0);     // groups at the stop node
-  const bool eager = !rng && kp.eager > 0 && d + 1 < n && n - (d + 1) >= kp.eager;
-  const int nk = eager ? 1 + (Gs + 1) : 0;          // entry + children
-  if (eager) count += nk - 1;                       // (they replace piece 0)
   int first = 0;
   if (lane == 0) {  // CAS bump allocation: a failed attempt leaves no hole, and the
     // list head alone may use the last `reserve` slots (progress guarantee)
@@ -1164,31 +1163,6 @@ __device__ int split_run(const KParams& kp, int p, GState& S, Entry* E, const Ru
   Entry* pool = pool_ptr(kp, p, S.pool_cur);
   for (int k = lane; k < count; k += 32) {
     Entry& qe = pool[first + k];
-    if (k < nk) {  // the eager entry record and the stop node's children
-      for (int i = 0; i < d; ++i) qe.u[i] = sm->path[i];
-      qe.u[d] = (uint8_t)o.stop_c;
-      if (k == 0) {
-        for (int i = 0; i <= d; ++i) qe.end[i] = qe.u[i];
-        qe.end[d + 1] = 0;
-        qe.du = (uint8_t)(d + 1);
-        qe.dend = (uint8_t)(d + 2);
-        qe.hi = (uint8_t)o.stop_c;
-        qe.kind = KIND_PREFIX;
-      } else {
-        qe.u[d + 1] = (uint8_t)(k - 1);
-        qe.du = (uint8_t)(d + 2);
-        qe.hi = (uint8_t)(k - 1);
-        qe.kind = KIND_FULL;
-      }
-      qe.cver = -1;
-      qe.finished = 0;
-      qe.capped = 0;
-      qe.uncapped = 0;
-      qe.has_best = 0;
-      qe.a_star = -1;
-      continue;
-    }
-    const int kk = eager ? k - nk + 1 : k;  // index in the plain enumeration
     int lev = d, child = o.stop_c, last;
     if (rng) {
       for (int idx = k; idx > 0;) {  // the k-th non-empty level below d
@@ -1200,7 +1174,7 @@ __device__ int split_run(const KParams& kp, int p, GState& S, Entry* E, const Ru
       }
       last = lim(lev);
     } else {  // the k-th sibling piece, level by level (deepest first)
-      int idx = kk, base = o.stop_c - 1, cnt = lim(d) - base;
+      int idx = k, base = o.stop_c - 1, cnt = lim(d) - base;
       while (idx >= cnt) {
         idx -= cnt;
         --lev;
@@ -2577,7 +2551,6 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
     // schedule phase (the live count drops as problems finish mid-phase; using it
     // let late schedulers over-push past qcap, starving problems)
     const int act = max(1, *((volatile int*)kp.active + 6));
-    const int act_units = max(1, *((volatile int*)kp.active + 63));
     // ... throttled by the list's headroom: each queued run may split, adding
     // about as many pieces as this wave's runs did on average; a full list
     // would revert splits (wasted runs) every wave
@@ -2585,11 +2558,8 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
     const long long dr = runs_now - S.runs_prev;
     const int est = (int)min((long long)kp.reserve, max(1LL, (etot + dr - 1) / max(1LL, dr)));
     const int headroom = kp.lcap - kp.reserve - nlen;
-    // the share: by the problem's units when kp.unit_share (deeper searches need
-    // more runs per wave to move their commit front), else equal
-    const int fair = kp.unit_share
-                         ? (int)((long long)kp.qmax * S.n_units / act_units)
-                         : kp.qmax / act;
+    // an equal share of the run slots per active problem
+    const int fair = kp.qmax / act;
     const int qmax = max(1, min(min(max(32, fair), kp.qmax_one), headroom / est));
     const long long bl = P.budget < 0 ? -1 : P.budget - S.V;
     if (kp.par_push && P.top_k <= 1 && nagg > 0) {
@@ -2940,17 +2910,19 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
           rec->ntin = item.ntv;
         }
         __syncwarp();
-        o = run_segment<true>(PV, E, E, C, item.cap, ws, lane, kp.err, kp.deadline_ns,
-                              (kp.trace >= 2 && kp.trace < 5) ? kp.prof : nullptr,
-                              stoppable ? kp.stop : nullptr, kp.minq,
-                              stoppable && kp.wave_ns ? wave_t0 + kp.wave_ns : 0ull, tk,
-                              S.seed_obj, rec);
+#define HPK_RUN(TK, DR, WS, TKV, FL, REC)                                                  \
+  run_segment<TK, DR>(PV, E, E, C, item.cap, WS, lane, kp.err, kp.deadline_ns,              \
+                      (kp.trace >= 2 && kp.trace < 5) ? kp.prof : nullptr,                  \
+                      stoppable ? kp.stop : nullptr, kp.minq,                               \
+                      stoppable && kp.wave_ns ? wave_t0 + kp.wave_ns : 0ull, TKV, FL, REC)
+        // the drift-checking instantiation only for problems outside the
+        // exact-sum contract: the common case carries no extra instructions
+        o = PV.check_drift ? HPK_RUN(true, true, ws, tk, S.seed_obj, rec)
+                           : HPK_RUN(true, false, ws, tk, S.seed_obj, rec);
       } else {
-        o = run_segment<false>(PV, E, E, C, item.cap, wsm + warp, lane, kp.err, kp.deadline_ns,
-                               (kp.trace >= 2 && kp.trace < 5) ? kp.prof : nullptr,
-                               stoppable ? kp.stop : nullptr, kp.minq,
-                               stoppable && kp.wave_ns ? wave_t0 + kp.wave_ns : 0ull, 1, 0.0,
-                               nullptr);
+        o = PV.check_drift ? HPK_RUN(false, true, wsm + warp, 1, 0.0, nullptr)
+                           : HPK_RUN(false, false, wsm + warp, 1, 0.0, nullptr);
+#undef HPK_RUN
       }
       int* pcv = list_arr(kp, p, S.cur, 1);
       int* cnt = list_arr(kp, p, S.cur, 2);
@@ -3685,6 +3657,15 @@ double seed_floor(const hpk_grouping_problem& pr) {
 
 }  // namespace
 
+#ifndef HPK_WIDE
+// The wide (128-unit) build's entry points (hpk_grouping_wide.cu).
+extern "C" int hpk_grouping_search_wide(const hpk_grouping_problem*, int, hpk_grouping_result*,
+                                        const hpk_search_config*);
+extern "C" void hpk_last_timing_wide(hpk_timing*);
+extern "C" void hpk_reset_timing_wide(void);
+extern "C" const char* hpk_last_error_wide(void);
+#endif
+
 // Hooks shared with hpk_partition.cu (same thread-local error / timing).
 void hpkp_fail(const std::string& msg) { t_err = msg; }
 namespace hpk_timing_bridge {
@@ -3898,7 +3879,7 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
   HPK_CUDA(cudaSetDevice(device));
 
   // Partition problems between the engines.
-  std::vector<int> wave_ix, serial_ix, enum_ix;
+  std::vector<int> wave_ix, serial_ix, enum_ix, wide_ix;
   for (int i = 0; i < n_problems; ++i) {
     const hpk_grouping_problem& pr = problems[i];
     results[i].status = 0;
@@ -3918,8 +3899,37 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
     const bool wave_ok = !cfg.force_serial && pr.n <= MAXN && pr.top_k <= KW;
     const bool enum_ok = wave_ok && contract && cfg.enumerate && pr.n <= pr.exact_threshold &&
                          pr.n <= ENUM_MAXN;
+#ifndef HPK_WIDE
+    if (!cfg.force_serial && !wave_ok && pr.n <= HPK_MAX_UNITS && pr.top_k <= KW) {
+      wide_ix.push_back(i);  // 65..128 units: the wide build's wave engine
+      continue;
+    }
+#endif
     (enum_ok ? enum_ix : wave_ok ? wave_ix : serial_ix).push_back(i);
   }
+#ifndef HPK_WIDE
+  if (!wide_ix.empty()) {
+    std::vector<hpk_grouping_problem> wp;
+    std::vector<hpk_grouping_result> wr;
+    for (int i : wide_ix) {
+      wp.push_back(problems[i]);
+      wr.push_back(results[i]);
+    }
+    hpk_search_config wc = cfg;
+    wc.device = device;
+    hpk_reset_timing_wide();
+    const int rc = hpk_grouping_search_wide(wp.data(), (int)wp.size(), wr.data(), &wc);
+    hpk_timing tw;
+    hpk_last_timing_wide(&tw);
+    t_timing.search_ms += tw.search_ms;
+    t_timing.serial_ms += tw.serial_ms;
+    t_timing.h2d_bytes += tw.h2d_bytes;
+    t_timing.d2h_bytes += tw.d2h_bytes;
+    t_timing.kernel_launches += tw.kernel_launches;
+    if (rc != 0) return fail(rc, hpk_last_error_wide());
+    for (size_t k = 0; k < wide_ix.size(); ++k) results[wide_ix[k]] = wr[k];
+  }
+#endif
 
   // ---------------- enumeration engine (exhaustive searches, planner path)
   if (!enum_ix.empty()) {
@@ -4059,11 +4069,10 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
     for (int k = 0; k < P; ++k) max_n = std::max(max_n, problems[wave_ix[k]].n);
     // piece shape: sibling ranges for big batches (cfg5: 1.3x faster, shorter
     // lists), single siblings for a few problems (cfg3: 1.9x faster — more
-    // parallel pieces near one search's commit front); HPK_RANGES overrides
+    // parallel pieces near one search's commit front)
     const int ranges = P > 16 ? 1 : 0;
-    const int reserve = ranges ? max_n + 64                          // one piece per level
-                               : max_n * (max_n + 1) / 2 + 32 + 66;  // one per sibling,
-                                                                      // + an eager split
+    const int reserve = ranges ? max_n + 64                     // one piece per level
+                               : max_n * (max_n + 1) / 2 + 98;  // one per sibling
     if (pcap < 4 * reserve) pcap = 4 * reserve;
     std::vector<GProb> hp(P);
     for (int k = 0; k < P; ++k) {
@@ -4152,7 +4161,6 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
     kp.minq = 0;
     kp.runners = WARPS_PER_BLOCK;
     kp.ranges = ranges;
-    kp.eager = 0;
     // run-phase time slice: 300 us (HPK_WAVE_US overrides; 0 = none)
     kp.wave_ns = HPK_WAVE_NS;
     kp.n_problems = P;
@@ -4162,7 +4170,6 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
     kp.qcap = qcap;
     kp.qmax = qmax;
     kp.qmax_one = (int)(HPK_QONE * nwarps);
-    kp.unit_share = 0;
     kp.seg_cap = seg_cap;
     kp.front_cap = seg_cap;
     kp.ramp = 64;  // measured: -0.7 ms cfg4, -1.3 ms tp1 alone
