@@ -194,6 +194,13 @@ typedef struct hpk_search_config {
 
 void hpk_search_config_init(hpk_search_config* cfg);
 
+/* The device assignment HPK_ALL_DEVICES uses (host only, no CUDA call):
+ * problems in decreasing estimated cost (budgeted: node_budget visits,
+ * exhaustive: Bell(n), weighted by n + 8; ties in caller order) each to the
+ * device with the least assigned cost (ties: lowest ordinal). */
+int hpk_assign_devices(const hpk_grouping_problem* problems, int n_problems, int n_devices,
+                       int* out_device);
+
 /* Batched grouping search: every problem is searched concurrently on the GPU
  * (one persistent cooperative kernel for the wave engine). */
 int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,

@@ -3768,6 +3768,25 @@ double search_cost(const hpk_grouping_problem& pr) {
   return visits * (double)(pr.n + 8);
 }
 
+// Longest-first (LPT) assignment of searches to devices: each problem, in
+// decreasing search_cost (ties: caller order), to the device with the least
+// assigned cost so far (ties: the lowest ordinal).
+void assign_devices(const hpk_grouping_problem* problems, int n, int ndev, int* out) {
+  std::vector<int> order(n);
+  std::vector<double> cost(n);
+  for (int i = 0; i < n; ++i) {
+    order[i] = i;
+    cost[i] = search_cost(problems[i]);
+  }
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+  std::vector<double> load(std::max(1, ndev), 0.0);
+  for (int i : order) {
+    const int d = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+    load[d] += cost[i];
+    out[i] = d;
+  }
+}
+
 // hpk_grouping_search over every visible device: problems go longest-first to
 // the least-loaded device (one host thread and one persistent kernel per
 // device, each on its own context and stream); results land in the caller's
@@ -3775,21 +3794,10 @@ double search_cost(const hpk_grouping_problem& pr) {
 int search_all_devices(const hpk_grouping_problem* problems, int n_problems,
                        hpk_grouping_result* results, const hpk_search_config& cfg, int ndev) {
   const int D = std::min(ndev, 16);
-  std::vector<int> order(n_problems);
-  std::vector<double> cost(n_problems);
-  for (int i = 0; i < n_problems; ++i) {
-    order[i] = i;
-    cost[i] = search_cost(problems[i]);
-  }
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
-  std::vector<double> load(D, 0.0);
+  std::vector<int> dev(n_problems);
+  assign_devices(problems, n_problems, D, dev.data());
   std::vector<std::vector<int>> mine(D);
-  for (int i : order) {
-    int d = (int)(std::min_element(load.begin(), load.end()) - load.begin());
-    load[d] += cost[i];
-    mine[d].push_back(i);
-  }
-  for (auto& m : mine) std::sort(m.begin(), m.end());  // batch in caller order
+  for (int i = 0; i < n_problems; ++i) mine[dev[i]].push_back(i);  // caller order
   std::vector<int> rc(D, 0);
   std::vector<hpk_timing> tim(D);
   std::vector<std::string> err(D);
@@ -3835,6 +3843,14 @@ int search_all_devices(const hpk_grouping_problem* problems, int n_problems,
 }  // namespace hpk
 
 extern "C" {
+
+int hpk_assign_devices(const hpk_grouping_problem* problems, int n_problems, int n_devices,
+                       int* out_device) {
+  if (n_problems < 0 || n_devices < 1 || (n_problems > 0 && (!problems || !out_device)))
+    return 6;
+  assign_devices(problems, n_problems, n_devices, out_device);
+  return 0;
+}
 
 int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
                         hpk_grouping_result* results, const hpk_search_config* cfg_in) {

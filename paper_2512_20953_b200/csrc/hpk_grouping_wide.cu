@@ -15,4 +15,5 @@
 #define hpk_last_timing hpk_last_timing_wide
 #define hpk_reset_timing hpk_reset_timing_wide
 #define hpk_grouping_search hpk_grouping_search_wide
+#define hpk_assign_devices hpk_assign_devices_wide
 #include "hpk_grouping.cu"

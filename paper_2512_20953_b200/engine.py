@@ -238,6 +238,9 @@ class Engine:
         L.hpk_pipeline_sim.restype = C.c_int
         L.hpk_stage_affinity.argtypes = [C.POINTER(hpk_affinity_problem), C.c_int, C.c_int]
         L.hpk_stage_affinity.restype = C.c_int
+        L.hpk_assign_devices.argtypes = [C.POINTER(hpk_grouping_problem), C.c_int, C.c_int,
+                                         C.POINTER(C.c_int)]
+        L.hpk_assign_devices.restype = C.c_int
         L.hpk_last_timing.argtypes = [C.POINTER(hpk_timing)]
         L.hpk_reset_timing.argtypes = []
 
@@ -399,3 +402,22 @@ class Engine:
             raise EngineError(rc, self.lib.hpk_last_error().decode())
         return [(arr[i].makespan, list(outs[i][0]), list(outs[i][1]), list(outs[i][2]),
                  list(outs[i][3])) for i in range(n)]
+
+    def assign_devices(self, problems: Sequence[GroupingProblem], n_devices: int) -> List[int]:
+        """hpk_assign_devices: the device of each search under HPK_ALL_DEVICES
+        (host-only; no GPU needed)."""
+        n = len(problems)
+        arr = (hpk_grouping_problem * n)()
+        keep = []
+        for i, pb in enumerate(problems):
+            m = pb.n
+            pw = (C.c_double * m)(*pb.power)
+            me = (C.c_double * m)(*pb.memory)
+            keep += [pw, me]
+            arr[i] = hpk_grouping_problem(m, pb.n_microbatches, pb.min_mem, pb.exact_threshold,
+                                          pb.node_budget, pb.top_k, pw, me, None, None)
+        out = (C.c_int * max(1, n))()
+        rc = self.lib.hpk_assign_devices(arr, n, n_devices, out)
+        if rc != 0:
+            raise EngineError(rc, "hpk_assign_devices: bad arguments")
+        return list(out[:n])
