@@ -189,7 +189,8 @@ typedef struct hpk_search_config {
   int enumerate;         /* 1: exhaustive top_k = 1 problems with n <= 12 take the
                             enumeration engine (engine 2: winner only, visited = -1) */
   int max_waves;         /* watchdog on the wave loop (0: default 1000000) */
-  double max_seconds;    /* device wall-clock watchdog (0: default 120 s) */
+  double max_seconds;    /* device wall-clock watchdog (0: derived from the budgets) */
+  int max_ctas;          /* wave-engine grid cap (0: every SM, 2 CTAs each) */
 } hpk_search_config;
 
 void hpk_search_config_init(hpk_search_config* cfg);

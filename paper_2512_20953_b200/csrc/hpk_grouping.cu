@@ -3734,6 +3734,7 @@ void hpk_search_config_init(hpk_search_config* cfg) {
   cfg->enumerate = 0;
   cfg->max_waves = 0;
   cfg->max_seconds = 0;
+  cfg->max_ctas = 0;
 }
 
 void hpk_last_timing(hpk_timing* out) {
@@ -4126,7 +4127,8 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
     if (int rc = grow(c.pagg, c.cap_pagg, (size_t)P * xtn)) return rc;
     HPK_CUDA(cudaMemsetAsync(c.pagg, 0xff, sizeof(PushAgg) * P * xtn, c.stream));  // stamps -1
     HPK_CUDA(cudaMemsetAsync(c.xt, 0, sizeof(int) * P * xtn, c.stream));
-    const int grid = c.sms * c.blocks_per_sm;
+    const int grid = cfg.max_ctas > 0 ? std::min(cfg.max_ctas, c.sms * c.blocks_per_sm)
+                                      : c.sms * c.blocks_per_sm;
     const int nwarps = grid * WARPS_PER_BLOCK;
     // total run slots per wave, shared by the active problems (most segments are
     // small: several per warp keep the warps busy through the time slice)

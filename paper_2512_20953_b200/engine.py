@@ -62,6 +62,7 @@ class hpk_search_config(C.Structure):
         ("enumerate", C.c_int),
         ("max_waves", C.c_int),
         ("max_seconds", C.c_double),
+        ("max_ctas", C.c_int),
     ]
 
 
@@ -261,7 +262,8 @@ class Engine:
     def grouping_search(self, problems: Sequence[GroupingProblem], *, device: int = -1,
                         segment_cap: int = 0, max_list: int = 0,
                         force_serial: bool = False, max_waves: int = 0,
-                        max_seconds: float = 0.0, enumeration: bool = False) -> List[GroupingResult]:
+                        max_seconds: float = 0.0, enumeration: bool = False,
+                        max_ctas: int = 0) -> List[GroupingResult]:
         n = len(problems)
         arr = (hpk_grouping_problem * n)()
         res = (hpk_grouping_result * n)()
@@ -290,6 +292,7 @@ class Engine:
         cfg.enumerate = int(enumeration)
         cfg.max_waves = max_waves
         cfg.max_seconds = max_seconds
+        cfg.max_ctas = max_ctas
         rc = self.lib.hpk_grouping_search(arr, n, res, C.byref(cfg))
         if rc != 0:
             raise EngineError(rc, self.lib.hpk_last_error().decode())
