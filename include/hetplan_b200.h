@@ -273,6 +273,15 @@ typedef struct hpk_affinity_problem {
 /* All problems in one launch (one CTA each). */
 int hpk_stage_affinity(hpk_affinity_problem* problems, int n_problems, int device);
 
+/* The planner's fused launch: candidate k's affinity pass (affinity[k]), then
+ * its partition + cost (cands[k]) in the same CTA, with stage_node /
+ * stage_rank0 given in the PRE-affinity slot order — the kernel permutes them
+ * (swaps exchange same-type units, so types, indices and capacities do not
+ * change). affinity[k].n_slots must equal cands[k]'s stage count. One H2D copy,
+ * one launch, one D2H copy for the whole batch. */
+int hpk_affinity_partition_cost(hpk_affinity_problem* affinity, const hpk_plan_candidate* cands,
+                                int n_cands, hpk_plan_result* results, int device);
+
 /* The planner's whole stage mapping (map_nodes_and_stages,
  * P/src/stage_map.cpp:63-216) for n_groupings groupings of one cluster's TP
  * units at tp, exactly as hp_plan_compute runs it: the joint / fallback

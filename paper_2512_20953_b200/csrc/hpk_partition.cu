@@ -29,6 +29,7 @@
 #include <vector>
 
 #include "hetplan_b200.h"
+#include "hpk_affinity.cuh"
 #include "hpk_common.cuh"
 
 namespace hpkp {
@@ -89,8 +90,9 @@ __device__ __forceinline__ double stage_memory(const Cand& c, int layers, int st
   return fixed + variable;
 }
 
-__global__ void __launch_bounds__(THREADS) partition_cost_kernel(Args a) {
-  extern __shared__ __align__(16) double sbest[];
+// The partition + cost of candidate blockIdx.x by the calling CTA; sbest is the
+// dynamic shared memory (best tables when they fit, per-layer scratch).
+__device__ __forceinline__ void partition_body(const Args& a, double* sbest) {
   __shared__ int s_first_missing;
   __shared__ double s_bottleneck;
   __shared__ int s_status;
@@ -402,6 +404,34 @@ __global__ void __launch_bounds__(THREADS) partition_cost_kernel(Args a) {
   }
 }
 
+__global__ void __launch_bounds__(THREADS) partition_cost_kernel(Args a) {
+  extern __shared__ __align__(16) double sbest[];
+  partition_body(a, sbest);
+}
+
+// The planner's fused launch: the stage mapper's DP-affinity pass of a
+// candidate (hpk_affinity.cuh), then its partition + cost with the swapped
+// units' nodes and ranks. Swaps exchange units of the same type, so only the
+// stage_node / stage_rank0 arrays change (slot s now holds the unit of slot
+// perm[s]); types, indices and capacities are the pre-affinity ones.
+__global__ void __launch_bounds__(THREADS) affinity_partition_kernel(
+    hpks::Prob* probs, const int* goff_all, const int* type_all, const int* node_all,
+    int* perm_all, const int* snode_pre, const int* srank_pre, int* snode_w, int* srank_w,
+    Args a) {
+  extern __shared__ __align__(16) double sbest[];
+  hpks::Prob& pr = probs[blockIdx.x];
+  hpks::affinity_body(pr, goff_all, type_all, node_all, perm_all, reinterpret_cast<int*>(sbest));
+  __syncthreads();
+  const int base = a.cands[blockIdx.x].stage_base;
+  for (int s = threadIdx.x; s < pr.n_slots; s += blockDim.x) {
+    const int q = perm_all[pr.in_off + s];
+    snode_w[base + s] = snode_pre[base + q];
+    srank_w[base + s] = srank_pre[base + q];
+  }
+  __syncthreads();
+  partition_body(a, sbest);
+}
+
 struct Ctx {
   int device = -1;
   cudaStream_t stream = nullptr;
@@ -433,16 +463,34 @@ using namespace hpkp;
 
 void hpkp_fail(const std::string& msg);
 
-extern "C" int hpk_partition_cost_ex(const hpk_plan_candidate* cands, int n_cands,
-                                     hpk_plan_result* results, int device, int flags);
+namespace {
+int partition_launch(const hpk_plan_candidate* cands, int n_cands, hpk_plan_result* results,
+                     int device, int flags, hpk_affinity_problem* aff);
+}
 
 extern "C" int hpk_partition_cost(const hpk_plan_candidate* cands, int n_cands,
                                   hpk_plan_result* results, int device) {
-  return hpk_partition_cost_ex(cands, n_cands, results, device, 0);
+  return partition_launch(cands, n_cands, results, device, 0, nullptr);
 }
 
 extern "C" int hpk_partition_cost_ex(const hpk_plan_candidate* cands, int n_cands,
                                      hpk_plan_result* results, int device, int flags) {
+  return partition_launch(cands, n_cands, results, device, flags, nullptr);
+}
+
+extern "C" int hpk_affinity_partition_cost(hpk_affinity_problem* affinity,
+                                           const hpk_plan_candidate* cands, int n_cands,
+                                           hpk_plan_result* results, int device) {
+  if (n_cands > 0 && !affinity) {
+    hpkp_fail("hpk_affinity_partition_cost: null affinity problems");
+    return 6;
+  }
+  return partition_launch(cands, n_cands, results, device, 0, affinity);
+}
+
+namespace {
+int partition_launch(const hpk_plan_candidate* cands, int n_cands, hpk_plan_result* results,
+                     int device, int flags, hpk_affinity_problem* aff) {
   if (n_cands <= 0) return 0;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0) {
@@ -554,7 +602,33 @@ extern "C" int hpk_partition_cost_ex(const hpk_plan_candidate* cands, int n_cand
   const size_t o_steady = ar.take(sizeof(double) * Gn);
   const size_t o_total = ar.take(sizeof(double) * Gn);
   const size_t o_bubble = ar.take(sizeof(double) * Gn);
+  // fused launch: the affinity pass's problems (swap counts come back) and
+  // permutation are outputs too; its inputs and the permuted node / rank
+  // arrays go to the scratch region
+  std::vector<hpks::Prob> ahp;
+  std::vector<int> agoff, atype, anode;
+  size_t aff_smem = 0;
+  if (aff) {
+    aff_smem = hpks::affinity_flatten(aff, n_cands, ahp, agoff, atype, anode);
+    if (aff_smem > 200 * 1024) {
+      hpkp_fail("hetplan_b200: stage-affinity problem too large for shared memory");
+      return 6;
+    }
+    for (int k = 0; k < n_cands; ++k)
+      if (aff[k].n_slots != cands[k].group_stage_off[cands[k].n_groups]) {
+        hpkp_fail("hpk_affinity_partition_cost: affinity slots differ from the stages");
+        return 6;
+      }
+  }
+  const size_t AS = std::max<size_t>(1, atype.size());
+  const size_t o_aprobs = ar.take(sizeof(hpks::Prob) * (aff ? n_cands : 1));
+  const size_t o_aperm = ar.take(sizeof(int) * AS);
   const size_t out_end = ar.used;
+  const size_t o_agoff = ar.take(sizeof(int) * std::max<size_t>(1, agoff.size()));
+  const size_t o_atype = ar.take(sizeof(int) * AS);
+  const size_t o_anode = ar.take(sizeof(int) * AS);
+  const size_t o_snode_w = ar.take(sizeof(int) * S);
+  const size_t o_srank_w = ar.take(sizeof(int) * S);
   const size_t o_tt = ar.take(sizeof(double) * std::max<size_t>(1, tt_total));
   const size_t o_tm = ar.take(std::max<size_t>(1, tt_total));
   const size_t o_gbest = ar.take(sizeof(double) * std::max<size_t>(1, gbest_total));
@@ -571,7 +645,19 @@ extern "C" int hpk_partition_cost_ex(const hpk_plan_candidate* cands, int n_cand
   stage(o_srank, srank.data(), sizeof(int) * srank.size());
   stage(o_scap, scap.data(), sizeof(double) * scap.size());
   stage(o_prof, prof.data(), sizeof(double) * prof.size());
+  if (aff) {
+    stage(o_aprobs, ahp.data(), sizeof(hpks::Prob) * n_cands);
+    stage(o_agoff, agoff.data(), sizeof(int) * agoff.size());
+    stage(o_atype, atype.data(), sizeof(int) * atype.size());
+    stage(o_anode, anode.data(), sizeof(int) * anode.size());
+  }
   HPKP_CUDA(cudaMemcpyAsync(ar.d, ar.h, in_end, cudaMemcpyHostToDevice, cx.stream));
+  if (aff) {  // the affinity inputs sit after the outputs (one more small copy)
+    HPKP_CUDA(cudaMemcpyAsync(ar.d + o_aprobs, ar.h + o_aprobs, sizeof(hpks::Prob) * n_cands,
+                              cudaMemcpyHostToDevice, cx.stream));
+    HPKP_CUDA(cudaMemcpyAsync(ar.d + o_agoff, ar.h + o_agoff, o_snode_w - o_agoff,
+                              cudaMemcpyHostToDevice, cx.stream));
+  }
   HPKP_CUDA(cudaMemsetAsync(ar.d + o_outs, 0, sizeof(Outs) * n_cands, cx.stream));
   const long long h2d = (long long)in_end;
   Cand* d_c = ar.dp<Cand>(o_c);
@@ -615,12 +701,23 @@ extern "C" int hpk_partition_cost_ex(const hpk_plan_candidate* cands, int n_cand
   a.out_total = d_total;
   a.out_bubble = d_bubble;
   a.outs = d_outs;
-  const size_t smem = max_smem_best * sizeof(double);
+  const size_t smem = std::max(max_smem_best * sizeof(double), aff_smem);
   a.smem_best_doubles = max_smem_best;
-  HPKP_CUDA(cudaFuncSetAttribute(partition_cost_kernel,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (smem > 48 * 1024)
+    HPKP_CUDA(cudaFuncSetAttribute(aff ? (const void*)affinity_partition_kernel
+                                       : (const void*)partition_cost_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   HPKP_CUDA(cudaEventRecord(cx.ev0, cx.stream));
-  partition_cost_kernel<<<n_cands, THREADS, smem, cx.stream>>>(a);
+  if (aff) {
+    a.stage_node = ar.dp<int>(o_snode_w);
+    a.stage_rank0 = ar.dp<int>(o_srank_w);
+    affinity_partition_kernel<<<n_cands, THREADS, smem, cx.stream>>>(
+        ar.dp<hpks::Prob>(o_aprobs), ar.dp<int>(o_agoff), ar.dp<int>(o_atype),
+        ar.dp<int>(o_anode), ar.dp<int>(o_aperm), d_snode, d_srank, ar.dp<int>(o_snode_w),
+        ar.dp<int>(o_srank_w), a);
+  } else {
+    partition_cost_kernel<<<n_cands, THREADS, smem, cx.stream>>>(a);
+  }
   HPKP_CUDA(cudaGetLastError());
   HPKP_CUDA(cudaEventRecord(cx.ev1, cx.stream));
   HPKP_CUDA(cudaMemcpyAsync(ar.h + o_outs, ar.d + o_outs, out_end - o_outs, cudaMemcpyDeviceToHost,
@@ -638,6 +735,14 @@ extern "C" int hpk_partition_cost_ex(const hpk_plan_candidate* cands, int n_cand
   cudaEventElapsedTime(&ms, cx.ev0, cx.ev1);
   const long long d2h = (long long)(out_end - o_outs);
   hpk_timing_bridge::add_partition(ms, h2d, d2h);
+  if (aff) {
+    const hpks::Prob* hpr = ar.hp<hpks::Prob>(o_aprobs);
+    const int* hperm = ar.hp<int>(o_aperm);
+    for (int k = 0; k < n_cands; ++k) {
+      for (int q = 0; q < aff[k].n_slots; ++q) aff[k].slot_perm[q] = hperm[hpr[k].in_off + q];
+      aff[k].swaps = hpr[k].swaps;
+    }
+  }
   for (int k = 0; k < n_cands; ++k) {
     const Cand& c = hc[k];
     hpk_plan_result& r = results[k];
@@ -664,6 +769,7 @@ extern "C" int hpk_partition_cost_ex(const hpk_plan_candidate* cands, int n_cand
   }
   return 0;
 }
+}  // namespace
 
 // ----------------------------------------------------------------------------
 // Issue-rate microbenchmarks: the roofline denominators for this path

@@ -449,6 +449,7 @@ struct PlanJob {
   std::vector<std::vector<double>> obj_buf, z_buf;
   std::vector<Candidate> cands;
   std::vector<hpk_plan_candidate> pin;
+  std::vector<hpk_affinity_problem> pin_aff;  // the affinity pass of each pin entry
   std::vector<int> pin_of;
   std::vector<hpk_plan_result> pres;
   std::exception_ptr error;  // raised by a phase; the job is finished
@@ -644,8 +645,9 @@ void job_partition_inputs(PlanJob& J) {
   auto& pin = J.pin;
   auto& pin_of = J.pin_of;
   auto& pres = J.pres;
-  for (auto& c : cands)
-    if (c.map_error.kind == Pending::NONE) apply_affinity(c.mapping, c.aff);
+  // inputs from the pre-affinity mapping: the fused launch runs the affinity
+  // pass and permutes stage_node / stage_rank0 itself (same-type swaps leave
+  // types, stage indices and capacities unchanged)
   int n_bits = 0;
   while ((1 << n_bits) <= cfg.n_layers) ++n_bits;
   pin_of.assign(cands.size(), -1);
@@ -711,6 +713,15 @@ void job_partition_inputs(PlanJob& J) {
     p.prof = c.prof.data();
     pin_of[ci] = (int)pin.size();
     pin.push_back(p);
+    hpk_affinity_problem a;
+    a.n_groups = (int)c.aff.goff.size() - 1;
+    a.n_slots = (int)c.aff.type.size();
+    a.group_off = c.aff.goff.data();
+    a.slot_type = c.aff.type.data();
+    a.slot_node = c.aff.node.data();
+    a.slot_perm = c.aff.perm.data();
+    a.swaps = 0;
+    J.pin_aff.push_back(a);
   }
   // result buffers of the batched partition + cost launch (phase 4)
   pres.assign(pin.size(), hpk_plan_result{});
@@ -986,46 +997,18 @@ void plan_jobs(std::vector<PlanJob*>& jobs, int threads) {
   clk.lap("search");
   for_jobs(jobs, threads, job_candidates);
   clk.lap("candidates(premap)");
-  // ---- phase 3 (GPU): the stage mapper's affinity pass, every candidate at once
-  {
-    std::vector<hpk_affinity_problem> ap;
-    std::vector<PlanJob*> aowner;
-    for (PlanJob* J : jobs) {
-      if (J->error) continue;
-      for (auto& c : J->cands) {
-        if (c.map_error.kind != Pending::NONE) continue;
-        hpk_affinity_problem a;
-        a.n_groups = (int)c.aff.goff.size() - 1;
-        a.n_slots = (int)c.aff.type.size();
-        a.group_off = c.aff.goff.data();
-        a.slot_type = c.aff.type.data();
-        a.slot_node = c.aff.node.data();
-        a.slot_perm = c.aff.perm.data();
-        a.swaps = 0;
-        ap.push_back(a);
-        aowner.push_back(J);
-      }
-    }
-    if (!ap.empty()) {
-      try {
-        const int rc = hpk_stage_affinity(ap.data(), (int)ap.size(), -1);
-        if (rc != 0) gpu_fail(rc);
-      } catch (...) {
-        fail_unfinished(jobs, std::current_exception());
-        return;
-      }
-    }
-  }
-  clk.lap("affinity");
   for_jobs(jobs, threads, job_partition_inputs);
   clk.lap("partition-inputs");
-  // ---- phase 4: one batched GPU launch for every candidate's partition + cost
+  // ---- phases 3 + 4 (GPU, one launch): every candidate's stage-mapper affinity
+  // pass, then its layer partition + cost
+  std::vector<hpk_affinity_problem> aff;
   std::vector<hpk_plan_candidate> pin;
   std::vector<hpk_plan_result> pres;
   std::vector<std::pair<PlanJob*, size_t>> powner;
   for (PlanJob* J : jobs) {
     if (J->error) continue;
     for (size_t k = 0; k < J->pin.size(); ++k) {
+      aff.push_back(J->pin_aff[k]);
       pin.push_back(J->pin[k]);
       pres.push_back(J->pres[k]);
       powner.emplace_back(J, k);
@@ -1033,7 +1016,8 @@ void plan_jobs(std::vector<PlanJob*>& jobs, int threads) {
   }
   if (!pin.empty()) {
     try {
-      const int rc = hpk_partition_cost(pin.data(), (int)pin.size(), pres.data(), -1);
+      const int rc = hpk_affinity_partition_cost(aff.data(), pin.data(), (int)pin.size(),
+                                                 pres.data(), -1);
       if (rc != 0) gpu_fail(rc);
     } catch (...) {
       fail_unfinished(jobs, std::current_exception());
@@ -1041,7 +1025,11 @@ void plan_jobs(std::vector<PlanJob*>& jobs, int threads) {
     }
     for (size_t i = 0; i < pin.size(); ++i) powner[i].first->pres[powner[i].second] = pres[i];
   }
-  clk.lap("partition");
+  clk.lap("affinity+partition");
+  for_jobs(jobs, threads, [](PlanJob& J) {
+    for (auto& c : J.cands)
+      if (c.map_error.kind == Pending::NONE) apply_affinity(c.mapping, c.aff);
+  });
   for_jobs(jobs, threads, [](PlanJob& J) { J.plan = job_select(J); });
   clk.lap("select");
   validate_jobs_with_sim(jobs);
