@@ -70,7 +70,10 @@ namespace hpk {
 #define HPK_MAXN 64
 #endif
 constexpr int MAXN = HPK_MAXN;
-constexpr int WARPS_PER_BLOCK = 8;
+#ifndef HPK_WPB
+#define HPK_WPB 8
+#endif
+constexpr int WARPS_PER_BLOCK = HPK_WPB;
 constexpr int BLOCK_THREADS = WARPS_PER_BLOCK * 32;
 constexpr int TILE = BLOCK_THREADS * 8;  // list positions per expansion / commit tile
 constexpr uint8_t KIND_FULL = 0;
