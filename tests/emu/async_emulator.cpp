@@ -235,6 +235,9 @@ struct Params {
   int stale_abort;   // 1: a running segment whose cutoff fell behind the front restarts
   long long min_split;  // do not split a run with fewer than this many visits done
   long long slice;      // > 0: a FULL run is preempted after this many units
+  long long merge;      // > 0: new pieces become dispatchable only at the scheduler's
+                        // next list merge (every `merge` units), like a GPU scheduler
+                        // CTA that rebuilds the ordered list periodically
 };
 
 struct Event {
@@ -292,6 +295,19 @@ struct Sim {
   std::vector<int> idle;       // idle warps
   double now = 0;
   bool tick_pending = false;
+  std::vector<int> pending;  // pieces waiting for the next list merge
+  bool merge_pending = false;
+  void publish(int id) {
+    if (prm.merge <= 0) {
+      ready.push_back(id);
+      return;
+    }
+    pending.push_back(id);
+    if (!merge_pending) {
+      merge_pending = true;
+      ev.push({now + (double)prm.merge, 5, 0, 0});
+    }
+  }
   long long ticks = 0;
   Outcome out;
 
@@ -411,10 +427,10 @@ struct Sim {
     e2.next = ids[0];
     // the splitting warp keeps the first (deepest) piece, the rest become ready
     if (keep) {
-      for (size_t i = 1; i < ids.size(); ++i) ready.push_back(ids[i]);
+      for (size_t i = 1; i < ids.size(); ++i) publish(ids[i]);
       start(ids[0], w, t + prm.split_cost - prm.pop_cost);
     } else {  // preempted: every piece goes back to the ready set
-      for (size_t i = 0; i < ids.size(); ++i) ready.push_back(ids[i]);
+      for (size_t i = 0; i < ids.size(); ++i) publish(ids[i]);
       idle.push_back(w);
     }
   }
@@ -519,9 +535,13 @@ struct Sim {
       const Event x = ev.top();
       ev.pop();
       Seg& e = segs[x.seg];
-      if (x.kind != 2 && x.gen != e.gen) continue;  // superseded
+      if (x.kind != 2 && x.kind != 5 && x.gen != e.gen) continue;  // superseded
       now = x.t;
-      if (x.kind == 2) {  // scheduler tick: re-issue split requests while warps idle
+      if (x.kind == 5) {  // list merge: pending pieces become dispatchable
+        merge_pending = false;
+        for (int id : pending) ready.push_back(id);
+        pending.clear();
+      } else if (x.kind == 2) {  // scheduler tick: re-issue split requests while warps idle
         tick_pending = false;
         if (getenv("ASYNC_EMU_TRACE") && ++ticks % 200 == 0)
           fprintf(stderr, "t=%.0f V=%lld C=%g segs=%zu ready=%zu idle=%zu runs=%lld splits=%lld\n",
@@ -566,7 +586,7 @@ extern "C" {
 int async_emu_search(int n, const double* p, const double* m, int K, double min_mem,
                      long long budget, double floor_obj, int warps, double pop_cost,
                      double split_cost, double req_latency, double commit_cost, int order,
-                     int stale_abort, long long min_split, long long slice, int* out_rgs, double* out_obj,
+                     int stale_abort, long long min_split, long long slice, long long merge, int* out_rgs, double* out_obj,
                      int* out_has, long long* out_visited, int* out_aborted, double* out_time,
                      long long* out_stats /* runs, run_visits, splits, reruns, aborts */) {
   Problem pb;
@@ -578,7 +598,7 @@ int async_emu_search(int n, const double* p, const double* m, int K, double min_
   pb.budget = budget;
   pb.floor_obj = floor_obj;
   Params prm{warps, pop_cost, split_cost, req_latency, commit_cost, order, stale_abort,
-             min_split, slice};
+             min_split, slice, merge};
   Sim sim(pb, prm);
   Outcome o = sim.run();
   *out_has = o.best.has ? 1 : 0;

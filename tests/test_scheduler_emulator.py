@@ -130,7 +130,8 @@ def test_async_scheduler_emulator_matches_oracle(async_emu, oracle):
             rng.choice([1, 2, 4, 16]), C.c_double(rng.choice([0, 1, 5])),
             C.c_double(rng.choice([0, 2, 9])), C.c_double(rng.choice([0, 1, 3])), C.c_double(2),
             rng.choice([0, 1]), rng.choice([0, 1]), C.c_longlong(rng.choice([1, 4])),
-            C.c_longlong(rng.choice([0, 0, 50, 200])), rgs, C.byref(obj), C.byref(has),
+            C.c_longlong(rng.choice([0, 0, 50, 200])), C.c_longlong(rng.choice([0, 0, 7, 40])),
+            rgs, C.byref(obj), C.byref(has),
             C.byref(vis), C.byref(ab), C.byref(tt), st)
         assert vis.value == o.visited and bool(ab.value) == (not o.optimal)
         if o.status == 0 and has.value and not (ab.value and floor > obj.value):
