@@ -415,6 +415,50 @@ struct Groups {
   bool drift;  // check_drift: a += on this lane's groups would not round-trip
 };
 
+#ifndef HPK_SELECT_UPDATES
+// Only the owner lane's slot changes: a warp-uniform branch on the slot (group
+// >> 5) and a one-lane predicated update, instead of branch-free selects on
+// both slots of every lane (same values: the other lanes' sums are untouched,
+// which x + 0.0 also gave). -DHPK_SELECT_UPDATES restores the select form.
+template <bool DRIFT>
+__device__ __forceinline__ void add_unit(const PView& P, Groups& g, int lane, int grp, double up,
+                                         double um) {
+  const int ks = grp >> 5;  // warp-uniform
+  const bool me = (grp & 31) == lane;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    if (k == ks && me) {
+      if (DRIFT && g.gc[k] > 0) {
+        // the reference's -= after this += must give back the same sum
+        // (grouping.cpp:184-198); a new group (push_back) cannot drift
+        const double yp = g.gp[k] + up, ym = g.gm[k] + um;
+        g.drift = g.drift || (yp - up) != g.gp[k] || (ym - um) != g.gm[k];
+      }
+      g.gp[k] += up;
+      g.gm[k] += um;
+      g.gc[k] += 1;
+      g.f0[k] = g.f1[k];
+      g.f1[k] = P.f[g.gc[k] + 1];
+    }
+  }
+}
+
+__device__ __forceinline__ void remove_unit(const PView& P, Groups& g, int lane, int grp,
+                                            double up, double um) {
+  const int ks = grp >> 5;
+  const bool me = (grp & 31) == lane;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    if (k == ks && me) {
+      g.gp[k] -= up;
+      g.gm[k] -= um;
+      g.gc[k] -= 1;
+      g.f1[k] = g.f0[k];
+      g.f0[k] = P.f[g.gc[k]];
+    }
+  }
+}
+#else
 template <bool DRIFT>
 __device__ __forceinline__ void add_unit(const PView& P, Groups& g, int lane, int grp, double up,
                                          double um) {
@@ -449,6 +493,8 @@ __device__ __forceinline__ void remove_unit(const PView& P, Groups& g, int lane,
     g.f0[k] = o ? fp : g.f0[k];
   }
 }
+
+#endif
 
 __device__ __forceinline__ void groups_init(const PView& P, Groups& g) {
   g.drift = false;
