@@ -179,7 +179,7 @@ typedef struct hpk_grouping_result {
   long long exact_checks;            /* child checks inside the filter margin (exact path) */
 } hpk_grouping_result;
 
-#define HPK_ALL_DEVICES (-2)
+#define HPK_ALL_DEVICES (-2) /* batches worth < ~100 K budgeted visits stay on device 0 */
 typedef struct hpk_search_config {
   int device;            /* CUDA ordinal (-1: current; HPK_ALL_DEVICES: every visible
                             device, problems longest-first to the least-loaded one) */

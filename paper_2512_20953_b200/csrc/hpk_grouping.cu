@@ -3914,7 +3914,11 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     return fail(5, "hetplan_b200: no CUDA device visible; the B200 planner has no CPU "
                    "fallback");
   if (cfg.device == HPK_ALL_DEVICES) {
-    if (ndev > 1) return search_all_devices(problems, n_problems, results, cfg, ndev);
+    // a batch worth less than ~100 K budgeted visits stays on one device: the
+    // extra host threads and launches would cost more than the split saves
+    double total = 0;
+    for (int i = 0; i < n_problems; ++i) total += search_cost(problems[i]);
+    if (ndev > 1 && total > 5e6) return search_all_devices(problems, n_problems, results, cfg, ndev);
     cfg.device = 0;
   }
   if (cfg.device < 0) {

@@ -40,3 +40,26 @@ def test_plan_uses_every_device_and_matches_reference(product_lib, golden_plans,
     got = product_lib.plan_json(w.cluster_json(), w.model_json(), w.max_layers)
     assert got == golden_plans["cfg4"]["json"]
     assert engine.timing().devices_used == min(engine.device_count(), 4)  # 4 TP dims
+
+
+def test_concurrent_plan_calls_are_reentrant(product_lib, golden_plans):
+    """The reference C ABI is reentrant (no static mutable state, thread-local
+    error); the B200 library keeps that: per-device contexts with
+    their own stream and lock, thread-local errors and timings. Four host
+    threads planning at once (ctypes releases the GIL) get the reference's
+    plans."""
+    import threading
+    names = ["cfg1", "cfg2", "cfg3", "cfg1", "cfg2", "cfg3", "cfg4", "cfg2"]
+    out = [None] * len(names)
+
+    def work(i):
+        w = configs.get(names[i])
+        out[i] = product_lib.plan_json(w.cluster_json(), w.model_json(), w.max_layers)
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(len(names))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for nm, js in zip(names, out):
+        assert js == golden_plans[nm]["json"], nm
