@@ -612,7 +612,7 @@ struct RunOut {
 // state loaded by the caller; cut = its cutoff) — a feasible leaf above the
 // cutoff joins it — and the run keeps its own top_k candidates in sm->r*,
 // written to rec at the end (grouping.cpp:117-132).
-template <bool TOPK, bool DRIFT>
+template <bool TOPK, bool DRIFT, bool PFX>
 __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, double C,
                               long long cap, WarpSmem* sm, int lane, int* err,
                               unsigned long long deadline, unsigned long long* prof,
@@ -638,7 +638,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
   if (prof) pc0 = clock64();
   const int n = P.n;
   const int du = E->du;
-  const bool prefix = E->kind == KIND_PREFIX;
+  const bool prefix = PFX;  // E->kind == KIND_PREFIX (the caller dispatches)
   RunOut o;
   o.visits = 0;
   o.m = -1.0;
@@ -802,7 +802,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
         const int lim = d == dtop && hil < G ? hil : G;  // last child of this node in the segment
         int count = lim + 1 - c0;
         bool end_hit = false;
-        if (match == d) {  // dend == n here
+        if ((PFX && match == d)) {  // dend == n here
           if (ec - c0 < count) {
             count = ec - c0 > 0 ? ec - c0 : 0;
             end_hit = true;
@@ -990,12 +990,12 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
         G = (w0 >> 16) & 255;
         remove_unit(P, g, lane, grp, up, um);
         sums_ok = false;
-        if (match > d) match = d;
-        if (match == d) ec = sm->endp[d];
+        if (PFX && match > d) match = d;
+        if ((PFX && match == d)) ec = sm->endp[d];
         HPK_PC(6, 1);
         continue;
       }
-      if (match == d) {
+      if ((PFX && match == d)) {
         if (c > ec || (c == ec && d + 1 == dend)) {
           o.finished = true;
           break;
@@ -1057,7 +1057,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
         const int lim = d == dtop && hil < G ? hil : G;
         if (k > lim + 1 - c) k = lim + 1 - c;
         if ((long long)k > cap - o.visits) k = (int)(cap - o.visits);
-        if (match == d) {
+        if ((PFX && match == d)) {
           // the end node (d+1 == dend) is not visited; the end path's child is,
           // and its prune is the ancestor prune a* (grouping.cpp:162,169)
           const int kl = (d + 1 == dend) ? ec - c : ec - c + 1;
@@ -1079,7 +1079,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
         const bool pass = exact_passes(P, g, Gc, d + 1, cut);
         remove_unit(P, g, lane, c, up, um);
         if (!pass) {
-          if (match == d && c == ec && o.a_star < 0) o.a_star = d + 1;
+          if ((PFX && match == d) && c == ec && o.a_star < 0) o.a_star = d + 1;
           ++c;
           continue;
         }
@@ -1112,9 +1112,9 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
       }
       add_unit<DRIFT>(P, g, lane, c, up, um);
       if (c == G) ++G;
-      if (match == d && c == ec) match = d + 1;
+      if ((PFX && match == d) && c == ec) match = d + 1;
       ++d;
-      if (G > 63 && d < n) {  // an internal node with 64 groups: 65 children
+      if (MAXN > 64 && G > 63 && d < n) {  // an internal node with 64 groups: 65 children
         o.overflow = true;
         o.finished = true;
         break;
@@ -1126,7 +1126,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
       sums_ok = false;
       up = P.p[d];
       um = P.m[d];
-      if (match == d) ec = sm->endp[d];
+      if ((PFX && match == d)) ec = sm->endp[d];
       HPK_PC(5, 1);
     }
   }
@@ -2959,11 +2959,14 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
           rec->ntin = item.ntv;
         }
         __syncwarp();
-#define HPK_RUN(TK, DR, WS, TKV, FL, REC)                                                  \
-  run_segment<TK, DR>(PV, E, E, C, item.cap, WS, lane, kp.err, kp.deadline_ns,              \
+#define HPK_RUN3(TK, DR, PF, WS, TKV, FL, REC)                                             \
+  run_segment<TK, DR, PF>(PV, E, E, C, item.cap, WS, lane, kp.err, kp.deadline_ns,          \
                       (kp.trace >= 2 && kp.trace < 5) ? kp.prof : nullptr,                  \
                       stoppable ? kp.stop : nullptr, kp.minq,                               \
                       stoppable && kp.wave_ns ? wave_t0 + kp.wave_ns : 0ull, TKV, FL, REC)
+#define HPK_RUN(TK, DR, WS, TKV, FL, REC)                                                  \
+  (E->kind == KIND_PREFIX ? HPK_RUN3(TK, DR, true, WS, TKV, FL, REC)                       \
+                          : HPK_RUN3(TK, DR, false, WS, TKV, FL, REC))
         // the drift-checking instantiation only for problems outside the
         // exact-sum contract: the common case carries no extra instructions
         o = PV.check_drift ? HPK_RUN(true, true, ws, tk, S.seed_obj, rec)
@@ -2972,6 +2975,7 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
         o = PV.check_drift ? HPK_RUN(false, true, wsm + warp, 1, 0.0, nullptr)
                            : HPK_RUN(false, false, wsm + warp, 1, 0.0, nullptr);
 #undef HPK_RUN
+#undef HPK_RUN3
       }
       int* pcv = list_arr(kp, p, S.cur, 1);
       int* cnt = list_arr(kp, p, S.cur, 2);
