@@ -221,7 +221,6 @@ struct KParams {
   int* active;        // problems still running
   int* err;           // watchdog flags
   int* stop;          // run phase: the queue has drained (capped runs stop early)
-  long long minq;     // ... after at least this many visits (0: never stop early)
   unsigned long long wave_ns;  // run-phase time slice (0: none): later runs stop and split
   int runners;        // warps per CTA that run segments (experiment knob; default all)
   int ranges;         // split pieces are sibling ranges (1) or single siblings (0)
@@ -297,6 +296,7 @@ struct WarpSmem {
   double robj[KW];
   int rG[KW];
   int nT, rn;  // (the candidates' RGS rows live in the run's CandRec, global)
+  unsigned long long wave_end;  // the current run's time-slice end (0: none)
   int staged;  // problem whose tables tp..tRM hold (-1: none)
 };
 
@@ -605,7 +605,7 @@ struct RunOut {
 // entry :161-169) and none is entered.
 //
 // stopf (optional): set once the wave's run queue has drained; a capped run
-// then stops at its next check after >= minq visits and is split like a run
+// then stops at its next check after the time slice and is split like a run
 // that hit its cap, so no warp idles behind the wave's longest run.
 //
 // TOPK (top_k = tk > 1): the cutoff follows the state vector sm->T (entering
@@ -615,9 +615,12 @@ struct RunOut {
 template <bool TOPK, bool DRIFT, bool PFX>
 __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, double C,
                               long long cap, WarpSmem* sm, int lane, int* err,
-                              unsigned long long deadline, unsigned long long* prof,
-                              const int* stopf, long long minq, unsigned long long wave_end,
-                              int tk, double floor_, CandRec* rec) {
+                              const unsigned long long* deadline_slot,
+                              unsigned long long* prof, const int* stopf, int tk, double floor_,
+                              CandRec* rec) {
+  // (the watchdog deadline and the wave's time slice end, sm->wave_end, are
+  // read where they are checked — every 1024 / 32 iterations — instead of
+  // occupying registers through the hot loop)
   // prof (trace >= 2): [0] run cycles [1] leaf batches [2] leaves [3] loop iterations
   //   [4] single checks [5] descends [6] pops [7] prune skips [8] children skipped
   //   [9] exact fallbacks [10] mask computations
@@ -773,7 +776,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
           unsigned long long now;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
           now = __shfl_sync(HPK_FULL_MASK, now, 0);
-          if (now > deadline) {
+          if (now > *((volatile const unsigned long long*)deadline_slot)) {
             if (lane == 0) atomicOr(err, 2);
             o.finished = true;
             break;
@@ -783,10 +786,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
           const int s = shfl(stop_pending, 0);  // the queue has drained
           if (lane == 0) stop_pending = *((volatile const int*)stopf);
           if (s) {
-            if (minq > 0) {
-              const long long lim = o.visits > minq ? o.visits : minq;
-              if (lim < cap) cap = lim;
-            }
+            const unsigned long long wave_end = sm->wave_end;
             if (wave_end != 0) {  // ... and the wave's time slice is over: stop
               unsigned long long now;
               asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
@@ -2943,6 +2943,9 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
       const PView PV = stage_problem(P, wsm + warp, lane, p);
       // (a PREFIX re-run must end at its end marker: it is never split)
       const bool stoppable = !E->capped && !E->uncapped && E->kind != KIND_PREFIX;
+      if (lane == 0)
+        wsm[warp].wave_end = stoppable && kp.wave_ns ? wave_t0 + kp.wave_ns : 0ull;
+      __syncwarp();
       const int tk = P.top_k;
       RunOut o;
       if (tk > 1) {
@@ -2960,10 +2963,9 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
         }
         __syncwarp();
 #define HPK_RUN3(TK, DR, PF, WS, TKV, FL, REC)                                             \
-  run_segment<TK, DR, PF>(PV, E, E, C, item.cap, WS, lane, kp.err, kp.deadline_ns,          \
-                      (kp.trace >= 2 && kp.trace < 5) ? kp.prof : nullptr,                  \
-                      stoppable ? kp.stop : nullptr, kp.minq,                               \
-                      stoppable && kp.wave_ns ? wave_t0 + kp.wave_ns : 0ull, TKV, FL, REC)
+  run_segment<TK, DR, PF>(PV, E, E, C, item.cap, WS, lane, kp.err, kp.deadline_slot,       \
+                          (kp.trace >= 2 && kp.trace < 5) ? kp.prof : nullptr,              \
+                          stoppable ? kp.stop : nullptr, TKV, FL, REC)
 #define HPK_RUN(TK, DR, WS, TKV, FL, REC)                                                  \
   (E->kind == KIND_PREFIX ? HPK_RUN3(TK, DR, true, WS, TKV, FL, REC)                       \
                           : HPK_RUN3(TK, DR, false, WS, TKV, FL, REC))
@@ -4233,7 +4235,6 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
     kp.active = c.active;
     kp.err = c.active + 1;
     kp.stop = c.active + 7;
-    kp.minq = 0;
     kp.runners = WARPS_PER_BLOCK;
     kp.ranges = ranges;
     // run-phase time slice: 300 us (HPK_WAVE_US overrides; 0 = none)
