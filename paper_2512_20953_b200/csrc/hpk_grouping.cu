@@ -409,8 +409,26 @@ constexpr double kEps52 = 2.220446049250313e-16;  // 2^-52
 // taken. Under the wave engine's contract every sum is exact, so x + 0.0,
 // 0.0 + up (push_back) and up - up (pop_back) equal the reference's values
 // (grouping.cpp:180-198) bit for bit.
+// The Eq. (2) factors of a slot: f[gc] (current members) and f[gc + 1] (one
+// more), cached in registers and rotated on every += / -=. -DHPK_NO_FCACHE
+// reads them from the staged table where used instead: fewer registers and
+// spills, but measured 2 % slower on the cfg5 sweep (0.655 vs 0.640 s).
+#ifndef HPK_NO_FCACHE
+#define HPK_FCACHE 1
+#endif
+#ifdef HPK_FCACHE
+#define HPK_F0(P, g, k) ((g).f0[k])
+#define HPK_F1(P, g, k) ((g).f1[k])
+#else
+#define HPK_F0(P, g, k) ((P).f[(g).gc[k]])
+#define HPK_F1(P, g, k) ((P).f[(g).gc[k] + 1])
+#endif
+
 struct Groups {
-  double gp[2], gm[2], f0[2], f1[2];
+  double gp[2], gm[2];
+#ifdef HPK_FCACHE
+  double f0[2], f1[2];  // cached Eq. (2) factors f[gc], f[gc + 1]
+#endif
   int gc[2];
   bool drift;  // check_drift: a += on this lane's groups would not round-trip
 };
@@ -437,8 +455,10 @@ __device__ __forceinline__ void add_unit(const PView& P, Groups& g, int lane, in
       g.gp[k] += up;
       g.gm[k] += um;
       g.gc[k] += 1;
+#ifdef HPK_FCACHE
       g.f0[k] = g.f1[k];
       g.f1[k] = P.f[g.gc[k] + 1];
+#endif
     }
   }
 }
@@ -453,8 +473,10 @@ __device__ __forceinline__ void remove_unit(const PView& P, Groups& g, int lane,
       g.gp[k] -= up;
       g.gm[k] -= um;
       g.gc[k] -= 1;
+#ifdef HPK_FCACHE
       g.f1[k] = g.f0[k];
       g.f0[k] = P.f[g.gc[k]];
+#endif
     }
   }
 }
@@ -475,8 +497,12 @@ __device__ __forceinline__ void add_unit(const PView& P, Groups& g, int lane, in
     g.gm[k] += o ? um : 0.0;
     g.gc[k] += o ? 1 : 0;
     const double fn = P.f[g.gc[k] + 1];
+#ifdef HPK_FCACHE
     g.f0[k] = o ? g.f1[k] : g.f0[k];
     g.f1[k] = o ? fn : g.f1[k];
+#else
+    (void)fn;
+#endif
   }
 }
 
@@ -489,8 +515,12 @@ __device__ __forceinline__ void remove_unit(const PView& P, Groups& g, int lane,
     g.gm[k] -= o ? um : 0.0;
     g.gc[k] -= o ? 1 : 0;
     const double fp = P.f[g.gc[k]];
+#ifdef HPK_FCACHE
     g.f1[k] = o ? g.f0[k] : g.f1[k];
     g.f0[k] = o ? fp : g.f0[k];
+#else
+    (void)fp;
+#endif
   }
 }
 
@@ -503,8 +533,10 @@ __device__ __forceinline__ void groups_init(const PView& P, Groups& g) {
     g.gp[k] = 0;
     g.gm[k] = 0;
     g.gc[k] = 0;
+#ifdef HPK_FCACHE
     g.f0[k] = P.f[0];
     g.f1[k] = P.f[1];
+#endif
   }
 }
 
@@ -512,7 +544,7 @@ __device__ __forceinline__ void groups_init(const PView& P, Groups& g) {
 // group (grouping.cpp:103-108); an empty slot has gp = 0 and f[0] = 0.
 __device__ __forceinline__ double slot_eff(const PView& P, const Groups& g, int k) {
   (void)P;
-  return g.gp[k] * g.f0[k];
+  return g.gp[k] * HPK_F0(P, g, k);
 }
 __device__ __forceinline__ double slot_def(const PView& P, const Groups& g, int k) {
   const double d = P.min_mem - g.gm[k];
@@ -855,7 +887,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
           for (int k = 0; k < 2; ++k) {
             const int ch = lane + 32 * k;
             const bool isnew = ch == G;  // new singleton group (the slot is empty)
-            const double eff_new = (g.gp[k] + up) * g.f1[k];
+            const double eff_new = (g.gp[k] + up) * HPK_F1(P, g, k);
             const double mem_new = g.gm[k] + um;
             const int others_inf = n_inf - (inf_k[k] ? 1 : 0);
             const double other_min = (!isnew && ch == i1) ? m2 : m1;
@@ -1022,8 +1054,8 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
           const int ci = lane + 32 * k;
-          const double eff_old = g.gp[k] * g.f0[k];
-          const double eff_new = (g.gp[k] + up) * g.f1[k];
+          const double eff_old = g.gp[k] * HPK_F0(P, g, k);
+          const double eff_new = (g.gp[k] + up) * HPK_F1(P, g, k);
           const double d0 = mm_ - g.gm[k];
           const double def_old = (g.gc[k] > 0 && d0 > 0.0) ? d0 : 0.0;
           const double d1 = mm_ - (g.gm[k] + um);
@@ -1088,8 +1120,8 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
       if (!sums_ok) {  // (after a pop) the lanes recompute their children's sums
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-          const double eff_old = g.gp[k] * g.f0[k];
-          const double eff_new = (g.gp[k] + up) * g.f1[k];
+          const double eff_old = g.gp[k] * HPK_F0(P, g, k);
+          const double eff_new = (g.gp[k] + up) * HPK_F1(P, g, k);
           const double d0 = mm_ - g.gm[k];
           const double def_old = (g.gc[k] > 0 && d0 > 0.0) ? d0 : 0.0;
           const double d1 = mm_ - (g.gm[k] + um);
