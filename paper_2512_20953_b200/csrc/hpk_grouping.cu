@@ -438,13 +438,13 @@ struct Groups {
 // >> 5) and a one-lane predicated update, instead of branch-free selects on
 // both slots of every lane (same values: the other lanes' sums are untouched,
 // which x + 0.0 also gave). -DHPK_SELECT_UPDATES restores the select form.
-template <bool DRIFT>
+template <bool DRIFT, int NS = 2>
 __device__ __forceinline__ void add_unit(const PView& P, Groups& g, int lane, int grp, double up,
                                          double um) {
   const int ks = grp >> 5;  // warp-uniform
   const bool me = (grp & 31) == lane;
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < NS; ++k) {
     if (k == ks && me) {
       if (DRIFT && g.gc[k] > 0) {
         // the reference's -= after this += must give back the same sum
@@ -463,12 +463,13 @@ __device__ __forceinline__ void add_unit(const PView& P, Groups& g, int lane, in
   }
 }
 
+template <int NS = 2>
 __device__ __forceinline__ void remove_unit(const PView& P, Groups& g, int lane, int grp,
                                             double up, double um) {
   const int ks = grp >> 5;
   const bool me = (grp & 31) == lane;
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < NS; ++k) {
     if (k == ks && me) {
       g.gp[k] -= up;
       g.gm[k] -= um;
@@ -644,7 +645,10 @@ struct RunOut {
 // state loaded by the caller; cut = its cutoff) — a feasible leaf above the
 // cutoff joins it — and the run keeps its own top_k candidates in sm->r*,
 // written to rec at the end (grouping.cpp:117-132).
-template <bool TOPK, bool DRIFT, bool PFX>
+// NS: group slots per lane in use — 1 when the problem has at most 32 units
+// (every child index and group then fits lane slot 0, so slot 1 stays empty
+// and its work compiles out), else 2.
+template <bool TOPK, bool DRIFT, bool PFX, int NS>
 __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, double C,
                               long long cap, WarpSmem* sm, int lane, int* err,
                               const unsigned long long* deadline_slot,
@@ -704,7 +708,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
   if (lane == 0) sm->lvl[0] = 0;
   for (int i = 0; i + 1 < du; ++i) {  // the range's parent node: units 0..du-2
     const int grp = sm->path[i];
-    add_unit<DRIFT>(P, g, lane, grp, P.p[i], P.m[i]);
+    add_unit<DRIFT, NS>(P, g, lane, grp, P.p[i], P.m[i]);
     if (grp == G) ++G;
     if (lane == 0) sm->lvl[i + 1] = (unsigned)G << 16;
   }
@@ -728,7 +732,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
   if (single) {  // enter the segment root u
     const int i = du - 1;
     const int grp = sm->path[i];
-    add_unit<DRIFT>(P, g, lane, grp, P.p[i], P.m[i]);
+    add_unit<DRIFT, NS>(P, g, lane, grp, P.p[i], P.m[i]);
     if (grp == G) ++G;
     if (lane == 0) sm->lvl[du] = (unsigned)G << 16;
     o.visits = 1;
@@ -742,7 +746,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
       bool infeas = false;
       double z = INFINITY;
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
+      for (int k = 0; k < NS; ++k) {
         if (g.gc[k] > 0) {
           if (g.gm[k] < P.min_mem) infeas = true;
           const double e = slot_eff(P, g, k);
@@ -772,8 +776,8 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
     }
   }
   {
-    const double le = slot_eff(P, g, 0) + slot_eff(P, g, 1);
-    const double ld = slot_def(P, g, 0) + slot_def(P, g, 1);
+    const double le = NS == 2 ? slot_eff(P, g, 0) + slot_eff(P, g, 1) : slot_eff(P, g, 0);
+    const double ld = NS == 2 ? slot_def(P, g, 0) + slot_def(P, g, 1) : slot_def(P, g, 0);
     Sd = warp_sum_approx(le);
     Dd = warp_sum_approx(ld);
   }
@@ -847,16 +851,16 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
           end_hit = false;
         }
         if (count > 0) {
-          bool inf_k[2];
-          double eff_k[2];
+          bool inf_k[2] = {false, false};
+          double eff_k[2] = {INFINITY, INFINITY};
 #pragma unroll
-          for (int k = 0; k < 2; ++k) {
+          for (int k = 0; k < NS; ++k) {
             const bool valid = g.gc[k] > 0;
             inf_k[k] = valid && g.gm[k] < mm_;
             eff_k[k] = valid ? slot_eff(P, g, k) : INFINITY;
           }
           const int n_inf = __popc(__ballot_sync(HPK_FULL_MASK, inf_k[0])) +
-                            __popc(__ballot_sync(HPK_FULL_MASK, inf_k[1]));
+                            (NS == 2 ? __popc(__ballot_sync(HPK_FULL_MASK, inf_k[1])) : 0);
           // min1 / idx1 / min2 over existing groups. Effective powers are
           // non-negative doubles (empty slots: +inf), whose bit patterns order
           // like the values: two 32-bit redux.sync per 64-bit min, exact.
@@ -865,14 +869,14 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
           const unsigned long long m1b = warp_min_u64(eb0 < eb1 ? eb0 : eb1);
           const double m1 = __longlong_as_double((long long)m1b);
           const unsigned bz0 = __ballot_sync(HPK_FULL_MASK, eb0 == m1b);
-          const unsigned bz1 = __ballot_sync(HPK_FULL_MASK, eb1 == m1b);
+          const unsigned bz1 = NS == 2 ? __ballot_sync(HPK_FULL_MASK, eb1 == m1b) : 0u;
           const int i1 = bz0 ? __ffs(bz0) - 1 : 31 + __ffs(bz1);  // lowest index attaining it
           const unsigned long long x0 = lane == i1 ? ~0ull : eb0;
           const unsigned long long x1 = lane + 32 == i1 ? ~0ull : eb1;
           const double m2 = __longlong_as_double((long long)warp_min_u64(x0 < x1 ? x0 : x1));
           if (DRIFT) {  // every visited leaf child does += / -= on its group
 #pragma unroll
-            for (int k = 0; k < 2; ++k) {
+            for (int k = 0; k < NS; ++k) {
               const int ch = lane + 32 * k;
               if (ch >= c0 && ch < c0 + count && ch < G &&
                   (((g.gp[k] + up) - up) != g.gp[k] || ((g.gm[k] + um) - um) != g.gm[k]))
@@ -880,11 +884,11 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
             }
           }
           // each lane evaluates the children it owns (c = lane, lane+32)
-          double obj_s[2];
-          int gc_s[2];
-          bool fe_s[2];
+          double obj_s[2] = {-1.0, -1.0};
+          int gc_s[2] = {0, 0};
+          bool fe_s[2] = {false, false};
 #pragma unroll
-          for (int k = 0; k < 2; ++k) {
+          for (int k = 0; k < NS; ++k) {
             const int ch = lane + 32 * k;
             const bool isnew = ch == G;  // new singleton group (the slot is empty)
             const double eff_new = (g.gp[k] + up) * HPK_F1(P, g, k);
@@ -911,7 +915,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
               o.m = mx > o.m ? mx : o.m;
               if (mx > cut) {  // the cutoff state takes every leaf above the cutoff
 #pragma unroll
-                for (int k = 0; k < 2; ++k) {
+                for (int k = 0; k < NS; ++k) {
                   unsigned b = __ballot_sync(HPK_FULL_MASK, fe_s[k] && obj_s[k] > cut);
                   while (b) {
                     const int l = __ffs(b) - 1;
@@ -929,7 +933,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
               const int kg = rn >= tk ? sm->rG[tk - 1] : 0;
               bool any = false;
 #pragma unroll
-              for (int k = 0; k < 2; ++k) {
+              for (int k = 0; k < NS; ++k) {
                 unsigned b = __ballot_sync(HPK_FULL_MASK, fe_s[k] && (rn < tk || rank_better(obj_s[k], gc_s[k], ko, kg)));
                 if (b && !any) {
                   __syncwarp();  // lane 0's path spills are visible
@@ -1020,7 +1024,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
         const int grp = w0 & 255;
         c = (w0 >> 8) & 255;
         G = (w0 >> 16) & 255;
-        remove_unit(P, g, lane, grp, up, um);
+        remove_unit<NS>(P, g, lane, grp, up, um);
         sums_ok = false;
         if (PFX && match > d) match = d;
         if ((PFX && match == d)) ec = sm->endp[d];
@@ -1050,9 +1054,9 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
       if (mc != cut) {
         const double Rn = P.R[d + 1], RMn = P.RM[d + 1];
         const bool hc = cut >= 0;
-        bool pr[2], ps[2];
+        bool pr[2] = {true, true}, ps[2] = {false, false};  // slot 1 unused when NS == 1
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < NS; ++k) {
           const int ci = lane + 32 * k;
           const double eff_old = g.gp[k] * HPK_F0(P, g, k);
           const double eff_new = (g.gp[k] + up) * HPK_F1(P, g, k);
@@ -1074,9 +1078,10 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
           ps[k] = !pr[k] && (!hc || A - mb >= cut) && (lD[k] + md <= RMn);
         }
         mp = (unsigned long long)__ballot_sync(HPK_FULL_MASK, ps[0]) |
-             ((unsigned long long)__ballot_sync(HPK_FULL_MASK, ps[1]) << 32);
+             (NS == 2 ? ((unsigned long long)__ballot_sync(HPK_FULL_MASK, ps[1]) << 32) : 0ull);
         mr = (unsigned long long)__ballot_sync(HPK_FULL_MASK, pr[0]) |
-             ((unsigned long long)__ballot_sync(HPK_FULL_MASK, pr[1]) << 32);
+             (NS == 2 ? ((unsigned long long)__ballot_sync(HPK_FULL_MASK, pr[1]) << 32)
+                      : 0xffffffff00000000ull);
         mc = cut;
         sums_ok = true;
         HPK_PC(10, 1);
@@ -1106,10 +1111,10 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
       HPK_PC(4, 1);
       if (!(mp & bit)) {  // inside the error margin: the exact serial check
         o.exact += 1;
-        add_unit<DRIFT>(P, g, lane, c, up, um);
+        add_unit<DRIFT, NS>(P, g, lane, c, up, um);
         const int Gc = c == G ? G + 1 : G;
         const bool pass = exact_passes(P, g, Gc, d + 1, cut);
-        remove_unit(P, g, lane, c, up, um);
+        remove_unit<NS>(P, g, lane, c, up, um);
         if (!pass) {
           if ((PFX && match == d) && c == ec && o.a_star < 0) o.a_star = d + 1;
           ++c;
@@ -1119,7 +1124,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
       // ---- PASS: descend into child c
       if (!sums_ok) {  // (after a pop) the lanes recompute their children's sums
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < NS; ++k) {
           const double eff_old = g.gp[k] * HPK_F0(P, g, k);
           const double eff_new = (g.gp[k] + up) * HPK_F1(P, g, k);
           const double d0 = mm_ - g.gm[k];
@@ -1131,8 +1136,8 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
         }
         sums_ok = true;
       }
-      const double Sn = shfl(c < 32 ? lS[0] : lS[1], c & 31);
-      const double Dn = shfl(c < 32 ? lD[0] : lD[1], c & 31);
+      const double Sn = shfl((NS == 1 || c < 32) ? lS[0] : lS[1], c & 31);
+      const double Dn = shfl((NS == 1 || c < 32) ? lD[0] : lD[1], c & 31);
       if (lane == 0) {  // spill this level
         sm->lvl[d] = (unsigned)c | ((unsigned)(c + 1) << 8) | ((unsigned)G << 16);
         sm->path[d] = (uint8_t)c;
@@ -1142,7 +1147,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
         sm->mprune[d] = mr;
         sm->mcut[d] = mc;
       }
-      add_unit<DRIFT>(P, g, lane, c, up, um);
+      add_unit<DRIFT, NS>(P, g, lane, c, up, um);
       if (c == G) ++G;
       if ((PFX && match == d) && c == ec) match = d + 1;
       ++d;
@@ -2994,10 +2999,13 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
           rec->ntin = item.ntv;
         }
         __syncwarp();
+#define HPK_RUN4(TK, DR, PF, NS, WS, TKV, FL, REC)                                         \
+  run_segment<TK, DR, PF, NS>(PV, E, E, C, item.cap, WS, lane, kp.err, kp.deadline_slot,   \
+                              (kp.trace >= 2 && kp.trace < 5) ? kp.prof : nullptr,          \
+                              stoppable ? kp.stop : nullptr, TKV, FL, REC)
 #define HPK_RUN3(TK, DR, PF, WS, TKV, FL, REC)                                             \
-  run_segment<TK, DR, PF>(PV, E, E, C, item.cap, WS, lane, kp.err, kp.deadline_slot,       \
-                          (kp.trace >= 2 && kp.trace < 5) ? kp.prof : nullptr,              \
-                          stoppable ? kp.stop : nullptr, TKV, FL, REC)
+  ((MAXN <= 64 && PV.n <= 32) ? HPK_RUN4(TK, DR, PF, 1, WS, TKV, FL, REC)                  \
+                              : HPK_RUN4(TK, DR, PF, 2, WS, TKV, FL, REC))
 #define HPK_RUN(TK, DR, WS, TKV, FL, REC)                                                  \
   (E->kind == KIND_PREFIX ? HPK_RUN3(TK, DR, true, WS, TKV, FL, REC)                       \
                           : HPK_RUN3(TK, DR, false, WS, TKV, FL, REC))
@@ -3010,6 +3018,7 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
                            : HPK_RUN(false, false, wsm + warp, 1, 0.0, nullptr);
 #undef HPK_RUN
 #undef HPK_RUN3
+#undef HPK_RUN4
       }
       int* pcv = list_arr(kp, p, S.cur, 1);
       int* cnt = list_arr(kp, p, S.cur, 2);
