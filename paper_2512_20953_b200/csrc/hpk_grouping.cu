@@ -47,6 +47,9 @@ namespace cg = cooperative_groups;
 #ifndef HPK_WAVE_NS
 #define HPK_WAVE_NS 300000ull // run-phase time slice
 #endif
+#ifndef HPK_CHECK_EVERY
+#define HPK_CHECK_EVERY 64    // DFS iterations between stop-flag / time-slice checks (A/B: 32/64/128)
+#endif
 #ifndef HPK_QMUL
 #define HPK_QMUL 4            // run slots per warp per wave
 #endif
@@ -807,8 +810,8 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
 
     while (true) {
       HPK_PC(3, 1);
-      if ((++it & 31) == 0) {
-        if ((it & 1023) == 0) {  // wall-clock watchdog (uniform: lane 0's clock)
+      if ((++it & (HPK_CHECK_EVERY - 1)) == 0) {  // stop flag / time slice
+        if ((it & (32 * HPK_CHECK_EVERY - 1)) == 0) {  // wall-clock watchdog (lane 0's clock)
           unsigned long long now;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
           now = __shfl_sync(HPK_FULL_MASK, now, 0);
