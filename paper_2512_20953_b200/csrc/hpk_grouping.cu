@@ -627,6 +627,7 @@ struct RunOut {
   bool overflow;  // reached an internal node with more than 63 groups (lanes own
                   // groups g, g+32): the problem goes to the serial replica
   bool drift;     // check_drift problems: some group sum would not round-trip
+  bool retry;     // NS == 1 run met an internal node with 32 groups: rerun with NS == 2
 };
 
 // DFS of subtree(E.u) in preorder (PREFIX: stopping before E.end), cap visits.
@@ -693,6 +694,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
   o.stop_c = 0;
   o.exact = 0;
   o.overflow = false;
+  o.retry = false;
   o.drift = false;
   if (TOPK && lane == 0) sm->rn = 0;
   if (cap <= 0) {  // budget already exhausted: the reference aborts before entering u
@@ -732,6 +734,11 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
     o.finished = true;
     goto done;
   }
+  if (NS == 1 && G > 31) {  // the parent's children would need lane slot 1
+    o.retry = true;
+    o.finished = true;
+    goto done;
+  }
   if (single) {  // enter the segment root u
     const int i = du - 1;
     const int grp = sm->path[i];
@@ -742,6 +749,11 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
     __syncwarp();
     if (d < n && G > 63) {  // its children would need group slot 64
       o.overflow = true;
+      o.finished = true;
+      goto done;
+    }
+    if (NS == 1 && d < n && G > 31) {
+      o.retry = true;
       o.finished = true;
       goto done;
     }
@@ -1156,6 +1168,11 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
       ++d;
       if (MAXN > 64 && G > 63 && d < n) {  // an internal node with 64 groups: 65 children
         o.overflow = true;
+        o.finished = true;
+        break;
+      }
+      if (NS == 1 && G > 31 && d < n) {  // 33 children: slot 1 needed, rerun with NS == 2
+        o.retry = true;
         o.finished = true;
         break;
       }
@@ -3006,9 +3023,21 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
   run_segment<TK, DR, PF, NS>(PV, E, E, C, item.cap, WS, lane, kp.err, kp.deadline_slot,   \
                               (kp.trace >= 2 && kp.trace < 5) ? kp.prof : nullptr,          \
                               stoppable ? kp.stop : nullptr, TKV, FL, REC)
+// one lane slot while every node holds <= 32 groups (always for <= 32 units;
+// a run that meets more is redone with two slots)
 #define HPK_RUN3(TK, DR, PF, WS, TKV, FL, REC)                                             \
-  ((MAXN <= 64 && PV.n <= 32) ? HPK_RUN4(TK, DR, PF, 1, WS, TKV, FL, REC)                  \
-                              : HPK_RUN4(TK, DR, PF, 2, WS, TKV, FL, REC))
+  [&]() {                                                                                  \
+    if (MAXN <= 64) {                                                                      \
+      RunOut r1 = HPK_RUN4(TK, DR, PF, 1, WS, TKV, FL, REC);                               \
+      if (!r1.retry) return r1;                                                            \
+      if (TK) { /* the entering top-k state again: the first try moved it */               \
+        if (lane < KW) (WS)->T[lane] = item.tv[lane];                                      \
+        if (lane == 0) (WS)->nT = item.ntv;                                                \
+        __syncwarp();                                                                      \
+      }                                                                                    \
+    }                                                                                      \
+    return HPK_RUN4(TK, DR, PF, 2, WS, TKV, FL, REC);                                      \
+  }()
 #define HPK_RUN(TK, DR, WS, TKV, FL, REC)                                                  \
   (E->kind == KIND_PREFIX ? HPK_RUN3(TK, DR, true, WS, TKV, FL, REC)                       \
                           : HPK_RUN3(TK, DR, false, WS, TKV, FL, REC))
