@@ -2,26 +2,33 @@
 // planner: dfs() in P/src/grouping.cpp:135-202 under solve_grouping_topk
 // :269-335; P = /root/reference/proj).
 //
-// Two engines, both on the GPU, both exact (bit-identical winner, visits and
+// Three engines, all on the GPU, all exact (bit-identical winners, visits and
 // optimal flag):
 //
 //  * Wave engine (hpk_wave_kernel): one persistent cooperative kernel searches
 //    a batch of problems. The lexicographic (preorder) DFS is cut into an
-//    ordered list of segments (subtrees). Each wave every warp runs one segment
-//    (a warp-cooperative DFS: lane g owns DP group g) with the front's exact
-//    cutoff and a visit cap; unfinished segments are split speculatively into a
-//    prefix record plus the remainder's subtrees; a per-problem scheduler CTA
-//    then commits the longest prefix of the list whose runs are exact (cutoff
-//    at their position unchanged), applying the budget cut exactly where the
-//    serial DFS would abort. A prefix record whose cutoff turned out stale is
-//    re-run with an end marker; the ancestor it now prunes deletes the pieces
-//    beneath it. Exactness argument and data layout: DESIGN.md.
+//    ordered list of segments (subtrees). Each wave every warp runs segments
+//    (a warp-cooperative DFS: lane g owns DP groups g and g + 32) with the
+//    front's exact cutoff and a visit cap / time slice; unfinished segments are
+//    split speculatively into a prefix record plus the remainder's pieces; a
+//    per-problem scheduler CTA then commits the longest prefix of the list
+//    whose runs are exact (cutoff at their position unchanged), applying the
+//    budget cut exactly where the serial DFS would abort. A prefix record whose
+//    cutoff turned out stale is re-run with an end marker; the ancestor it now
+//    prunes deletes the pieces beneath it. The runner is specialised per
+//    (top_k > 1, drift check, PREFIX segment, lane slots in use). Covers top_k
+//    <= 16, <= 64 units here and <= 128 in the wide build
+//    (hpk_grouping_wide.cu), and non-dyadic sums while no += / -= round trip
+//    drifts. Exactness argument and data layout: DESIGN.md.
+//
+//  * Enumeration engine (hpk_enum_kernel): exhaustive top-1 searches of <= 12
+//    units (the planner path) as an argmax over every leaf, unranked from the
+//    restricted-growth-string index.
 //
 //  * Serial replica (hpk_serial_kernel): one thread per problem replays the
 //    reference DFS statement by statement (including the += / -= group sums
-//    and top_k bookkeeping). Used when a problem is outside the wave engine's
-//    contract (n > 64 units, top_k > 1, or unit powers / memories whose sums
-//    are not exact in fp64 so the reference's sums are path dependent).
+//    and the top_k list). Used for what the wave engine hands back: drifting
+//    sums, a node with more than 64 groups, more than 128 units, top_k > 16.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
