@@ -52,7 +52,7 @@ namespace cg = cooperative_groups;
 #define HPK_SEG_CAP 1024      // visits per segment run per wave
 #endif
 #ifndef HPK_WAVE_NS
-#define HPK_WAVE_NS 300000ull // run-phase time slice
+#define HPK_WAVE_NS 225000ull // run-phase time slice (A/B 200/225/250/300/400 us on the specialised runner)
 #endif
 #ifndef HPK_CHECK_EVERY
 #define HPK_CHECK_EVERY 64    // DFS iterations between stop-flag / time-slice checks (A/B: 32/64/128)
