@@ -51,6 +51,9 @@ namespace cg = cooperative_groups;
 #ifndef HPK_SEG_CAP
 #define HPK_SEG_CAP 1024      // visits per segment run per wave
 #endif
+#ifndef HPK_SEG_CAP_BATCH
+#define HPK_SEG_CAP_BATCH 2048  // ... for batches of more than 16 searches
+#endif
 #ifndef HPK_WAVE_NS
 #define HPK_WAVE_NS 225000ull // run-phase time slice (A/B 200/225/250/300/400 us on the specialised runner)
 #endif
@@ -4207,7 +4210,11 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
   // ---------------- wave engine
   if (!wave_ix.empty()) {
     const int P = (int)wave_ix.size();
-    const long long seg_cap = cfg.segment_cap > 0 ? cfg.segment_cap : HPK_SEG_CAP;
+    // (big batches — a replanning sweep — run longer segments: fewer splits and
+    // list positions for the same work; one plan's few searches need the
+    // shorter cap to spread their fronts)
+    const long long seg_cap = cfg.segment_cap > 0 ? cfg.segment_cap
+                              : (P > 16 ? HPK_SEG_CAP_BATCH : HPK_SEG_CAP);
     // list capacity (ids) and entry-pool capacity per problem; large by default
     // (the list must hold the whole speculative frontier), scaled down so that
     // big batches (cfg5 sweeps) stay within ~4 GB of HBM.
