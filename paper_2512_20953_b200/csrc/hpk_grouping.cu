@@ -58,7 +58,9 @@ namespace cg = cooperative_groups;
 #define HPK_WAVE_NS 225000ull // run-phase time slice (A/B 200/225/250/300/400 us on the specialised runner)
 #endif
 #ifndef HPK_CHECK_EVERY
-#define HPK_CHECK_EVERY 64    // DFS iterations between stop-flag / time-slice checks (A/B: 32/64/128)
+#define HPK_CHECK_EVERY 64    // DFS iterations between stop-flag / time-slice checks (A/B: 32/64/128;
+                              // a clock read every 16 with the flag read after the slice end:
+                              // cfg5 +4 %, cfg4 no gain, profiles/r2_ab_slice_check.txt)
 #endif
 #ifndef HPK_QMUL
 #define HPK_QMUL 4            // run slots per warp per wave
@@ -2968,6 +2970,12 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
     *kp.deadline_slot = kp.deadline_ns;
   }
   if (kp.trace >= 4 && blockIdx.x == 0 && threadIdx.x == 0) kp.prof[11] = 4;  // per-decision trace
+  if (HPK_TRACE_LEVEL == 1 && blockIdx.x == 0 && threadIdx.x == 0) {
+    kp.prof[24] = ~0ull;
+    kp.prof[25] = ~0ull;
+    kp.prof[32] = 0;
+    for (int k = 0; k < 4; ++k) kp.prof[28 + k] = 0;
+  }
   for (int p = blockIdx.x; p < kp.n_problems; p += gridDim.x) init_problem(kp, p);
   gsync(kp.bar);
   kp.deadline_ns = *((volatile unsigned long long*)kp.deadline_slot);
@@ -2989,7 +2997,7 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(wave_t0));
       wave_t0 = __shfl_sync(HPK_FULL_MASK, wave_t0, 0);
     }
-    unsigned long long t_w0 = 0;
+    unsigned long long t_w0 = 0, t_dr = 0, t_x[4] = {0, 0, 0, 0}, t_x0 = 0;
     if (kp.trace && blockIdx.x == 0 && threadIdx.x == 0)
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_w0));
     while (warp < kp.runners) {
@@ -2998,9 +3006,19 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
       it = shfl(it, 0);
       if (it >= qlen) {  // queue drained: tell the runs still going to wrap up
         if (lane == 0) *((volatile int*)kp.stop) = 1;
+        if (HPK_TRACE_LEVEL == 1 && lane == 0) {  // trace: when the queue drained
+          unsigned long long now;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+          atomicMin(kp.prof + 24, now);
+        }
         break;
       }
       const RunItem item = items[it];
+      unsigned long long t_start = 0;
+      if (HPK_TRACE_LEVEL == 1) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+        if (lane == 0) atomicMin(kp.prof + 25, wave_t0);
+      }
       const int p = item.problem;
       const GProb& P = kp.probs[p];
       GState& S = kp.states[p];
@@ -3106,6 +3124,20 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
           pcv[item.pos] = -1;
           cnt[item.pos] = 1;
         }
+        if (HPK_TRACE_LEVEL == 1) {  // trace: end of the wave's stoppable / other runs
+          unsigned long long now;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+          atomicMax(kp.prof + (stoppable ? 29 : 28), now);
+          if (now > wave_t0 + kp.wave_ns + 60000ull && atomicAdd(kp.prof + 32, 1ull) < 6)
+            printf("[hpk-late] wave %d item %d/%d: start %.1f us end %.1f us (own slice start), "
+                   "visits %lld cap %lld finished %d pieces %d stoppable %d kind %d retry-free\n",
+                   wave, it, qlen, (t_start - wave_t0) * 1e-3, (now - wave_t0) * 1e-3,
+                   o.visits, item.cap, (int)o.finished, pieces, (int)stoppable, (int)E->kind);
+          if (!stoppable) {
+            atomicMax(kp.prof + 30, (unsigned long long)o.visits);
+            atomicAdd(kp.prof + 31, 1ull);
+          }
+        }
         atomicAdd((unsigned long long*)&S.runs, 1ull);
         atomicAdd((unsigned long long*)&S.run_visits, (unsigned long long)o.visits);
         if (o.exact) atomicAdd((unsigned long long*)&S.exact_checks, (unsigned long long)o.exact);
@@ -3153,6 +3185,15 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       *((volatile int*)kp.stop) = 0;  // re-armed for the next run phase
+      if (HPK_TRACE_LEVEL == 1) {
+        t_dr = *((volatile unsigned long long*)kp.prof + 24);
+        for (int k = 0; k < 4; ++k) t_x[k] = *((volatile unsigned long long*)kp.prof + 28 + k);
+        kp.prof[24] = ~0ull;
+        for (int k = 0; k < 4; ++k) kp.prof[28 + k] = 0;
+        t_x0 = *((volatile unsigned long long*)kp.prof + 25);
+        kp.prof[25] = ~0ull;
+        kp.prof[32] = 0;
+      }
       unsigned long long now;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
       if (now > kp.deadline_ns) {  // wall-clock watchdog: stop every block
@@ -3170,8 +3211,14 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
     if (kp.trace && kp.trace < 5 && kp.trace_p < 0 && blockIdx.x == 0 && threadIdx.x == 0) {
       unsigned long long t_w2;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_w2));
-      printf("[hpk] wave %d: %d runs, run %.1f us, schedule %.1f us (active %d)\n", wave, qlen,
-             (t_w1 - t_w0) * 1e-3, (t_w2 - t_w1) * 1e-3, *((volatile int*)kp.active));
+      const unsigned long long t_b = t_x0 < t_w0 ? t_x0 : t_w0;  // first warp's start
+      auto rel = [&](unsigned long long t) {
+        return t >= t_b && t != ~0ull ? (double)(t - t_b) * 1e-3 : -1.0;
+      };
+      printf("[hpk] wave %d: %d runs, run %.1f us (queue drained at %.1f us, last sliced run "
+             "%.1f us, last other run %.1f us: %llu of them, max %llu visits), schedule %.1f us "
+             "(active %d)\n", wave, qlen, (t_w1 - t_b) * 1e-3, rel(t_dr), rel(t_x[1]),
+             rel(t_x[0]), t_x[3], t_x[2], (t_w2 - t_w1) * 1e-3, *((volatile int*)kp.active));
     }
     if (*((volatile int*)kp.active) <= 0) break;
     cur ^= 1;
@@ -3664,7 +3711,7 @@ int ensure_ctx(DeviceCtx& c, int device) {
   HPK_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
   HPK_CUDA(cudaEventCreate(&c.ev0));
   HPK_CUDA(cudaEventCreate(&c.ev1));
-  HPK_CUDA(cudaMalloc(&c.active, sizeof(int) * 64));
+  HPK_CUDA(cudaMalloc(&c.active, sizeof(int) * 128));  // [64, 128): trace slots
   HPK_CUDA(cudaMalloc(&c.queues, sizeof(RunQueue) * 2));
   c.device = device;
   return 0;
