@@ -51,6 +51,9 @@ namespace cg = cooperative_groups;
 #ifndef HPK_SEG_CAP
 #define HPK_SEG_CAP 1024      // visits per segment run per wave
 #endif
+#ifndef HPK_CUT_IV_MAX
+#define HPK_CUT_IV_MAX 16  // launches of at most this many searches use cutoff intervals
+#endif
 #ifndef HPK_SEG_CAP_BATCH
 #define HPK_SEG_CAP_BATCH 2048  // ... for batches of more than 16 searches
 #endif
@@ -134,6 +137,9 @@ struct __align__(16) Entry {
   uint8_t du, dend, kind, finished;
   uint8_t has_best, capped, uncapped;
   uint8_t hi;              // the segment is children [u[du-1], hi] of node u[0..du-1)
+  float chi;               // k = 1: the last run is exact for any entering cutoff in
+                           // [its cutoff, chi] (same decisions, so the same run);
+                           // rounded down, so the float only narrows the interval
 };
 
 struct GState {
@@ -239,6 +245,8 @@ struct KParams {
   unsigned long long wave_ns;  // run-phase time slice (0: none): later runs stop and split
   int runners;        // warps per CTA that run segments (experiment knob; default all)
   int ranges;         // split pieces are sibling ranges (1) or single siblings (0)
+  int cut_iv;         // k = 1 runs record their cutoff interval (few problems: the
+                      // latency-bound case; a big batch has almost no stale runs)
   int n_problems;
   int lcap, pcap, qcap, qmax, reserve;
   int qmax_one;       // cap of one problem's share (a lone search floods its list past it)
@@ -640,6 +648,7 @@ struct RunOut {
                   // groups g, g+32): the problem goes to the serial replica
   bool drift;     // check_drift problems: some group sum would not round-trip
   bool retry;     // NS == 1 run met an internal node with 32 groups: rerun with NS == 2
+  double hi;      // k = 1: every entering cutoff in [C, hi] gives this same run
 };
 
 // DFS of subtree(E.u) in preorder (PREFIX: stopping before E.end), cap visits.
@@ -664,7 +673,7 @@ struct RunOut {
 // NS: group slots per lane in use — 1 when the problem has at most 32 units
 // (every child index and group then fits lane slot 0, so slot 1 stays empty
 // and its work compiles out), else 2.
-template <bool TOPK, bool DRIFT, bool PFX, int NS>
+template <bool TOPK, bool DRIFT, bool PFX, int NS, bool CI>
 __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, double C,
                               long long cap, WarpSmem* sm, int lane, int* err,
                               const unsigned long long* deadline_slot,
@@ -708,6 +717,16 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
   o.overflow = false;
   o.retry = false;
   o.drift = false;
+  o.hi = INFINITY;
+  // Cutoff interval (k = 1). A larger entering cutoff C' only changes a run
+  // through a child or node check that PASSED: a prune stays a prune, leaves
+  // are not pruned and the run's own improvements raise both cutoffs alike. So
+  // the run is the same for every C' <= each passed check's value — hl keeps
+  // this lane's minimum of the filter's lower bound A - mb over its passed
+  // children (the value the filter compared with the cutoff), or the cutoff
+  // itself for a check resolved exactly; the commit walk then accepts the run
+  // for an exact cutoff anywhere in [C, min over lanes].
+  double hl = INFINITY;
   if (TOPK && lane == 0) sm->rn = 0;
   if (cap <= 0) {  // budget already exhausted: the reference aborts before entering u
     if (TOPK && lane == 0) rec->n = 0;
@@ -810,7 +829,13 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
   }
   if (single) {  // node check of u itself
     int dec = decide(P, Sd + P.R[d], Dd, d, cut);
-    if (dec == DEC_EXACT) dec = exact_passes(P, g, G, d, cut) ? DEC_PASS : DEC_PRUNE;
+    if (CI && dec == DEC_PASS) {
+      const double lb = (Sd + P.R[d]) - P.mb_abs;
+      hl = lb < hl ? lb : hl;
+    } else if (dec == DEC_EXACT) {
+      dec = exact_passes(P, g, G, d, cut) ? DEC_PASS : DEC_PRUNE;
+      if (CI && dec == DEC_PASS) hl = cut < hl ? cut : hl;
+    }
     if (dec == DEC_PRUNE) {
       if (prefix) o.a_star = du;
       o.finished = true;
@@ -1103,6 +1128,10 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
             g.drift = true;
           pr[k] = !valid || (hc && A + mb < cut) || (lD[k] - md > RMn);
           ps[k] = !pr[k] && (!hc || A - mb >= cut) && (lD[k] + md <= RMn);
+          if (CI && ps[k]) {
+            const double lb = A - mb;
+            hl = lb < hl ? lb : hl;
+          }
         }
         mp = (unsigned long long)__ballot_sync(HPK_FULL_MASK, ps[0]) |
              (NS == 2 ? ((unsigned long long)__ballot_sync(HPK_FULL_MASK, ps[1]) << 32) : 0ull);
@@ -1147,6 +1176,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
           ++c;
           continue;
         }
+        if (CI) hl = cut < hl ? cut : hl;
       }
       // ---- PASS: descend into child c
       if (!sums_ok) {  // (after a pop) the lanes recompute their children's sums
@@ -1202,6 +1232,7 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
 done:
   __syncwarp();
   if (DRIFT) o.drift = __any_sync(HPK_FULL_MASK, g.drift);
+  o.hi = CI ? warp_min(hl) : C;
   if (TOPK) {
     const int rn = sm->rn;
     o.has_best = rn > 0;
@@ -1562,7 +1593,8 @@ __device__ void push_items(const KParams& kp, int queue, int p, const int* ids, 
       for (int k = 0; k < 8; ++k) {
         chat[k] = run;
         if (!topk) run = mj[k] > run ? mj[k] : run;
-        bool exact = ran[k] && cj[k] == chat[k];
+        bool exact = ran[k] && (cj[k] == chat[k] || (!topk && cj[k] < chat[k] &&
+                                                     chat[k] <= pool[ids[head + j0 + k]].chi));
         if (topk && exact && j0 + k - base == fi_rel) {  // the improver: compare the vectors
           const CandRec& r = crec[ids[head + j0 + k]];
           bool same = r.ntin == sh->ntv;
@@ -1727,7 +1759,8 @@ __device__ void push_tile(const KParams& kp, int p, int t, int queue, int wave, 
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         if (j0 + k < hi) {
-          const bool exact = ran[k] && cj[k] == run;
+          const bool exact =
+              ran[k] && (cj[k] == run || (cj[k] < run && run <= pool[ids[j0 + k]].chi));
           v += exact ? vj[k] : 1;
           nn += exact ? 0 : 1;
         }
@@ -1809,7 +1842,8 @@ __device__ void push_tile(const KParams& kp, int p, int t, int queue, int wave, 
       for (int k = 0; k < 8; ++k) {
         chat[k] = run;
         run = mj[k] > run ? mj[k] : run;
-        const bool exact = ran[k] && cj[k] == chat[k];
+        const bool exact =
+            ran[k] && (cj[k] == chat[k] || (cj[k] < chat[k] && chat[k] <= pool[ids[j0 + k]].chi));
         vj[k] = (j0 + k < hi) ? (exact ? vj[k] : 1) : 0;
         need[k] = (j0 + k < hi) && !exact;
         vsum += vj[k];
@@ -2378,7 +2412,8 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
       if (topk) run = C;  // improvers end the tile (below)
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        ok[k] = pc[k] == 1 && cu[k] == run;
+        ok[k] = pc[k] == 1 && (cu[k] == run || (!topk && cu[k] < run &&
+                                                 run <= pool[ids_out[i + r0 + k]].chi));
         if (topk && ok[k] && mm[k] > C)  // an improver is exact only with the front's vector
           ok[k] = same_state(crec[ids_out[i + r0 + k]], S);
         if (pc[k] == 1 && !topk) run = mm[k] > run ? mm[k] : run;
@@ -3047,16 +3082,16 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
           rec->ntin = item.ntv;
         }
         __syncwarp();
-#define HPK_RUN4(TK, DR, PF, NS, WS, TKV, FL, REC)                                         \
-  run_segment<TK, DR, PF, NS>(PV, E, E, C, item.cap, WS, lane, kp.err, kp.deadline_slot,   \
+#define HPK_RUN4(TK, DR, PF, NS, CI_, WS, TKV, FL, REC)                                      \
+  run_segment<TK, DR, PF, NS, CI_>(PV, E, E, C, item.cap, WS, lane, kp.err, kp.deadline_slot,   \
                               (kp.trace >= 2 && kp.trace < 5) ? kp.prof : nullptr,          \
                               stoppable ? kp.stop : nullptr, TKV, FL, REC)
 // one lane slot while every node holds <= 32 groups (always for <= 32 units;
 // a run that meets more is redone with two slots)
-#define HPK_RUN3(TK, DR, PF, WS, TKV, FL, REC)                                             \
+#define HPK_RUN3(TK, DR, PF, CI_, WS, TKV, FL, REC)                                        \
   [&]() {                                                                                  \
     if (MAXN <= 64) {                                                                      \
-      RunOut r1 = HPK_RUN4(TK, DR, PF, 1, WS, TKV, FL, REC);                               \
+      RunOut r1 = HPK_RUN4(TK, DR, PF, 1, CI_, WS, TKV, FL, REC);                          \
       if (!r1.retry) return r1;                                                            \
       if (TK) { /* the entering top-k state again: the first try moved it */               \
         if (lane < KW) (WS)->T[lane] = item.tv[lane];                                      \
@@ -3064,18 +3099,26 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
         __syncwarp();                                                                      \
       }                                                                                    \
     }                                                                                      \
-    return HPK_RUN4(TK, DR, PF, 2, WS, TKV, FL, REC);                                      \
+    return HPK_RUN4(TK, DR, PF, 2, CI_, WS, TKV, FL, REC);                                 \
   }()
-#define HPK_RUN(TK, DR, WS, TKV, FL, REC)                                                  \
-  (E->kind == KIND_PREFIX ? HPK_RUN3(TK, DR, true, WS, TKV, FL, REC)                       \
-                          : HPK_RUN3(TK, DR, false, WS, TKV, FL, REC))
+#define HPK_RUN(TK, DR, CI_, WS, TKV, FL, REC)                                             \
+  (E->kind == KIND_PREFIX ? HPK_RUN3(TK, DR, true, CI_, WS, TKV, FL, REC)                  \
+                          : HPK_RUN3(TK, DR, false, CI_, WS, TKV, FL, REC))
         // the drift-checking instantiation only for problems outside the
         // exact-sum contract: the common case carries no extra instructions
-        o = PV.check_drift ? HPK_RUN(true, true, ws, tk, S.seed_obj, rec)
-                           : HPK_RUN(true, false, ws, tk, S.seed_obj, rec);
+        o = PV.check_drift ? HPK_RUN(true, true, false, ws, tk, S.seed_obj, rec)
+                           : HPK_RUN(true, false, false, ws, tk, S.seed_obj, rec);
       } else {
-        o = PV.check_drift ? HPK_RUN(false, true, wsm + warp, 1, 0.0, nullptr)
-                           : HPK_RUN(false, false, wsm + warp, 1, 0.0, nullptr);
+        // k = 1 runs of a latency-bound launch (few problems) record their
+        // cutoff interval; drift-checked problems keep the exact-cutoff rule
+#if HPK_CUT_IV_MAX > 0
+        o = PV.check_drift ? HPK_RUN(false, true, false, wsm + warp, 1, 0.0, nullptr)
+            : kp.cut_iv    ? HPK_RUN(false, false, true, wsm + warp, 1, 0.0, nullptr)
+                           : HPK_RUN(false, false, false, wsm + warp, 1, 0.0, nullptr);
+#else
+        o = PV.check_drift ? HPK_RUN(false, true, false, wsm + warp, 1, 0.0, nullptr)
+                           : HPK_RUN(false, false, false, wsm + warp, 1, 0.0, nullptr);
+#endif
 #undef HPK_RUN
 #undef HPK_RUN3
 #undef HPK_RUN4
@@ -3098,6 +3141,7 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
         E->finished = 1;
         E->has_best = o.has_best ? 1 : 0;
         E->best_obj = o.best_obj;
+        E->chi = __double2float_rd(o.hi);
         E->best_G = o.best_G;
         E->m = o.m;
         E->a_star = o.a_star;
@@ -4371,6 +4415,7 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
     kp.stop = c.active + 7;
     kp.runners = WARPS_PER_BLOCK;
     kp.ranges = ranges;
+    kp.cut_iv = P <= HPK_CUT_IV_MAX ? 1 : 0;
     // run-phase time slice: 300 us (HPK_WAVE_US overrides; 0 = none)
     kp.wave_ns = HPK_WAVE_NS;
     kp.n_problems = P;
