@@ -137,9 +137,6 @@ struct __align__(16) Entry {
   uint8_t du, dend, kind, finished;
   uint8_t has_best, capped, uncapped;
   uint8_t hi;              // the segment is children [u[du-1], hi] of node u[0..du-1)
-  float chi;               // k = 1: the last run is exact for any entering cutoff in
-                           // [its cutoff, chi] (same decisions, so the same run);
-                           // rounded down, so the float only narrows the interval
 };
 
 struct GState {
@@ -196,6 +193,8 @@ struct TileAgg {
   int nrun, ndel;   // positions with a finished run; PREFIX re-runs that pruned an ancestor
   double mmax;      // max objective over the runs (-1: none)
   double cutc;      // the cutoff every run used (NaN: not all the same / none)
+  double cutx;      // max cutoff the runs used (NaN: none) ...
+  double chimin;    // ... and min of their interval ends: all exact for C in [cutx, chimin]
   long long sumvis; // visits of the runs
   double bobj;      // best candidate of the tile: (obj desc, G asc, position asc); -1: none
   int bG, bidx;
@@ -272,7 +271,7 @@ __device__ __forceinline__ CandRec* cand_ptr(const KParams& kp, int p, int which
 // position, -1 = needs a run), 2 cnt (expansion count), 3 pfirst, 4 info (the
 // run's best_G | 256 has_best | 512 PREFIX re-run that pruned an ancestor)
 __device__ __forceinline__ int* list_arr(const KParams& kp, int p, int buf, int which) {
-  return kp.lists + (((size_t)p * 2 + buf) * 5 + which) * kp.lcap;
+  return kp.lists + (((size_t)p * 2 + buf) * 6 + which) * kp.lcap;
 }
 __device__ __forceinline__ long long* list_vis(const KParams& kp, int p, int buf) {
   return kp.lvis + ((size_t)p * 2 + buf) * kp.lcap;
@@ -1496,6 +1495,7 @@ struct OpAddI {
 // (any other run only depends on the cutoff). At most 16 improvers per pass.
 __device__ void push_items(const KParams& kp, int queue, int p, const int* ids, const int* pran,
                            const long long* pvis, const double* pcut, const double* pm,
+                           const int* pchi,
                            const Entry* pool, int head, int len, double C, int qmax,
                            long long budget_left, long long* shl, double* shd, int* shi,
                            const TileAgg* ag, int nagg, int ashift, SchedSmem* sh, int tk,
@@ -1527,7 +1527,8 @@ __device__ void push_items(const KParams& kp, int queue, int p, const int* ids, 
       while (ta < nagg && ag[ta].ob - ashift + ag[ta].n <= at) ++ta;
       if (ta < nagg && ag[ta].ob - ashift == at) {
         const TileAgg a = ag[ta];
-        if (a.nrun == a.n && a.mmax <= cmax && a.cutc == cmax) {
+        if (a.nrun == a.n && a.mmax <= cmax &&
+            (a.cutc == cmax || (!topk && a.cutx <= cmax && cmax <= a.chimin))) {
           before += a.sumvis;
           base += a.n;
           ++ta;
@@ -1593,8 +1594,9 @@ __device__ void push_items(const KParams& kp, int queue, int p, const int* ids, 
       for (int k = 0; k < 8; ++k) {
         chat[k] = run;
         if (!topk) run = mj[k] > run ? mj[k] : run;
-        bool exact = ran[k] && (cj[k] == chat[k] || (!topk && cj[k] < chat[k] &&
-                                                     chat[k] <= pool[ids[head + j0 + k]].chi));
+        bool exact = ran[k] && (cj[k] == chat[k] ||
+                                (!topk && cj[k] < chat[k] &&
+                                 chat[k] <= __int_as_float(pchi[head + j0 + k])));
         if (topk && exact && j0 + k - base == fi_rel) {  // the improver: compare the vectors
           const CandRec& r = crec[ids[head + j0 + k]];
           bool same = r.ntin == sh->ntv;
@@ -1726,12 +1728,14 @@ __device__ void push_tile(const KParams& kp, int p, int t, int queue, int wave, 
   const long long* pvis = list_vis(kp, p, cur);
   const double* pcut = list_dbl(kp, p, cur, 0);
   const double* pm = list_dbl(kp, p, cur, 1);
+  const int* pchi = list_arr(kp, p, cur, 5);
   const Entry* pool = pool_ptr(kp, p, S.pool_cur);
   // pass 1: needs and lower-bound visits of the tile
   long long tvis = 0;
   int tneed = 0;
   const bool whole = lo == tlo && hi == tlo + a.n;
-  if (whole && a.nrun == a.n && a.mmax <= cin && a.cutc == cin) {
+  if (whole && a.nrun == a.n && a.mmax <= cin &&
+      (a.cutc == cin || (a.cutx <= cin && cin <= a.chimin))) {
     tvis = a.sumvis;  // every run exact under the predicted cutoff
   } else {
     double cmax = cin;
@@ -1760,7 +1764,7 @@ __device__ void push_tile(const KParams& kp, int p, int t, int queue, int wave, 
       for (int k = 0; k < 8; ++k) {
         if (j0 + k < hi) {
           const bool exact =
-              ran[k] && (cj[k] == run || (cj[k] < run && run <= pool[ids[j0 + k]].chi));
+              ran[k] && (cj[k] == run || (cj[k] < run && run <= __int_as_float(pchi[j0 + k])));
           v += exact ? vj[k] : 1;
           nn += exact ? 0 : 1;
         }
@@ -1843,7 +1847,8 @@ __device__ void push_tile(const KParams& kp, int p, int t, int queue, int wave, 
         chat[k] = run;
         run = mj[k] > run ? mj[k] : run;
         const bool exact =
-            ran[k] && (cj[k] == chat[k] || (cj[k] < chat[k] && chat[k] <= pool[ids[j0 + k]].chi));
+            ran[k] &&
+            (cj[k] == chat[k] || (cj[k] < chat[k] && chat[k] <= __int_as_float(pchi[j0 + k])));
         vj[k] = (j0 + k < hi) ? (exact ? vj[k] : 1) : 0;
         need[k] = (j0 + k < hi) && !exact;
         vsum += vj[k];
@@ -1937,8 +1942,10 @@ struct AggAcc {
   int nrun, ndel;
   long long sumvis;
   double mmax, cmin, cmax, bo;
+  float chimin;
   int bg, bi;
   __device__ void init() {
+    chimin = INFINITY;
     nrun = 0;
     ndel = 0;
     sumvis = 0;
@@ -1949,8 +1956,10 @@ struct AggAcc {
     bg = 0;
     bi = 0x7fffffff;
   }
-  __device__ void add(int pc, int inf, long long vis, double cut, double m, double bobj, int pos) {
+  __device__ void add(int pc, int inf, long long vis, double cut, double m, double bobj, int pos,
+                      float chi) {
     if (pc != 1) return;
+    chimin = chi < chimin ? chi : chimin;
     ++nrun;
     ndel += (inf & 512) ? 1 : 0;
     sumvis += vis;
@@ -1973,6 +1982,7 @@ struct AggAcc {
     mmax = o.mmax > mmax ? o.mmax : mmax;
     cmin = o.cmin < cmin ? o.cmin : cmin;
     cmax = o.cmax > cmax ? o.cmax : cmax;
+    chimin = o.chimin < chimin ? o.chimin : chimin;
     if (o.bo >= 0 && (bo < 0 || key_better(o.bo, o.bg, o.bi, bo, bg, bi))) {
       bo = o.bo;
       bg = o.bg;
@@ -1987,6 +1997,7 @@ struct AggAcc {
     o.mmax = __shfl_xor_sync(HPK_FULL_MASK, mmax, off);
     o.cmin = __shfl_xor_sync(HPK_FULL_MASK, cmin, off);
     o.cmax = __shfl_xor_sync(HPK_FULL_MASK, cmax, off);
+    o.chimin = __shfl_xor_sync(HPK_FULL_MASK, chimin, off);
     o.bo = __shfl_xor_sync(HPK_FULL_MASK, bo, off);
     o.bg = __shfl_xor_sync(HPK_FULL_MASK, bg, off);
     o.bi = __shfl_xor_sync(HPK_FULL_MASK, bi, off);
@@ -2012,6 +2023,8 @@ __device__ void write_tile_agg(AggAcc acc, TileAgg* out, int ob, int n, SchedSme
     a.mmax = acc.mmax;
     a.cutc = (acc.nrun > 0 && acc.cmin == acc.cmax) ? acc.cmin
                                                      : __longlong_as_double(0x7ff8000000000000LL);
+    a.cutx = acc.nrun > 0 ? acc.cmax : __longlong_as_double(0x7ff8000000000000LL);
+    a.chimin = (double)acc.chimin;
     a.sumvis = acc.sumvis;
     a.bobj = acc.bo;
     a.bG = acc.bg;
@@ -2037,6 +2050,7 @@ __device__ void expand_tile(const KParams& kp, int p, int t, SchedSmem* sh) {
   const int* __restrict__ cnt_i = list_arr(kp, p, cur, 2) + head + lo;
   const int* __restrict__ pf_i = list_arr(kp, p, cur, 3) + head + lo;
   const int* __restrict__ inf_i = list_arr(kp, p, cur, 4) + head + lo;
+  const int* __restrict__ chi_i = list_arr(kp, p, cur, 5) + head + lo;
   const long long* __restrict__ vis_i = list_vis(kp, p, cur) + head + lo;
   const double* __restrict__ cut_i = list_dbl(kp, p, cur, 0) + head + lo;
   const double* __restrict__ m_i = list_dbl(kp, p, cur, 1) + head + lo;
@@ -2046,6 +2060,7 @@ __device__ void expand_tile(const KParams& kp, int p, int t, SchedSmem* sh) {
   int* __restrict__ pcv_o = list_arr(kp, p, cur ^ 1, 1) + ob;
   int* __restrict__ cnt_o = list_arr(kp, p, cur ^ 1, 2) + ob;
   int* __restrict__ inf_o = list_arr(kp, p, cur ^ 1, 4) + ob;
+  int* __restrict__ chi_o = list_arr(kp, p, cur ^ 1, 5) + ob;
   long long* __restrict__ vis_o = list_vis(kp, p, cur ^ 1) + ob;
   double* __restrict__ cut_o = list_dbl(kp, p, cur ^ 1, 0) + ob;
   double* __restrict__ m_o = list_dbl(kp, p, cur ^ 1, 1) + ob;
@@ -2056,18 +2071,19 @@ __device__ void expand_tile(const KParams& kp, int p, int t, SchedSmem* sh) {
   if (xtt == 0) {  // no split in this tile: shifted copy
 #pragma unroll 4
     for (int i = tid; i < n; i += blockDim.x) {
-      const int id = ids_i[i], pc = pcv_i[i], inf = inf_i[i];
+      const int id = ids_i[i], pc = pcv_i[i], inf = inf_i[i], ch = chi_i[i];
       const long long vv = vis_i[i];
       const double cu = cut_i[i], mm = m_i[i], bb = bo_i[i];
       ids_o[i] = id;
       pcv_o[i] = pc;
       inf_o[i] = inf;
+      chi_o[i] = ch;
       vis_o[i] = vv;
       cut_o[i] = cu;
       m_o[i] = mm;
       bo_o[i] = bb;
       cnt_o[i] = 1;
-      acc.add(pc, inf, vv, cu, mm, bb, ob + i);
+      acc.add(pc, inf, vv, cu, mm, bb, ob + i, __int_as_float(ch));
     }
     write_tile_agg(acc, kp.agg + (size_t)p * kp.xtn + t, ob, n, sh);
     return;
@@ -2078,7 +2094,7 @@ __device__ void expand_tile(const KParams& kp, int p, int t, SchedSmem* sh) {
   const int* __restrict__ o_ = off;
   // 4 consecutive inputs per thread, all loads issued before the stores
   for (int i0 = tid * 4; i0 < n; i0 += blockDim.x * 4) {
-    int o[5], id[4], pc[4], inf[4];
+    int o[5], id[4], pc[4], inf[4], ch[4];
     long long vv[4];
     double cu[4], mm[4], bb[4];
 #pragma unroll
@@ -2089,6 +2105,7 @@ __device__ void expand_tile(const KParams& kp, int p, int t, SchedSmem* sh) {
       id[k] = ids_i[i];
       pc[k] = pcv_i[i];
       inf[k] = inf_i[i];
+      ch[k] = chi_i[i];
       vv[k] = vis_i[i];
       cu[k] = cut_i[i];
       mm[k] = m_i[i];
@@ -2101,12 +2118,13 @@ __device__ void expand_tile(const KParams& kp, int p, int t, SchedSmem* sh) {
         ids_o[q] = id[k];
         pcv_o[q] = pc[k];
         inf_o[q] = inf[k];
+        chi_o[q] = ch[k];
         vis_o[q] = vv[k];
         cut_o[q] = cu[k];
         m_o[q] = mm[k];
         bo_o[q] = bb[k];
         cnt_o[q] = 1;
-        acc.add(pc[k], inf[k], vv[k], cu[k], mm[k], bb[k], ob + q);
+        acc.add(pc[k], inf[k], vv[k], cu[k], mm[k], bb[k], ob + q, __int_as_float(ch[k]));
         const int c = o[k + 1] - q;
         if (c > 1) {
           const int pf = pf_i[i0 + k];
@@ -2114,6 +2132,7 @@ __device__ void expand_tile(const KParams& kp, int p, int t, SchedSmem* sh) {
             ids_o[q + tt] = pf + tt - 1;
             pcv_o[q + tt] = -1;
             inf_o[q + tt] = 0;
+            chi_o[q + tt] = 0;
             vis_o[q + tt] = 0;
             cut_o[q + tt] = -1.0;
             m_o[q + tt] = -1.0;
@@ -2160,6 +2179,8 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
   double* m_out = list_dbl(kp, p, cur ^ 1, 1);
   int* inf_in = list_arr(kp, p, cur, 4);
   int* inf_out = list_arr(kp, p, cur ^ 1, 4);
+  int* chi_in = list_arr(kp, p, cur, 5);
+  int* chi_out = list_arr(kp, p, cur ^ 1, 5);
   double* bo_in = list_dbl(kp, p, cur, 2);
   double* bo_out = list_dbl(kp, p, cur ^ 1, 2);
   Entry* pool = pool_ptr(kp, p, S.pool_cur);
@@ -2248,6 +2269,7 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
       const int* __restrict__ ids_i = ids_in + head;
       const int* __restrict__ pcv_i = pcv_in + head;
       const int* __restrict__ inf_i = inf_in + head;
+      const int* __restrict__ chi_i = chi_in + head;
       const int* __restrict__ pf_i = pf_in + head;
       const long long* __restrict__ vis_i = vis_in + head;
       const double* __restrict__ cut_i = cut_in + head;
@@ -2256,6 +2278,7 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
       int* __restrict__ ids_o = ids_out;
       int* __restrict__ pcv_o = pcv_out;
       int* __restrict__ inf_o = inf_out;
+      int* __restrict__ chi_o = chi_out;
       int* __restrict__ cnt_o = cnt_out;
       long long* __restrict__ vis_o = vis_out;
       double* __restrict__ cut_o = cut_out;
@@ -2263,7 +2286,7 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
       double* __restrict__ bo_o = bo_out;
       // run region: 4 consecutive inputs per thread, all loads issued before the stores
       for (int i0 = tid * 4; i0 < mr; i0 += blockDim.x * 4) {
-        int o[5], id[4], pc[4], inf[4];
+        int o[5], id[4], pc[4], inf[4], ch[4];
         long long vv[4];
         double cu[4], mm[4], bb[4];
   #pragma unroll
@@ -2274,6 +2297,7 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
           id[k] = ids_i[i];
           pc[k] = pcv_i[i];
           inf[k] = inf_i[i];
+          ch[k] = chi_i[i];
           vv[k] = vis_i[i];
           cu[k] = cut_i[i];
           mm[k] = m_i[i];
@@ -2286,6 +2310,7 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
             ids_o[q] = id[k];
             pcv_o[q] = pc[k];
             inf_o[q] = inf[k];
+            chi_o[q] = ch[k];
             vis_o[q] = vv[k];
             cut_o[q] = cu[k];
             m_o[q] = mm[k];
@@ -2298,6 +2323,7 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
                 ids_o[q + t] = pf + t - 1;
                 pcv_o[q + t] = -1;
                 inf_o[q + t] = 0;
+                chi_o[q + t] = 0;
                 vis_o[q + t] = 0;
                 cut_o[q + t] = -1.0;
                 m_o[q + t] = -1.0;
@@ -2316,6 +2342,7 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
         ids_o[q] = ids_i[i];
         pcv_o[q] = pcv_i[i];
         inf_o[q] = inf_i[i];
+        chi_o[q] = chi_i[i];
         vis_o[q] = vis_i[i];
         cut_o[q] = cut_i[i];
         m_o[q] = m_i[i];
@@ -2354,7 +2381,8 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
       while (ta < nagg && ag[ta].ob + ag[ta].n <= i) ++ta;
       if (ta < nagg && ag[ta].ob == i) {
         const TileAgg a = ag[ta];
-        if (a.nrun == a.n && a.ndel == 0 && a.mmax <= C && a.cutc == C &&
+        if (a.nrun == a.n && a.ndel == 0 && a.mmax <= C &&
+            (a.cutc == C || (!topk && a.cutx <= C && C <= a.chimin)) &&
             (B < 0 || V + a.sumvis < B) &&
             (!topk || a.bobj < 0 ||
              (S.nbest >= tk && !rank_better(a.bobj, a.bG, S.bl_obj[tk - 1], S.bl_G[tk - 1])))) {
@@ -2387,6 +2415,7 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
     const int r0 = tid * 8;  // this thread's positions, relative to i
     int pc[8], inf[8];
     double cu[8], mm[8];
+    float ch[8];
     long long vv[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -2394,6 +2423,7 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
       const int j = i + (r < tile ? r : 0);
       pc[k] = r < tile ? pcv_out[j] : 0;
       cu[k] = cut_out[j];
+      ch[k] = __int_as_float(chi_out[j]);
       mm[k] = m_out[j];
       vv[k] = vis_out[j];
       inf[k] = inf_out[j];
@@ -2412,8 +2442,7 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
       if (topk) run = C;  // improvers end the tile (below)
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        ok[k] = pc[k] == 1 && (cu[k] == run || (!topk && cu[k] < run &&
-                                                 run <= pool[ids_out[i + r0 + k]].chi));
+        ok[k] = pc[k] == 1 && (cu[k] == run || (!topk && cu[k] < run && run <= ch[k]));
         if (topk && ok[k] && mm[k] > C)  // an improver is exact only with the front's vector
           ok[k] = same_state(crec[ids_out[i + r0 + k]], S);
         if (pc[k] == 1 && !topk) run = mm[k] > run ? mm[k] : run;
@@ -2670,6 +2699,7 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
       cut_in[k] = cut_out[nhead + k];
       m_in[k] = m_out[nhead + k];
       inf_in[k] = inf_out[nhead + k];
+      chi_in[k] = chi_out[nhead + k];
       bo_in[k] = bo_out[nhead + k];
     }
     __syncthreads();
@@ -2680,6 +2710,7 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
       cut_out[k] = cut_in[k];
       m_out[k] = m_in[k];
       inf_out[k] = inf_in[k];
+      chi_out[k] = chi_in[k];
       bo_out[k] = bo_in[k];
       cnt_out[k] = 1;
     }
@@ -2729,7 +2760,7 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
         publish_push(S, 1, wave);
       }
     } else {
-      push_items(kp, next_queue, p, ids_out, pcv_out, vis_out, cut_out, m_out,
+      push_items(kp, next_queue, p, ids_out, pcv_out, vis_out, cut_out, m_out, chi_out,
                  pool_ptr(kp, p, S.pool_cur), nhead, nlen, S.C, qmax, bl, sh->l, sh->d, sh->i,
                  ag, nagg, ashift, sh, P.top_k, S.seed_obj,
                  P.top_k > 1 ? cand_ptr(kp, p, S.pool_cur) : nullptr, S);
@@ -2932,6 +2963,7 @@ __device__ void init_problem(const KParams& kp, int p) {
       list_dbl(kp, p, 0, 1)[0] = -1.0;
       list_dbl(kp, p, 0, 2)[0] = -1.0;
       list_arr(kp, p, 0, 4)[0] = 0;
+      list_arr(kp, p, 0, 5)[0] = 0;
       list_arr(kp, p, 0, 0)[0] = 0;   // id
       list_arr(kp, p, 0, 1)[0] = -1;  // needs a run
       list_arr(kp, p, 0, 2)[0] = 1;
@@ -3141,7 +3173,6 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
         E->finished = 1;
         E->has_best = o.has_best ? 1 : 0;
         E->best_obj = o.best_obj;
-        E->chi = __double2float_rd(o.hi);
         E->best_G = o.best_G;
         E->m = o.m;
         E->a_star = o.a_star;
@@ -3157,6 +3188,7 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
           list_dbl(kp, p, S.cur, 0)[item.pos] = C;
           list_dbl(kp, p, S.cur, 1)[item.pos] = o.m;
           list_dbl(kp, p, S.cur, 2)[item.pos] = o.best_obj;
+          list_arr(kp, p, S.cur, 5)[item.pos] = __float_as_int(__double2float_rd(o.hi));
           list_arr(kp, p, S.cur, 4)[item.pos] =
               o.best_G | (o.has_best ? 256 : 0) |
               ((E->kind == KIND_PREFIX && o.a_star >= 0) ? 512 : 0);
@@ -4315,7 +4347,7 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
     int lcap = cfg.max_list > 0 ? cfg.max_list : (1 << 17);
     int pcap = 2 * lcap;
     while (lcap > 4096 &&
-           (size_t)P * ((size_t)pcap * 2 * entry_bytes + (size_t)lcap * 100) > ((size_t)4 << 30)) {
+           (size_t)P * ((size_t)pcap * 2 * entry_bytes + (size_t)lcap * 108) > ((size_t)4 << 30)) {
       lcap /= 2;
       pcap /= 2;
     }
@@ -4353,7 +4385,7 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
     if (int rc = grow(c.pools, c.cap_pools, (size_t)P * 2 * pcap)) return rc;
     if (any_topk)
       if (int rc = grow(c.cands, c.cap_cands, (size_t)P * 2 * pcap)) return rc;
-    if (int rc = grow(c.lists, c.cap_lists, (size_t)P * 2 * 5 * lcap)) return rc;
+    if (int rc = grow(c.lists, c.cap_lists, (size_t)P * 2 * 6 * lcap)) return rc;
     if (int rc = grow(c.scratch, c.cap_scratch, (size_t)P * (lcap + 1))) return rc;
     if (int rc = grow(c.lvis, c.cap_lvis, (size_t)P * 2 * lcap)) return rc;
     if (int rc = grow(c.ldbl, c.cap_ldbl, (size_t)P * 6 * lcap)) return rc;
