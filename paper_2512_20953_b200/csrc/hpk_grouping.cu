@@ -717,7 +717,8 @@ __device__ RunOut run_segment(const PView& P, const Entry* E, Entry* Eout, doubl
   o.retry = false;
   o.drift = false;
   o.hi = INFINITY;
-  // Cutoff interval (k = 1). A larger entering cutoff C' only changes a run
+  // Cutoff interval (k = 1, and top_k > 1 runs that find no leaf above their
+  // entering cutoff: their cutoff stays that scalar). A larger entering cutoff C' only changes a run
   // through a child or node check that PASSED: a prune stays a prune, leaves
   // are not pruned and the run's own improvements raise both cutoffs alike. So
   // the run is the same for every C' <= each passed check's value — hl keeps
@@ -1595,7 +1596,7 @@ __device__ void push_items(const KParams& kp, int queue, int p, const int* ids, 
         chat[k] = run;
         if (!topk) run = mj[k] > run ? mj[k] : run;
         bool exact = ran[k] && (cj[k] == chat[k] ||
-                                (!topk && cj[k] < chat[k] &&
+                                (cj[k] < chat[k] && (!topk || mj[k] <= cj[k]) &&
                                  chat[k] <= __int_as_float(pchi[head + j0 + k])));
         if (topk && exact && j0 + k - base == fi_rel) {  // the improver: compare the vectors
           const CandRec& r = crec[ids[head + j0 + k]];
@@ -2442,7 +2443,10 @@ __device__ void schedule_problem(const KParams& kp, int p, int next_queue, void*
       if (topk) run = C;  // improvers end the tile (below)
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        ok[k] = pc[k] == 1 && (cu[k] == run || (!topk && cu[k] < run && run <= ch[k]));
+        // (top_k > 1: only a run that found no leaf above its entering cutoff
+        // depends on that scalar alone; an improver needs the front's vector)
+        ok[k] = pc[k] == 1 &&
+                (cu[k] == run || (cu[k] < run && run <= ch[k] && (!topk || mm[k] <= cu[k])));
         if (topk && ok[k] && mm[k] > C)  // an improver is exact only with the front's vector
           ok[k] = same_state(crec[ids_out[i + r0 + k]], S);
         if (pc[k] == 1 && !topk) run = mm[k] > run ? mm[k] : run;
@@ -3138,8 +3142,14 @@ __global__ void HPK_WAVE_BOUNDS hpk_wave_kernel(KParams kp) {
                           : HPK_RUN3(TK, DR, false, CI_, WS, TKV, FL, REC))
         // the drift-checking instantiation only for problems outside the
         // exact-sum contract: the common case carries no extra instructions
+#if HPK_CUT_IV_MAX > 0
+        o = PV.check_drift ? HPK_RUN(true, true, false, ws, tk, S.seed_obj, rec)
+            : kp.cut_iv    ? HPK_RUN(true, false, true, ws, tk, S.seed_obj, rec)
+                           : HPK_RUN(true, false, false, ws, tk, S.seed_obj, rec);
+#else
         o = PV.check_drift ? HPK_RUN(true, true, false, ws, tk, S.seed_obj, rec)
                            : HPK_RUN(true, false, false, ws, tk, S.seed_obj, rec);
+#endif
       } else {
         // k = 1 runs of a latency-bound launch (few problems) record their
         // cutoff interval; drift-checked problems keep the exact-cutoff rule
