@@ -191,6 +191,9 @@ typedef struct hpk_search_config {
   int max_waves;         /* watchdog on the wave loop (0: default 1000000) */
   double max_seconds;    /* device wall-clock watchdog (0: derived from the budgets) */
   int max_ctas;          /* wave-engine grid cap (0: every SM, 2 CTAs each) */
+  int cut_intervals;     /* runs are accepted for any exact entering cutoff in their
+                            recorded interval: -1 auto (launches of at
+                            most 16 searches), 0 off (exact-cutoff rule), 1 on */
 } hpk_search_config;
 
 void hpk_search_config_init(hpk_search_config* cfg);

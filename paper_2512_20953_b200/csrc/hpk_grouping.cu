@@ -4006,6 +4006,7 @@ void hpk_search_config_init(hpk_search_config* cfg) {
   cfg->max_waves = 0;
   cfg->max_seconds = 0;
   cfg->max_ctas = 0;
+  cfg->cut_intervals = -1;
 }
 
 void hpk_last_timing(hpk_timing* out) {
@@ -4457,7 +4458,7 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
     kp.stop = c.active + 7;
     kp.runners = WARPS_PER_BLOCK;
     kp.ranges = ranges;
-    kp.cut_iv = P <= HPK_CUT_IV_MAX ? 1 : 0;
+    kp.cut_iv = cfg.cut_intervals < 0 ? (P <= HPK_CUT_IV_MAX ? 1 : 0) : (cfg.cut_intervals != 0);
     // run-phase time slice: 300 us (HPK_WAVE_US overrides; 0 = none)
     kp.wave_ns = HPK_WAVE_NS;
     kp.n_problems = P;

@@ -63,6 +63,7 @@ class hpk_search_config(C.Structure):
         ("max_waves", C.c_int),
         ("max_seconds", C.c_double),
         ("max_ctas", C.c_int),
+        ("cut_intervals", C.c_int),
     ]
 
 
@@ -263,7 +264,7 @@ class Engine:
                         segment_cap: int = 0, max_list: int = 0,
                         force_serial: bool = False, max_waves: int = 0,
                         max_seconds: float = 0.0, enumeration: bool = False,
-                        max_ctas: int = 0) -> List[GroupingResult]:
+                        max_ctas: int = 0, cut_intervals: int = -1) -> List[GroupingResult]:
         n = len(problems)
         arr = (hpk_grouping_problem * n)()
         res = (hpk_grouping_result * n)()
@@ -293,6 +294,7 @@ class Engine:
         cfg.max_waves = max_waves
         cfg.max_seconds = max_seconds
         cfg.max_ctas = max_ctas
+        cfg.cut_intervals = cut_intervals
         rc = self.lib.hpk_grouping_search(arr, n, res, C.byref(cfg))
         if rc != 0:
             raise EngineError(rc, self.lib.hpk_last_error().decode())

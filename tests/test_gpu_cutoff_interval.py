@@ -1,0 +1,125 @@
+"""Cutoff intervals: a run is accepted for any exact entering
+cutoff in [C, chi], chi bounded by the values its passed checks compared with
+the cutoff. These tests force the rule on where the default leaves it off (big
+launches), compare every result with the oracle / the reference-pinned goldens,
+and show the rule is live (fewer runs for the same exact answer)."""
+import json
+import math
+import os
+import random
+
+import pytest
+
+from paper_2512_20953_b200 import configs
+from paper_2512_20953_b200.configs import min_mem_for, units_for
+from paper_2512_20953_b200.engine import GroupingProblem
+
+pytestmark = pytest.mark.gpu
+
+
+def _same(r, o):
+    if o.status != 0:
+        return r.status == o.status
+    return (r.status == 0 and r.count == o.count and r.rgs == o.rgs
+            and r.objective == o.objective and r.z == o.z and r.visited == o.visited
+            and r.optimal == o.optimal)
+
+
+def _random_problems(seed, count, nmax, top_ks):
+    # the generator of test_gpu_grouping.py (ties, dyadic powers, budgets 0..20000)
+    rng = random.Random(seed)
+    out = []
+    for t in range(count):
+        topk = rng.choice(top_ks)
+        n = rng.randint(1, nmax)
+        if t % 5 == 0:
+            P = [2.0] * n
+            M = [8.0] * n
+        else:
+            P = [rng.choice([0.5, 1.0, 1.5, 2.0, 3.0]) for _ in range(n)]
+            M = [float(rng.randint(4, 20)) for _ in range(n)]
+        T = [int(p * 2) for p in P]
+        N = sorted(rng.randint(0, 3) for _ in range(n))
+        K = rng.randint(1, 16)
+        MIN = sum(M) * rng.uniform(0.1, 0.9) / rng.randint(1, 4)
+        if rng.random() < 0.5:
+            MIN = float(round(MIN))
+        thr = rng.choice([0, 4, 8])
+        B = rng.choice([0, 1, 2, 17, 300, 3000, 20000])
+        out.append(GroupingProblem(P, M, K, MIN, T, N, thr, B, topk))
+    return out
+
+
+def _config_problems(name, top_k=1):
+    w = configs.get(name)
+    g = 0
+    for nd in w.cluster["nodes"]:
+        g = math.gcd(g, nd["count"])
+    probs = []
+    for tp in [t for t in range(1, g + 1) if g % t == 0]:
+        P, M, T, N = units_for(w.cluster, tp)
+        probs.append(GroupingProblem(P, M, w.model["n_microbatches"], min_mem_for(w.model), T, N,
+                                     top_k=top_k))
+    return probs
+
+
+@pytest.mark.parametrize("cap,top_ks", [(3, (1,)), (64, (1,)), (2048, (1,)),
+                                        (3, (2, 3, 8, 16)), (64, (2, 4, 13))])
+def test_random_batches_with_intervals_forced_on(engine, oracle, cap, top_ks):
+    probs = _random_problems(7000 + cap + len(top_ks), 160, 10 if cap < 16 else 11, top_ks)
+    res = engine.grouping_search(probs, segment_cap=cap, max_seconds=60, cut_intervals=1)
+    bad = []
+    for pb, r in zip(probs, res):
+        o = oracle.solve_grouping(pb.power, pb.memory, pb.n_microbatches, pb.min_mem,
+                                  pb.type_key, pb.node_key, pb.exact_threshold, pb.node_budget,
+                                  pb.top_k)
+        if not _same(r, o):
+            bad.append((pb, r.visited, o.visited, r.objective, o.objective))
+    assert not bad, bad[:2]
+
+
+def test_full_cfg5_sweep_with_intervals_forced_on(engine):
+    """All 1167 searches of the sweep in one launch with the interval rule on
+    (the default keeps it off for batches): visits, optimal flag, objective and
+    RGS equal the reference-probe goldens (tests/golden/cfg5_search.json)."""
+    with open(os.path.join(os.path.dirname(__file__), "golden", "cfg5_search.json")) as f:
+        golden = json.load(f)
+    probs = []
+    for w in configs.cfg5_snapshots(1000):
+        g = 0
+        for nd in w.cluster["nodes"]:
+            g = math.gcd(g, nd["count"])
+        for tp in [t for t in range(1, g + 1) if g % t == 0]:
+            P, M, T, N = units_for(w.cluster, tp)
+            probs.append(GroupingProblem(P, M, w.model["n_microbatches"], min_mem_for(w.model),
+                                         T, N))
+    assert len(probs) == len(golden)
+    res = engine.grouping_search(probs, max_seconds=120, cut_intervals=1)
+    bad = []
+    for g, r in zip(golden, res):
+        if r.status != g["status"]:
+            bad.append(g)
+            continue
+        if g["status"] != 0:
+            continue
+        if (r.visited, r.optimal, r.objective[0].hex(), "".join(chr(48 + x) for x in r.rgs[0])) \
+                != (g["visited"], g["optimal"], g["objective"], g["rgs"]):
+            bad.append(g)
+    assert not bad, (len(bad), bad[:3])
+
+
+@pytest.mark.parametrize("name,k", [("cfg2", 1), ("cfg3", 1), ("cfg4", 1), ("cfg4", 2),
+                                    ("cfg3", 12)])
+def test_intervals_on_and_off_agree_and_the_rule_is_live(engine, oracle, name, k):
+    """Same exact answer with the rule off (exact-cutoff re-runs) and on; with it
+    on the budgeted searches need fewer runs (stale runs accepted, not re-run)."""
+    probs = _config_problems(name, k)
+    off = engine.grouping_search(probs, max_seconds=60, cut_intervals=0)
+    on = engine.grouping_search(probs, max_seconds=60, cut_intervals=1)
+    for pb, a, b in zip(probs, off, on):
+        o = oracle.solve_grouping(pb.power, pb.memory, pb.n_microbatches, pb.min_mem,
+                                  pb.type_key, pb.node_key, top_k=k)
+        assert _same(a, o) and _same(b, o), (name, k, pb.n)
+    runs_off = sum(r.segment_runs for r in off)
+    runs_on = sum(r.segment_runs for r in on)
+    assert runs_on < runs_off, (runs_on, runs_off)
