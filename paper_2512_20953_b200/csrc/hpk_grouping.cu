@@ -51,6 +51,12 @@ namespace cg = cooperative_groups;
 #ifndef HPK_SEG_CAP
 #define HPK_SEG_CAP 1024      // visits per segment run per wave
 #endif
+#ifndef HPK_SPLIT_ONE_DEVICE
+#define HPK_SPLIT_ONE_DEVICE 1  // run the costliest budgeted search of a small launch
+#endif                          // concurrently with the rest on a share of the SMs
+#ifndef HPK_SPLIT_SHARE
+#define HPK_SPLIT_SHARE 0.5     // its share of the wave-kernel CTA slots
+#endif
 #ifndef HPK_CUT_IV_MAX
 #define HPK_CUT_IV_MAX 16  // launches of at most this many searches use cutoff intervals
 #endif
@@ -3762,7 +3768,7 @@ struct DeviceCtx {
   std::mutex mu;
 };
 
-DeviceCtx g_ctx[16];
+DeviceCtx g_ctx[32];  // [device + 16 * slot]: slot 1 = a concurrent partition (split_device)
 
 thread_local std::string t_err;
 thread_local hpk_timing t_timing;
@@ -4020,7 +4026,7 @@ void hpk_reset_timing(void) { t_timing = hpk_timing{}; }
 namespace hpk {
 
 int search_device(const hpk_grouping_problem* problems, int n_problems,
-                  hpk_grouping_result* results, const hpk_search_config& cfg);
+                  hpk_grouping_result* results, const hpk_search_config& cfg, int slot = 0);
 
 // Relative cost of one search for the device assignment: a budgeted search
 // runs node_budget visits, an exhaustive one Bell(n); deeper searches cost more
@@ -4058,6 +4064,85 @@ void assign_devices(const hpk_grouping_problem* problems, int n, int ndev, int* 
     load[d] += cost[i];
     out[i] = d;
   }
+}
+
+// One device, two concurrent partitions: the costliest budgeted search alone on
+// one share of the SMs, the rest on the other, each a persistent cooperative
+// kernel on its own context slot and stream (the searches are independent).
+int split_device(const hpk_grouping_problem* problems, int n_problems,
+                 hpk_grouping_result* results, const hpk_search_config& cfg, int device,
+                 bool* done) {
+  *done = false;
+  if (n_problems < 2 || n_problems > 16 || cfg.force_serial || cfg.max_ctas > 0) return 0;
+  int big = -1, nbig = 0;
+  double cbig = 0;
+  for (int i = 0; i < n_problems; ++i) {
+    const hpk_grouping_problem& pr = problems[i];
+    if (pr.node_budget <= 0 || pr.n <= pr.exact_threshold || pr.n > MAXN || pr.top_k > KW)
+      continue;  // budgeted wave-engine searches only
+    const double c = search_cost(pr);
+    if (c >= 1e6) ++nbig;
+    if (c > cbig) {
+      cbig = c;
+      big = i;
+    }
+  }
+  if (nbig < 2 || big < 0) return 0;  // one long search: nothing to isolate it from
+  DeviceCtx& c0 = g_ctx[device];
+  {
+    std::lock_guard<std::mutex> lock(c0.mu);
+    if (int rc = ensure_ctx(c0, device)) return rc;
+  }
+  const int slots = c0.sms * c0.blocks_per_sm;
+  const int grid_a = std::max(1, (int)(slots * HPK_SPLIT_SHARE));
+  const int grid_b = slots - grid_a;
+  if (grid_b < 1) return 0;
+  std::vector<int> ia{big}, ib;
+  for (int i = 0; i < n_problems; ++i)
+    if (i != big) ib.push_back(i);
+  std::vector<hpk_grouping_problem> pa, pb;
+  std::vector<hpk_grouping_result> ra, rb;
+  for (int i : ia) {
+    pa.push_back(problems[i]);
+    ra.push_back(results[i]);
+  }
+  for (int i : ib) {
+    pb.push_back(problems[i]);
+    rb.push_back(results[i]);
+  }
+  hpk_search_config ca = cfg, cb = cfg;
+  ca.device = cb.device = device;
+  ca.max_ctas = grid_a;
+  cb.max_ctas = grid_b;
+  int rcb = 0;
+  hpk_timing tb{};
+  std::string eb;
+  std::thread worker([&]() {
+    t_timing = hpk_timing{};
+    rcb = search_device(pb.data(), (int)pb.size(), rb.data(), cb, 1);
+    tb = t_timing;
+    eb = t_err;
+  });
+  const hpk_timing before = t_timing;
+  t_timing = hpk_timing{};
+  const int rca = search_device(pa.data(), (int)pa.size(), ra.data(), ca, 0);
+  const hpk_timing ta = t_timing;
+  worker.join();
+  t_timing = before;
+  t_timing.search_ms += std::max(ta.search_ms, tb.search_ms);
+  t_timing.serial_ms += std::max(ta.serial_ms, tb.serial_ms);
+  t_timing.h2d_bytes += ta.h2d_bytes + tb.h2d_bytes;
+  t_timing.d2h_bytes += ta.d2h_bytes + tb.d2h_bytes;
+  t_timing.kernel_launches += ta.kernel_launches + tb.kernel_launches;
+  if (rca != 0) return rca;
+  if (rcb != 0) {
+    t_err = eb;
+    return rcb;
+  }
+  for (size_t k = 0; k < ia.size(); ++k) results[ia[k]] = ra[k];
+  for (size_t k = 0; k < ib.size(); ++k) results[ib[k]] = rb[k];
+  *done = true;
+  return 0;
 }
 
 // hpk_grouping_search over every visible device: problems go longest-first to
@@ -4149,6 +4234,14 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
     if (cudaGetDevice(&d) != cudaSuccess) d = 0;
     cfg.device = d;
   }
+  if (HPK_SPLIT_ONE_DEVICE) {
+    bool done = false;
+    if (int rc = split_device(problems, n_problems, results, cfg, cfg.device, &done)) return rc;
+    if (done) {
+      t_timing.devices_used = std::max(t_timing.devices_used, 1);
+      return 0;
+    }
+  }
   const int rc = search_device(problems, n_problems, results, cfg);
   t_timing.devices_used = std::max(t_timing.devices_used, 1);
   return rc;
@@ -4159,14 +4252,14 @@ int hpk_grouping_search(const hpk_grouping_problem* problems, int n_problems,
 namespace hpk {
 
 int search_device(const hpk_grouping_problem* problems, int n_problems,
-                  hpk_grouping_result* results, const hpk_search_config& cfg) {
+                  hpk_grouping_result* results, const hpk_search_config& cfg, int slot) {
   const int ndev = hpk_device_count();
   int device = cfg.device;
   if (device < 0) {
     if (cudaGetDevice(&device) != cudaSuccess) device = 0;
   }
   if (device >= ndev || device >= 16) return fail(6, "hetplan_b200: bad device ordinal");
-  DeviceCtx& c = g_ctx[device];
+  DeviceCtx& c = g_ctx[device + 16 * slot];
   std::lock_guard<std::mutex> lock(c.mu);
   if (int rc = ensure_ctx(c, device)) return rc;
   HPK_CUDA(cudaSetDevice(device));
@@ -4414,7 +4507,8 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
     // small: several per warp keep the warps busy through the time slice)
     // (4 per warp and a 300 us slice: measured best on cfg4 / cfg3 after the
     // parallel queue step; HPK_QMUL / HPK_WAVE_US override)
-    const int qmax = HPK_QMUL * nwarps;
+    const int qmax = HPK_QMUL * (HPK_SPLIT_ONE_DEVICE ? c.sms * c.blocks_per_sm * WARPS_PER_BLOCK
+                                                      : nwarps);
     const int qcap = qmax + 33 * P + 64;
     if (int rc = grow(c.items, c.cap_items, (size_t)2 * qcap)) return rc;
 
@@ -4467,7 +4561,10 @@ int search_device(const hpk_grouping_problem* problems, int n_problems,
     kp.reserve = reserve;
     kp.qcap = qcap;
     kp.qmax = qmax;
-    kp.qmax_one = (int)(HPK_QONE * nwarps);
+    // (a lone search's share is sized by the whole device: a launch on part of
+    // the SMs still runs its long runs side by side, the tiny ones fill in)
+    kp.qmax_one = (int)(HPK_QONE * (HPK_SPLIT_ONE_DEVICE ? c.sms * c.blocks_per_sm * WARPS_PER_BLOCK
+                                                         : nwarps));
     kp.seg_cap = seg_cap;
     kp.front_cap = seg_cap;
     kp.ramp = 64;  // measured: -0.7 ms cfg4, -1.3 ms tp1 alone
