@@ -52,10 +52,10 @@ namespace cg = cooperative_groups;
 #define HPK_SEG_CAP 1024      // visits per segment run per wave
 #endif
 #ifndef HPK_SPLIT_ONE_DEVICE
-#define HPK_SPLIT_ONE_DEVICE 1  // run the costliest budgeted search of a small launch
-#endif                          // concurrently with the rest on a share of the SMs
-#ifndef HPK_SPLIT_SHARE
-#define HPK_SPLIT_SHARE 0.5     // its share of the wave-kernel CTA slots
+#define HPK_SPLIT_ONE_DEVICE 1  // run the long budgeted searches of a small launch
+#endif                          // concurrently, each on a share of the SMs
+#ifndef HPK_SPLIT_MAX
+#define HPK_SPLIT_MAX 2         // partitions (equal shares of the wave-kernel CTA slots)
 #endif
 #ifndef HPK_CUT_IV_MAX
 #define HPK_CUT_IV_MAX 16  // launches of at most this many searches use cutoff intervals
@@ -3768,7 +3768,7 @@ struct DeviceCtx {
   std::mutex mu;
 };
 
-DeviceCtx g_ctx[32];  // [device + 16 * slot]: slot 1 = a concurrent partition (split_device)
+DeviceCtx g_ctx[16 * HPK_SPLIT_MAX];  // [device + 16 * slot]: slots 1.. = concurrent partitions (split_device)
 
 thread_local std::string t_err;
 thread_local hpk_timing t_timing;
@@ -4066,81 +4066,91 @@ void assign_devices(const hpk_grouping_problem* problems, int n, int ndev, int* 
   }
 }
 
-// One device, two concurrent partitions: the costliest budgeted search alone on
-// one share of the SMs, the rest on the other, each a persistent cooperative
-// kernel on its own context slot and stream (the searches are independent).
+// One device, concurrent partitions: each long budgeted search of a small launch
+// (the single-plan, latency-bound case) runs alone as its own persistent
+// cooperative kernel on an equal share of the CTA slots (at most HPK_SPLIT_MAX
+// partitions; shorter searches join the cheapest one), each on its own context
+// slot and stream, one host thread each. The searches are independent: the
+// long pole no longer waits for the others' schedule phases.
 int split_device(const hpk_grouping_problem* problems, int n_problems,
                  hpk_grouping_result* results, const hpk_search_config& cfg, int device,
                  bool* done) {
   *done = false;
   if (n_problems < 2 || n_problems > 16 || cfg.force_serial || cfg.max_ctas > 0) return 0;
-  int big = -1, nbig = 0;
-  double cbig = 0;
+  std::vector<std::pair<double, int>> big;
   for (int i = 0; i < n_problems; ++i) {
     const hpk_grouping_problem& pr = problems[i];
     if (pr.node_budget <= 0 || pr.n <= pr.exact_threshold || pr.n > MAXN || pr.top_k > KW)
       continue;  // budgeted wave-engine searches only
     const double c = search_cost(pr);
-    if (c >= 1e6) ++nbig;
-    if (c > cbig) {
-      cbig = c;
-      big = i;
-    }
+    if (c >= 1e6) big.push_back({-c, i});
   }
-  if (nbig < 2 || big < 0) return 0;  // one long search: nothing to isolate it from
+  if (big.size() < 2) return 0;  // one long search: nothing to isolate it from
+  std::sort(big.begin(), big.end());
+  const int K = std::min((int)big.size(), HPK_SPLIT_MAX);
   DeviceCtx& c0 = g_ctx[device];
   {
     std::lock_guard<std::mutex> lock(c0.mu);
     if (int rc = ensure_ctx(c0, device)) return rc;
   }
   const int slots = c0.sms * c0.blocks_per_sm;
-  const int grid_a = std::max(1, (int)(slots * HPK_SPLIT_SHARE));
-  const int grid_b = slots - grid_a;
-  if (grid_b < 1) return 0;
-  std::vector<int> ia{big}, ib;
-  for (int i = 0; i < n_problems; ++i)
-    if (i != big) ib.push_back(i);
-  std::vector<hpk_grouping_problem> pa, pb;
-  std::vector<hpk_grouping_result> ra, rb;
-  for (int i : ia) {
-    pa.push_back(problems[i]);
-    ra.push_back(results[i]);
+  if (slots / K < 1) return 0;
+  std::vector<std::vector<int>> part(K);
+  std::vector<double> pcost(K, 0.0);
+  std::vector<char> placed(n_problems, 0);
+  for (int k = 0; k < K; ++k) {
+    part[k].push_back(big[k].second);
+    pcost[k] = -big[k].first;
+    placed[big[k].second] = 1;
   }
-  for (int i : ib) {
-    pb.push_back(problems[i]);
-    rb.push_back(results[i]);
+  for (int i = 0; i < n_problems; ++i) {  // the rest: to the cheapest partition
+    if (placed[i]) continue;
+    const int k = (int)(std::min_element(pcost.begin(), pcost.end()) - pcost.begin());
+    part[k].push_back(i);
+    pcost[k] += search_cost(problems[i]);
   }
-  hpk_search_config ca = cfg, cb = cfg;
-  ca.device = cb.device = device;
-  ca.max_ctas = grid_a;
-  cb.max_ctas = grid_b;
-  int rcb = 0;
-  hpk_timing tb{};
-  std::string eb;
-  std::thread worker([&]() {
+  std::vector<std::vector<hpk_grouping_problem>> pp(K);
+  std::vector<std::vector<hpk_grouping_result>> rr(K);
+  std::vector<hpk_timing> tt(K);
+  std::vector<std::string> ee(K);
+  std::vector<int> rc(K, 0);
+  for (int k = 0; k < K; ++k)
+    for (int i : part[k]) {
+      pp[k].push_back(problems[i]);
+      rr[k].push_back(results[i]);
+    }
+  auto run = [&](int k) {
+    hpk_search_config ck = cfg;
+    ck.device = device;
+    ck.max_ctas = slots / K;
     t_timing = hpk_timing{};
-    rcb = search_device(pb.data(), (int)pb.size(), rb.data(), cb, 1);
-    tb = t_timing;
-    eb = t_err;
-  });
+    rc[k] = search_device(pp[k].data(), (int)pp[k].size(), rr[k].data(), ck, k);
+    tt[k] = t_timing;
+    ee[k] = t_err;
+  };
   const hpk_timing before = t_timing;
-  t_timing = hpk_timing{};
-  const int rca = search_device(pa.data(), (int)pa.size(), ra.data(), ca, 0);
-  const hpk_timing ta = t_timing;
-  worker.join();
+  std::vector<std::thread> workers;
+  for (int k = 1; k < K; ++k) workers.emplace_back(run, k);
+  run(0);
+  for (auto& w : workers) w.join();
   t_timing = before;
-  t_timing.search_ms += std::max(ta.search_ms, tb.search_ms);
-  t_timing.serial_ms += std::max(ta.serial_ms, tb.serial_ms);
-  t_timing.h2d_bytes += ta.h2d_bytes + tb.h2d_bytes;
-  t_timing.d2h_bytes += ta.d2h_bytes + tb.d2h_bytes;
-  t_timing.kernel_launches += ta.kernel_launches + tb.kernel_launches;
-  if (rca != 0) return rca;
-  if (rcb != 0) {
-    t_err = eb;
-    return rcb;
+  double sm = 0, se = 0;
+  for (int k = 0; k < K; ++k) {
+    sm = std::max(sm, tt[k].search_ms);
+    se = std::max(se, tt[k].serial_ms);
+    t_timing.h2d_bytes += tt[k].h2d_bytes;
+    t_timing.d2h_bytes += tt[k].d2h_bytes;
+    t_timing.kernel_launches += tt[k].kernel_launches;
   }
-  for (size_t k = 0; k < ia.size(); ++k) results[ia[k]] = ra[k];
-  for (size_t k = 0; k < ib.size(); ++k) results[ib[k]] = rb[k];
+  t_timing.search_ms += sm;
+  t_timing.serial_ms += se;
+  for (int k = 0; k < K; ++k)
+    if (rc[k] != 0) {
+      t_err = ee[k];
+      return rc[k];
+    }
+  for (int k = 0; k < K; ++k)
+    for (size_t m = 0; m < part[k].size(); ++m) results[part[k][m]] = rr[k][m];
   *done = true;
   return 0;
 }
