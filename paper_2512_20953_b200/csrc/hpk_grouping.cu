@@ -64,7 +64,7 @@ namespace cg = cooperative_groups;
 #define HPK_SEG_CAP_BATCH 2048  // ... for batches of more than 16 searches
 #endif
 #ifndef HPK_WAVE_NS
-#define HPK_WAVE_NS 225000ull // run-phase time slice (A/B 200/225/250/300/400 us on the specialised runner)
+#define HPK_WAVE_NS 275000ull // run-phase time slice (A/B 200/225/250/275 us with the one-device split)
 #endif
 #ifndef HPK_CHECK_EVERY
 #define HPK_CHECK_EVERY 64    // DFS iterations between stop-flag / time-slice checks (A/B: 32/64/128;
